@@ -1,0 +1,175 @@
+/*
+ * spin_c.h -- the C-ABI drop-in boundary of the B200 Spin verification path.
+ *
+ * Plain C types only (pointers, sizes, PODs); no C++ or torch types. Every entry
+ * point returns a spin_status; spin_last_error() holds a thread-local message.
+ * The C++ host layer (include/specsim/ headers) rethrows each status as the
+ * reference's exception type, so reference callers stay unchanged.
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj/core):
+ *   status codes        <- include/specsim/errors.hpp:7-33 (ConfigError .. IoError) + CUDA
+ *   spin_pack           <- include/specsim/packing.hpp:52  pack(kv_lens, width)
+ *   spin_naive_padding  <- include/specsim/packing.hpp:56  naive_padding(kv_lens)
+ *   spin_verify_batch_cost <- include/specsim/slot_engine.hpp:98-99 verify_batch_cost(...)
+ *   spin_decomposed_attention <- include/specsim/attention.hpp:42-44 decomposed_attention(...)
+ *   spin_reference_attention  <- include/specsim/attention.hpp:34 reference_attention(q,k,v)
+ *   spin_ctx_* / spin_prefill / spin_round <- include/specsim/slot_engine.hpp:50-88
+ *        SlotEngine ctor + run_slot (speculate -> verify -> accept -> update),
+ *        with the Bernoulli draw of src/model.cpp:110-134 replaced by real greedy
+ *        verification of SSM drafts against the target model.
+ */
+#ifndef SPIN_C_H_
+#define SPIN_C_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPIN_ABI_VERSION 1
+
+typedef enum spin_status {
+  SPIN_OK = 0,
+  SPIN_CONFIG_ERROR = 1,      /* specsim::ConfigError      */
+  SPIN_CAPACITY_ERROR = 2,    /* specsim::CapacityError    */
+  SPIN_INPUT_ERROR = 3,       /* specsim::InputError       */
+  SPIN_SIZE_ERROR = 4,        /* specsim::SizeError        */
+  SPIN_CONSISTENCY_ERROR = 5, /* specsim::ConsistencyError */
+  SPIN_METRIC_ERROR = 6,      /* specsim::MetricError      */
+  SPIN_IO_ERROR = 7,          /* specsim::IoError          */
+  SPIN_CUDA_ERROR = 8         /* device / driver failure (no reference equivalent) */
+} spin_status;
+
+int spin_abi_version(void);
+const char* spin_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * Request decomposition (packing.hpp:10-59, packing.cpp:16-136). Host-side,
+ * bit-identical to the reference's first-fit-decreasing packer.
+ * ---------------------------------------------------------------------- */
+typedef struct spin_segment {
+  int32_t request_id;
+  int32_t row;
+  int32_t col_start;
+  int32_t col_end; /* exclusive */
+  int32_t token_offset;
+} spin_segment;
+
+/* segments must hold seg_cap >= n + min(width, n) - 1 entries (the packer's
+ * bound); q_replica_rows holds n entries. Empty input -> length = rows = 0. */
+spin_status spin_pack(const int32_t* kv_lens, int32_t n, int32_t width, int32_t* length, int32_t* rows,
+                      spin_segment* segments, int32_t seg_cap, int32_t* n_segments, int64_t* padding_tokens,
+                      int32_t* q_replica_rows);
+spin_status spin_naive_padding(const int32_t* kv_lens, int32_t n, int64_t* padding);
+spin_status spin_verify_batch_cost(const int32_t* kv_lens, int32_t n, int32_t window, int32_t packing,
+                                   int32_t pack_width, int64_t* tokens, int64_t* padding);
+
+/* ------------------------------------------------------------------------
+ * Packed (decomposed) attention operator on the GPU. Host buffers in fp64 like
+ * the reference Matrix; computed on the device in fp32 by the same ragged
+ * split-KV kernel family the verifier uses, with scale = 1 and no causal mask
+ * (attention.cpp:67-96 semantics). q/k/v are the per-request matrices
+ * concatenated row-major: q rows sum(q_rows[i]), k/v rows sum(kv_rows[i]).
+ * mask (width*length owner ids, -1 empty) is checked against the layout like
+ * check_layout_consistency (attention.cpp:23-63); pass NULL to skip.
+ * ---------------------------------------------------------------------- */
+spin_status spin_decomposed_attention(int32_t n_req, int32_t dim, const int32_t* q_rows, const int32_t* kv_rows,
+                                      const double* q, const double* k, const double* v, const spin_segment* segs,
+                                      int32_t n_segs, int32_t width, int32_t length, const int32_t* mask,
+                                      double* out);
+spin_status spin_reference_attention(int32_t q_rows, int32_t kv_rows, int32_t dim, const double* q,
+                                     const double* k, const double* v, double* out);
+
+/* ------------------------------------------------------------------------
+ * Verification engine (one context per GPU / process).
+ * ---------------------------------------------------------------------- */
+typedef struct spin_model_desc {
+  int32_t d_model;
+  int32_t n_layers;
+  int32_t n_heads;
+  int32_t head_dim; /* 64 or 128 */
+  int32_t ffn;
+  int32_t vocab;
+  float rope_theta;
+  float rms_eps;
+  uint64_t seed;     /* synthetic weight stream */
+  float embed_scale; /* embedding entries ~ U(-a, a) * embed_scale          */
+  float planted_gain;/* strength of the planted next-token map in lm_head    */
+  float resid_scale; /* o_proj / down_proj scale: block contribution size    */
+  float init_scale;  /* other projections ~ U(-1,1) * init_scale             */
+} spin_model_desc;
+
+typedef struct spin_engine_opts {
+  int32_t device;
+  int32_t max_requests; /* request slots (KV cache rows) */
+  int32_t max_ctx;      /* positions per slot            */
+  int32_t window;       /* gamma                         */
+  int32_t pack_width;   /* 0: batch size (slot_engine.cpp:30-31)            */
+  int32_t packing;      /* 1: decomposed split-KV work list, 0: padded rows */
+  int32_t use_graphs;   /* capture draft/verify in CUDA graphs              */
+  int32_t use_pdl;      /* programmatic dependent launch between kernels    */
+  int32_t debug_logits; /* keep fp32 target logits of the last verify       */
+} spin_engine_opts;
+
+typedef struct spin_ctx spin_ctx;
+
+spin_status spin_ctx_create(const spin_model_desc* target, const spin_model_desc* ssms, int32_t n_ssm,
+                            const spin_engine_opts* opts, spin_ctx** out);
+spin_status spin_ctx_destroy(spin_ctx* ctx);
+
+/* Admits n requests into the given slots and runs the prompt prefill on the
+ * target and every SSM. prompts: concatenated token ids, prompt_lens[i] >= 2.
+ * The last prompt token stays pending (it is the first verify row). */
+spin_status spin_prefill(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* prompt_lens,
+                         const int32_t* prompts);
+
+typedef struct spin_round_out {
+  int32_t* accepted;      /* [n] leading-run length, 0..window          */
+  int32_t* bonus_token;   /* [n] target token after the accepted run    */
+  int32_t* committed;     /* [n] committed tokens after the round       */
+  int32_t* drafts;        /* [n*window] or NULL                         */
+  int32_t* target_tokens; /* [n*(window+1)] target argmax rows or NULL  */
+  float draft_ms;         /* device time: all SSM draft loops           */
+  float verify_ms;        /* device time: pack + verify forward + accept */
+  float round_ms;         /* device time: whole round                   */
+} spin_round_out;
+
+/* One speculation + verification slot for n admitted requests. ssm_of[i] is
+ * the draft model of request i (slots[i]); -1 idles it (not verified). Host
+ * buffers; H2D of the assignment and D2H of the outcome are inside the call. */
+spin_status spin_round(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
+                       spin_round_out* out);
+
+/* Device-resident loop: `rounds` rounds back to back on the current assignment
+ * with no host round trip; per-round accepted+bonus totals land in
+ * emitted[rounds] (host) after the final synchronisation. */
+spin_status spin_run_rounds(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
+                            int32_t rounds, int64_t* emitted, float* device_ms);
+
+/* Committed token history of one slot (prompt + generated). */
+spin_status spin_read_tokens(spin_ctx* ctx, int32_t slot, int32_t* tokens, int32_t cap, int32_t* len);
+/* fp32 target logits of the last verify ([rows, vocab]); needs debug_logits. */
+spin_status spin_read_logits(spin_ctx* ctx, float* logits, int64_t cap, int32_t* rows);
+/* Rebinds a request slot to a different SSM: the SSM's KV for the slot is
+ * recomputed up to the committed prefix (switching_cost, slot_engine.cpp:12-22). */
+spin_status spin_switch_ssm(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of);
+
+/* ------------------------------------------------------------------------
+ * Kernel-level entry points (device pointers; stream = cudaStream_t or NULL).
+ * Used by the parity tests to check each kernel against a reference of the
+ * same op, and by bench.py for the per-kernel roofline.
+ * ---------------------------------------------------------------------- */
+spin_status spin_gemm_info(int32_t n_out, int32_t k, int32_t t, int32_t mode, int32_t* max_pieces,
+                           int32_t* grid, int32_t* bn);
+/* mode 0: part[max_pieces][t][n_out] partial sums (caller zero-fills, sums slots);
+ * mode 1: amax_val/amax_idx [ceil(n_out/128)][t], logits [t][n_out] optional. */
+spin_status spin_gemm(void* stream, const void* w, const void* x, int32_t n_out, int32_t k, int32_t t,
+                      int32_t mode, float* part, float* amax_val, int32_t* amax_idx, float* logits);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPIN_C_H_ */

@@ -1,0 +1,77 @@
+// Weight-streaming projection GEMM for the verify / draft forward passes.
+//
+//   Y[t, n] = sum_k X[t, k] * W[n, k]          X: [T, K] bf16, W: [N_out, K] bf16
+//
+// The weight matrix is the tcgen05 "A" operand (M = 128 output features per
+// tile) and the token batch is the "B" operand (N = token tile, 16..256): at
+// verification batch sizes (T = B*(gamma+1) = 160) the product is HBM-bound on
+// the weight stream, so tiles are cut along the output features and K is split
+// stream-K style across all SMs so that every SM pulls 1/148 of the weights.
+//
+// Two epilogues:
+//   * PARTIAL: each CTA writes an fp32 partial sum for the (tile, k-range) piece
+//     it owns to part[slot][t][n]; the consumer kernel (residual+RMSNorm,
+//     RoPE+KV-append, SwiGLU) reduces the <= max_pieces slots of a tile in a
+//     fixed order, so results are deterministic run to run.
+//   * ARGMAX: full-K tiles (lm_head); the epilogue reduces each token column to
+//     (max logit, lowest index) over its 128 vocabulary rows.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace spin {
+
+enum GemmMode : int { kGemmPartial = 0, kGemmArgmax = 1 };
+
+// Stream-K bookkeeping shared by the GEMM and its consumers.
+struct PieceMap {
+  long long units;  // n_tiles * kb
+  int grid;         // CTAs
+  int kb;           // 64-wide k blocks per tile
+  int n_mtiles;     // 128-row tiles over N_out
+  int bn;           // token tile
+  int mode;         // GemmMode
+
+  // CTA that owns stream-K unit u.
+  __host__ __device__ __forceinline__ int cta_of(long long u) const {
+    return static_cast<int>((u * grid + grid - 1) / units);
+  }
+  // Number of partial slots written for (token t, feature n).
+  __host__ __device__ __forceinline__ int pieces(int t, int n) const {
+    if (mode != kGemmPartial) return 1;
+    const long long tile = static_cast<long long>(t / bn) * n_mtiles + n / 128;
+    return cta_of(tile * kb + kb - 1) - cta_of(tile * kb) + 1;
+  }
+};
+
+struct GemmPlan {
+  int n_out = 0, k = 0, t = 0;
+  int bn = 0, n_ntiles = 0, n_mtiles = 0, kb = 0;
+  int grid = 0, stages = 0, max_pieces = 1;
+  size_t smem_bytes = 0;
+  PieceMap map{};
+};
+
+struct GemmEpilogue {
+  int mode = kGemmPartial;
+  float* part = nullptr;     // PARTIAL: [max_pieces][t][n_out]
+  float* amax_val = nullptr; // ARGMAX: [n_mtiles][t]
+  int* amax_idx = nullptr;   // ARGMAX: [n_mtiles][t]
+  float* logits = nullptr;   // ARGMAX (optional): [t][n_out]
+};
+
+// Plans a launch for the given shape on `num_sms` SMs.
+GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms);
+
+// Encodes the two TMA descriptors (weights box 64x128, activations box 64xbn)
+// and launches. `pdl` enables programmatic dependent launch.
+cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, const GemmEpilogue& epi,
+                        cudaStream_t stream, bool pdl);
+
+// Encodes a 2-D bf16 K-major tensor map with 128-B swizzle (rows x cols, box rows x 64).
+bool encode_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                      uint32_t box_cols, bool swizzle128);
+
+}  // namespace spin
