@@ -1,0 +1,98 @@
+"""ctypes loaders for the CPU oracle (libspin_oracle.so) and the reference build
+(_ref/libspecsim_ref.so). TEST INFRASTRUCTURE ONLY: imported by tests/,
+__graft_entry__.smoke() and bench.py's CPU-baseline / reference arm, never by
+the product package."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "libspin_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libspecsim_ref.so")
+REF_SRC = "/root/reference/proj/core/src"
+
+_oracle = None
+_ref = None
+
+
+class SoModelDesc(C.Structure):
+    _fields_ = [
+        ("d_model", C.c_int32), ("n_layers", C.c_int32), ("n_heads", C.c_int32), ("head_dim", C.c_int32),
+        ("ffn", C.c_int32), ("vocab", C.c_int32), ("rope_theta", C.c_float), ("rms_eps", C.c_float),
+        ("seed", C.c_uint64), ("embed_scale", C.c_float), ("planted_gain", C.c_float),
+        ("resid_scale", C.c_float), ("init_scale", C.c_float),
+    ]
+
+
+def build(ref: bool | None = None) -> None:
+    """Compiles the oracle (and, when the reference sources exist, oracle/_ref)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+    if ref is None:
+        ref = os.path.isdir(REF_SRC)
+    if ref:
+        subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+
+
+def load_oracle() -> C.CDLL:
+    global _oracle
+    if _oracle is None:
+        if not os.path.exists(ORACLE_SO):
+            build(ref=False)
+        lib = C.CDLL(ORACLE_SO)
+        lib.so_splitmix64.restype = C.c_uint64
+        lib.so_splitmix64.argtypes = [C.c_uint64]
+        lib.so_mix_seed.restype = C.c_uint64
+        lib.so_mix_seed.argtypes = [C.c_uint64] * 4
+        lib.so_rng_next.restype = C.c_uint64
+        lib.so_rng_unit.restype = C.c_double
+        lib.so_rng_uniform.restype = C.c_double
+        lib.so_rng_uniform.argtypes = [C.c_void_p, C.c_double, C.c_double]
+        lib.so_rng_uniform_int.restype = C.c_longlong
+        lib.so_rng_uniform_int.argtypes = [C.c_void_p, C.c_longlong, C.c_longlong]
+        lib.so_rng_init.argtypes = [C.c_void_p, C.c_uint64]
+        lib.so_make_toy_input.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]
+        lib.so_expected_accepted_prefix.restype = C.c_double
+        lib.so_expected_accepted_prefix.argtypes = [C.c_double, C.c_int]
+        lib.so_sample_accepted_prefix.argtypes = [C.c_double, C.c_int, C.c_void_p]
+        lib.so_weight_bits.restype = C.c_uint16
+        lib.so_weight_bits.argtypes = [C.POINTER(SoModelDesc), C.c_int, C.c_int, C.c_int64, C.c_int64]
+        lib.so_planted_next.argtypes = [C.POINTER(SoModelDesc), C.c_int]
+        lib.so_engine_create.restype = C.c_void_p
+        lib.so_engine_create.argtypes = [C.POINTER(SoModelDesc), C.POINTER(SoModelDesc), C.c_int, C.c_int, C.c_int,
+                                         C.c_int, C.c_int]
+        lib.so_engine_destroy.argtypes = [C.c_void_p]
+        lib.so_engine_prefill.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.so_engine_round.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.so_engine_switch.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        lib.so_engine_read_tokens.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]
+        lib.so_engine_verify_seconds.restype = C.c_double
+        lib.so_engine_verify_seconds.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        _oracle = lib
+    return _oracle
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO) or os.path.isdir(REF_SRC)
+
+
+def load_ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_SO):
+            build(ref=True)
+        lib = C.CDLL(REF_SO)
+        lib.ref_mix_seed.restype = C.c_ulonglong
+        lib.ref_mix_seed.argtypes = [C.c_ulonglong] * 4
+        lib.ref_rng_draws.argtypes = [C.c_ulonglong, C.c_int, C.c_longlong, C.c_longlong, C.c_int, C.c_void_p,
+                                      C.c_void_p]
+        lib.ref_make_toy_input.argtypes = [C.c_ulonglong, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                           C.c_void_p]
+        lib.ref_expected_accepted_prefix.restype = C.c_double
+        lib.ref_expected_accepted_prefix.argtypes = [C.c_double, C.c_int]
+        lib.ref_sample_accepted_prefix.argtypes = [C.c_double, C.c_int, C.c_ulonglong, C.c_int, C.c_void_p]
+        _ref = lib
+    return _ref

@@ -1,0 +1,149 @@
+// extern "C" shim over the UNMODIFIED reference library functions on the
+// verification path, compiled together with the reference's own sources
+// (see oracle/Makefile, target `ref`). TEST INFRASTRUCTURE ONLY: used to pin
+// the oracle and to generate tests/golden/ fixtures; never shipped or linked
+// by libspin.so. Output goes to oracle/_ref/ (git-ignored).
+#include <cstring>
+#include <exception>
+#include <vector>
+
+#include "specsim/attention.hpp"
+#include "specsim/errors.hpp"
+#include "specsim/model.hpp"
+#include "specsim/packing.hpp"
+#include "specsim/rng.hpp"
+#include "specsim/slot_engine.hpp"
+
+using namespace specsim;
+
+namespace {
+int code_of(const std::exception& e) {
+  if (dynamic_cast<const ConfigError*>(&e)) return 1;
+  if (dynamic_cast<const CapacityError*>(&e)) return 2;
+  if (dynamic_cast<const InputError*>(&e)) return 3;
+  if (dynamic_cast<const SizeError*>(&e)) return 4;
+  if (dynamic_cast<const ConsistencyError*>(&e)) return 5;
+  if (dynamic_cast<const MetricError*>(&e)) return 6;
+  if (dynamic_cast<const IoError*>(&e)) return 7;
+  return 99;
+}
+template <typename F>
+int run(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+Matrix mat(const double* p, int r, int c) {
+  Matrix m(r, c);
+  std::memcpy(m.data.data(), p, sizeof(double) * r * c);
+  return m;
+}
+}  // namespace
+
+extern "C" {
+
+unsigned long long ref_mix_seed(unsigned long long s, unsigned long long a, unsigned long long b,
+                                unsigned long long c) {
+  return mix_seed(s, a, b, c);
+}
+
+// Draws `count` values from Rng(seed): kind 0 next(), 1 unit(), 2 uniform_int(lo, hi).
+void ref_rng_draws(unsigned long long seed, int kind, long long lo, long long hi, int count, double* out_d,
+                   unsigned long long* out_u) {
+  Rng r(seed);
+  for (int i = 0; i < count; ++i) {
+    if (kind == 0) out_u[i] = r.next();
+    if (kind == 1) out_d[i] = r.unit();
+    if (kind == 2) out_u[i] = static_cast<unsigned long long>(r.uniform_int(lo, hi));
+  }
+}
+
+void ref_make_toy_input(unsigned long long seed, int queries, int kv_len, int dim, double* q, double* k,
+                        double* v) {
+  const ToyAttentionInput in = make_toy_input(seed, queries, kv_len, dim);
+  std::memcpy(q, in.q.data.data(), sizeof(double) * queries * dim);
+  std::memcpy(k, in.k.data.data(), sizeof(double) * kv_len * dim);
+  std::memcpy(v, in.v.data.data(), sizeof(double) * kv_len * dim);
+}
+
+int ref_pack(const int* kv_lens, int n, int width, int* length, int* rows, int* segs, int seg_cap, int* n_segs,
+             long long* padding, int* q_replica_rows) {
+  return run([&] {
+    const PackedLayout L = pack(std::vector<int>(kv_lens, kv_lens + n), width);
+    *length = L.length;
+    *rows = L.width;
+    *padding = L.padding_tokens;
+    *n_segs = static_cast<int>(L.segments.size());
+    if (*n_segs > seg_cap) throw SizeError("segment buffer");
+    for (int i = 0; i < *n_segs; ++i) {
+      const Segment& s = L.segments[i];
+      int* o = segs + 5 * i;
+      o[0] = s.request_id, o[1] = s.row, o[2] = s.col_start, o[3] = s.col_end, o[4] = s.token_offset;
+    }
+    for (int i = 0; i < static_cast<int>(L.q_replica_rows.size()); ++i) q_replica_rows[i] = L.q_replica_rows[i];
+  });
+}
+
+int ref_naive_padding(const int* kv_lens, int n, long long* padding) {
+  return run([&] { *padding = naive_padding(std::vector<int>(kv_lens, kv_lens + n)); });
+}
+
+int ref_verify_batch_cost(const int* kv_lens, int n, int window, int packing, int pack_width, long long* tokens,
+                          long long* padding) {
+  return run([&] {
+    const VerifyBatchCost c = verify_batch_cost(std::vector<int>(kv_lens, kv_lens + n), window, packing != 0,
+                                                pack_width);
+    *tokens = c.tokens;
+    *padding = c.padding;
+  });
+}
+
+int ref_reference_attention(int qr, int kr, int dim, const double* q, const double* k, const double* v,
+                            double* out) {
+  return run([&] {
+    const Matrix o = reference_attention(mat(q, qr, dim), mat(k, kr, dim), mat(v, kr, dim));
+    std::memcpy(out, o.data.data(), sizeof(double) * qr * dim);
+  });
+}
+
+// Packs the requests' kv lengths itself (pack(kv_rows, width)) like the
+// reference tests do, then runs decomposed_attention on that layout.
+int ref_decomposed_attention(int n, int dim, const int* q_rows, const int* kv_rows, const double* q, const double* k,
+                             const double* v, int width, double* out) {
+  return run([&] {
+    std::vector<ToyAttentionInput> in(n);
+    std::vector<int> lens(n);
+    long qo = 0, ko = 0;
+    for (int i = 0; i < n; ++i) {
+      in[i].q = mat(q + qo * dim, q_rows[i], dim);
+      in[i].k = mat(k + ko * dim, kv_rows[i], dim);
+      in[i].v = mat(v + ko * dim, kv_rows[i], dim);
+      lens[i] = kv_rows[i];
+      qo += q_rows[i];
+      ko += kv_rows[i];
+    }
+    const PackedLayout L = pack(lens, width);
+    const auto outs = decomposed_attention(in, L, build_indicator(L));
+    long oo = 0;
+    for (int i = 0; i < n; ++i) {
+      std::memcpy(out + oo * dim, outs[i].data.data(), sizeof(double) * q_rows[i] * dim);
+      oo += q_rows[i];
+    }
+  });
+}
+
+int ref_sample_accepted_prefix(double p, int window, unsigned long long seed, int draws, int* out) {
+  return run([&] {
+    Request r;
+    r.accept_prob = {p};
+    Rng rng(seed);
+    for (int i = 0; i < draws; ++i) out[i] = sample_accepted_prefix(r, 0, window, rng);
+  });
+}
+
+double ref_expected_accepted_prefix(double p, int window) { return expected_accepted_prefix(p, window); }
+
+}  // extern "C"
