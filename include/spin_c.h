@@ -168,6 +168,15 @@ spin_status spin_gemm_info(int32_t n_out, int32_t k, int32_t t, int32_t mode, in
 spin_status spin_gemm(void* stream, const void* w, const void* x, int32_t n_out, int32_t k, int32_t t,
                       int32_t mode, float* part, float* amax_val, int32_t* amax_idx, float* logits);
 
+/* Packed ragged causal attention over a KV cache [layers][slots][heads][ctx][hd]
+ * (bf16, device). q: [sum(qlen)][heads*hd] fp32 rows, request i owning qlen[i]
+ * consecutive rows at positions kvlen[i]-qlen[i] .. kvlen[i]-1; the work list is
+ * pack(kvlen, width). out: [sum(qlen)][heads*hd] bf16. Host arrays for the request shapes. */
+spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int32_t layers, int32_t slots,
+                           int32_t ctx, int32_t layer, const void* k_cache, const void* v_cache, const void* q,
+                           int32_t n_req, const int32_t* req_slot, const int32_t* req_qlen, const int32_t* req_kvlen,
+                           int32_t width, void* out);
+
 #ifdef __cplusplus
 }
 #endif

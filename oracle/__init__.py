@@ -69,6 +69,9 @@ def load_oracle() -> C.CDLL:
                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         lib.so_engine_switch.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         lib.so_engine_read_tokens.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]
+        lib.so_set_gemm_lanes.argtypes = [C.c_int]
+        lib.so_debug_layer.argtypes = [C.c_int, C.c_void_p, C.c_int]
+        lib.so_debug_inner.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int]
         lib.so_engine_verify_seconds.restype = C.c_double
         lib.so_engine_verify_seconds.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         _oracle = lib
@@ -96,3 +99,78 @@ def load_ref() -> C.CDLL:
         lib.ref_sample_accepted_prefix.argtypes = [C.c_double, C.c_int, C.c_ulonglong, C.c_int, C.c_void_p]
         _ref = lib
     return _ref
+
+
+def so_desc(shape) -> SoModelDesc:
+    """SoModelDesc from a paper_2503_15921_b200.models.ModelShape (same fields)."""
+    d = SoModelDesc()
+    for f, _ in SoModelDesc._fields_:
+        setattr(d, f, getattr(shape, f))
+    return d
+
+
+class OracleEngine:
+    """CPU oracle twin of paper_2503_15921_b200.models.Engine (same round contract)."""
+
+    def __init__(self, target, ssms, *, max_requests, max_ctx, window, threads=0):
+        import numpy as np  # noqa: F401
+
+        self.lib = load_oracle()
+        self.window, self.max_ctx, self.vocab = window, max_ctx, target.vocab
+        self._t = so_desc(target)
+        arr = (SoModelDesc * len(ssms))(*[so_desc(s) for s in ssms])
+        self._s = arr
+        self.e = self.lib.so_engine_create(C.byref(self._t), arr, len(ssms), max_requests, max_ctx, window, threads)
+
+    def close(self):
+        if self.e:
+            self.lib.so_engine_destroy(self.e)
+            self.e = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def prefill(self, slots, prompts):
+        import numpy as np
+
+        slots = np.asarray(slots, dtype=np.int32)
+        lens = np.array([len(p) for p in prompts], dtype=np.int32)
+        flat = np.concatenate(prompts).astype(np.int32)
+        assert self.lib.so_engine_prefill(self.e, len(slots), slots.ctypes.data, lens.ctypes.data, flat.ctypes.data) == 0
+
+    def round(self, slots, ssm_of, want_logits=False):
+        import numpy as np
+
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        ssm_of = np.ascontiguousarray(ssm_of, dtype=np.int32)
+        n, W = len(slots), self.window
+        acc, bonus, comm = np.zeros(n, np.int32), np.zeros(n, np.int32), np.zeros(n, np.int32)
+        drafts, tgt = np.zeros(n * W, np.int32), np.zeros(n * (W + 1), np.int32)
+        act = int((ssm_of >= 0).sum())
+        logits = np.zeros(act * (W + 1) * self.vocab, np.float32) if want_logits else None
+        st = self.lib.so_engine_round(self.e, n, slots.ctypes.data, ssm_of.ctypes.data, acc.ctypes.data,
+                                      bonus.ctypes.data, comm.ctypes.data, drafts.ctypes.data, tgt.ctypes.data,
+                                      logits.ctypes.data if want_logits else None)
+        assert st == 0, st
+        out = {"accepted": acc, "bonus": bonus, "committed": comm, "drafts": drafts.reshape(n, W),
+               "target": tgt.reshape(n, W + 1)}
+        if want_logits:
+            out["logits"] = logits.reshape(act * (W + 1), self.vocab)
+        return out
+
+    def tokens(self, slot):
+        import numpy as np
+
+        buf = np.zeros(self.max_ctx, np.int32)
+        n = C.c_int()
+        assert self.lib.so_engine_read_tokens(self.e, slot, buf.ctypes.data, self.max_ctx, C.byref(n)) == 0
+        return buf[: n.value].copy()
+
+    def verify_seconds(self, slots):
+        import numpy as np
+
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        return self.lib.so_engine_verify_seconds(self.e, len(slots), slots.ctypes.data)

@@ -8,7 +8,8 @@
  *   - generated_len update / commit                    slot_engine.cpp:151-156
  *   - softmax attention, max-subtracted                attention.cpp:67-96
  * Rounding points mirror the GPU exactly (bf16 storage of weights, normalised
- * activations, attention output, SwiGLU output and KV; fp32 everywhere else),
+ * activations, attention output, SwiGLU output and KV -- the tensor-core GEMM
+ * inputs and HBM-resident state; fp32 everywhere else, including q),
  * so argmax tokens agree bit-for-bit and logits to ~1e-6 relative.
  */
 #include <math.h>
@@ -200,6 +201,10 @@ static void model_destroy(model* m) {
   free(m);
 }
 
+/* Debug knob (sensitivity experiments only): number of partial sums. */
+static int g_lanes = 16;
+void so_set_gemm_lanes(int lanes) { g_lanes = lanes == 8 ? 8 : 16; }
+
 /* Y[t][n] = sum_k X[t][k] W[n][k]; fp32 with 16 fixed partial sums. */
 static void gemm(const float* X, int T, int K, const uint16_t* W, int N, float* Y) {
 #pragma omp parallel
@@ -213,9 +218,13 @@ static void gemm(const float* X, int T, int K, const uint16_t* W, int N, float* 
         const float* x = X + (size_t)t * K;
         float acc[16] = {0};
         int k = 0;
-        for (; k + 16 <= K; k += 16)
-          for (int j = 0; j < 16; ++j) acc[j] += x[k + j] * wr[k + j];
-        for (int j = 0; k < K; ++k, ++j) acc[j] += x[k] * wr[k];
+        if (g_lanes == 16) {
+          for (; k + 16 <= K; k += 16)
+            for (int j = 0; j < 16; ++j) acc[j] += x[k + j] * wr[k + j];
+          for (int j = 0; k < K; ++k, ++j) acc[j] += x[k] * wr[k];
+        } else {
+          for (; k < K; ++k) acc[k & 7] += x[k] * wr[k];
+        }
         for (int s = 8; s > 0; s >>= 1)
           for (int j = 0; j < s; ++j) acc[j] += acc[j + s];
         Y[(size_t)t * N + n] = acc[0];
@@ -237,6 +246,18 @@ static void rmsnorm_bf16(const float* h, int T, int d, float eps, float* x) {
 
 /* Forward of T tokens (slot, pos) through the model; writes KV at (slot, pos)
  * and attends causally over keys [0, pos] of the slot. */
+/* Debug capture (sensitivity experiments): residual stream after each layer of
+ * the last forward, up to 64 layers x 4096 floats. */
+static float g_dbg[64][4096];
+static float g_dbg2[8][4][4096]; /* layer<8: attn-out, o-proj, act, down */
+static int g_dbg_n = 0;
+void so_debug_inner(int layer, int which, float* out, int n) {
+  memcpy(out, g_dbg2[layer][which], sizeof(float) * (n < 4096 ? n : 4096));
+}
+void so_debug_layer(int layer, float* out, int n) {
+  memcpy(out, g_dbg[layer], sizeof(float) * (n < 4096 ? n : 4096));
+}
+
 static void model_forward(model* m, int T, const int* tok, const int* slot, const int* pos, int* amax,
                           float* logits) {
   const so_model_desc* d = &m->d;
@@ -264,8 +285,8 @@ static void model_forward(model* m, int T, const int* tok, const int* slot, cons
         for (int i = 0; i < half; ++i) {
           const float q0 = qh[i], q1 = qh[i + half], k0 = kh[i], k1 = kh[i + half];
           const float a = q0 * c[i], b = q1 * s[i], e = q1 * c[i], f = q0 * s[i];
-          q[(size_t)t * D + hh * hd + i] = rbf(a - b);
-          q[(size_t)t * D + hh * hd + i + half] = rbf(e + f);
+          q[(size_t)t * D + hh * hd + i] = a - b;
+          q[(size_t)t * D + hh * hd + i + half] = e + f;
           const float ka = k0 * c[i], kb = k1 * s[i], ke = k1 * c[i], kf = k0 * s[i];
           kd[i] = f2bf(ka - kb);
           kd[i + half] = f2bf(ke + kf);
@@ -300,7 +321,10 @@ static void model_forward(model* m, int T, const int* tok, const int* slot, cons
         for (int i = 0; i < hd; ++i) x[(size_t)t * D + hh * hd + i] = rbf(o[i] / den);
         free(sc);
       }
+#define DBG(w, src, cnt) if (l < 8) memcpy(g_dbg2[l][w], src, sizeof(float) * ((size_t)(cnt) < 4096 ? (size_t)(cnt) : 4096))
+    DBG(0, x, (size_t)T * D);
     gemm(x, T, D, m->L[l].o, D, y);
+    DBG(1, y, (size_t)T * D);
     for (size_t i = 0; i < (size_t)T * D; ++i) h[i] += y[i];
     rmsnorm_bf16(h, T, D, d->rms_eps, x);
     gemm(x, T, D, m->L[l].gu, 2 * F, y);
@@ -310,9 +334,13 @@ static void model_forward(model* m, int T, const int* tok, const int* slot, cons
         const float sg = g / (1.0f + expf(-g));
         x[(size_t)t * F + i] = rbf(sg * u);
       }
+    DBG(2, x, (size_t)T * F);
     gemm(x, T, F, m->L[l].dn, D, y);
+    DBG(3, y, (size_t)T * D);
     for (size_t i = 0; i < (size_t)T * D; ++i) h[i] += y[i];
+    if (l < 64) memcpy(g_dbg[l], h, sizeof(float) * ((size_t)T * D < 4096 ? (size_t)T * D : 4096));
   }
+  g_dbg_n = d->n_layers;
   rmsnorm_bf16(h, T, D, d->rms_eps, x);
   float* lg = logits ? logits : (float*)malloc(sizeof(float) * (size_t)T * V);
   gemm(x, T, D, m->head, V, lg);

@@ -2,11 +2,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
 
+#include "engine.hpp"
 #include "gemm.cuh"
+#include "kernels.cuh"
 #include "pack.hpp"
 #include "spin_c.h"
 #include "status.hpp"
@@ -92,6 +95,278 @@ spin_status spin_gemm(void* stream, const void* w, const void* x, int32_t n_out,
       fail(SPIN_INPUT_ERROR, "spin_gemm: argmax buffers missing");
     check_cuda(gemm_launch(p, w, x, e, static_cast<cudaStream_t>(stream), false), "gemm launch");
     check_cuda(cudaGetLastError(), "gemm launch");
+  });
+}
+
+
+// ---------------------------------------------------------------- attention operator
+spin_status spin_reference_attention(int32_t q_rows, int32_t kv_rows, int32_t dim, const double* q, const double* k,
+                                     const double* v, double* out) {
+  if (kv_rows == 0) {
+    set_last_error("reference_attention: empty KV");
+    return SPIN_INPUT_ERROR;
+  }
+  spin_segment seg{0, 0, 0, kv_rows, 0};
+  return spin_decomposed_attention(1, dim, &q_rows, &kv_rows, q, k, v, &seg, 1, 1, kv_rows, nullptr, out);
+}
+
+spin_status spin_decomposed_attention(int32_t n_req, int32_t dim, const int32_t* q_rows, const int32_t* kv_rows,
+                                      const double* q, const double* k, const double* v, const spin_segment* segs,
+                                      int32_t n_segs, int32_t width, int32_t length, const int32_t* mask,
+                                      double* out) {
+  return guarded([&] {
+    if (n_req < 0 || dim < 1 || n_segs < 0 || width < 0 || length < 0)
+      fail(SPIN_INPUT_ERROR, "decomposed_attention: bad sizes");
+    // check_layout_consistency (attention.cpp:23-63): rebuild the indicator,
+    // compare with the caller's mask, and require every request's tokens be
+    // covered exactly once.
+    std::vector<int32_t> cells(static_cast<size_t>(width) * length, -1);
+    for (int s = 0; s < n_segs; ++s) {
+      const spin_segment& g = segs[s];
+      if (g.row < 0 || g.row >= width || g.col_start < 0 || g.col_end > length || g.col_start >= g.col_end)
+        fail(SPIN_CONSISTENCY_ERROR, "build_indicator: segment out of bounds");
+      for (int c = g.col_start; c < g.col_end; ++c) {
+        int32_t& cell = cells[static_cast<size_t>(g.row) * length + c];
+        if (cell != -1) fail(SPIN_CONSISTENCY_ERROR, "build_indicator: overlapping segments");
+        cell = g.request_id;
+      }
+    }
+    if (mask != nullptr && std::memcmp(mask, cells.data(), cells.size() * 4) != 0)
+      fail(SPIN_CONSISTENCY_ERROR, "decomposed_attention: mask does not match layout");
+    std::vector<int32_t> q_off(n_req + 1, 0), kv_off(n_req + 1, 0);
+    for (int i = 0; i < n_req; ++i) {
+      if (q_rows[i] < 0 || kv_rows[i] < 1) fail(SPIN_INPUT_ERROR, "decomposed_attention: empty request");
+      q_off[i + 1] = q_off[i] + q_rows[i];
+      kv_off[i + 1] = kv_off[i] + kv_rows[i];
+    }
+    std::vector<char> covered(kv_off[n_req], 0);
+    for (int s = 0; s < n_segs; ++s) {
+      const spin_segment& g = segs[s];
+      if (g.request_id < 0 || g.request_id >= n_req)
+        fail(SPIN_CONSISTENCY_ERROR, "decomposed_attention: segment references unknown request");
+      for (int t = 0; t < g.col_end - g.col_start; ++t) {
+        const int tok = g.token_offset + t;
+        if (tok >= kv_rows[g.request_id] || covered[kv_off[g.request_id] + tok])
+          fail(SPIN_CONSISTENCY_ERROR, "decomposed_attention: segment tokens do not tile the request");
+        covered[kv_off[g.request_id] + tok] = 1;
+      }
+    }
+    for (char c : covered)
+      if (!c) fail(SPIN_CONSISTENCY_ERROR, "decomposed_attention: request not fully packed");
+    // work lists: segments grouped by row (column order) and by request
+    std::vector<int32_t> seg5(static_cast<size_t>(n_segs) * 5), row_ptr(width + 1, 0), row_seg(n_segs),
+        req_seg0(n_req, 0), req_nseg(n_req, 0);
+    std::vector<int> order(n_segs);
+    for (int s = 0; s < n_segs; ++s) {
+      seg5[5 * s] = segs[s].request_id, seg5[5 * s + 1] = segs[s].row, seg5[5 * s + 2] = segs[s].col_start;
+      seg5[5 * s + 3] = segs[s].col_end, seg5[5 * s + 4] = segs[s].token_offset;
+      ++row_ptr[segs[s].row + 1];
+      order[s] = s;
+    }
+    for (int r = 0; r < width; ++r) row_ptr[r + 1] += row_ptr[r];
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return segs[a].row != segs[b].row ? segs[a].row < segs[b].row : segs[a].col_start < segs[b].col_start;
+    });
+    for (int s = 0; s < n_segs; ++s) row_seg[s] = order[s];
+    // partials are indexed by segment id; the combine walks a request's ids
+    std::vector<int32_t> by_req(n_segs);
+    std::vector<int> ro(n_segs);
+    for (int s = 0; s < n_segs; ++s) ro[s] = s;
+    std::stable_sort(ro.begin(), ro.end(), [&](int a, int b) { return segs[a].request_id < segs[b].request_id; });
+    // remap so each request's segments are contiguous ids
+    std::vector<int32_t> newid(n_segs);
+    for (int s = 0; s < n_segs; ++s) newid[ro[s]] = s;
+    std::vector<int32_t> seg5n(seg5.size());
+    for (int s = 0; s < n_segs; ++s)
+      for (int f = 0; f < 5; ++f) seg5n[5 * newid[s] + f] = seg5[5 * s + f];
+    for (int s = 0; s < n_segs; ++s) row_seg[s] = newid[row_seg[s]];
+    for (int s = n_segs - 1; s >= 0; --s) {
+      const int rq = seg5n[5 * s];
+      req_seg0[rq] = s;
+      ++req_nseg[rq];
+    }
+    int qmax = 1;
+    for (int i = 0; i < n_req; ++i) qmax = std::max(qmax, q_rows[i]);
+    // device buffers
+    auto bytes_d = [](size_t n) { return n * sizeof(double); };
+    const size_t nq = static_cast<size_t>(q_off[n_req]) * dim, nk = static_cast<size_t>(kv_off[n_req]) * dim;
+    const size_t np = static_cast<size_t>(std::max(n_segs, 1)) * qmax;
+    std::vector<void*> bufs;
+    auto dmal = [&](size_t b) {
+      void* p = nullptr;
+      check_cuda(cudaMalloc(&p, std::max<size_t>(b, 8)), "cudaMalloc");
+      bufs.push_back(p);
+      return p;
+    };
+    struct Free {
+      std::vector<void*>* b;
+      ~Free() {
+        for (void* p : *b) cudaFree(p);
+      }
+    } freer{&bufs};
+    double* dq = static_cast<double*>(dmal(bytes_d(nq)));
+    double* dk = static_cast<double*>(dmal(bytes_d(nk)));
+    double* dv = static_cast<double*>(dmal(bytes_d(nk)));
+    double* dout = static_cast<double*>(dmal(bytes_d(nq)));
+    double* pm = static_cast<double*>(dmal(bytes_d(np)));
+    double* pl = static_cast<double*>(dmal(bytes_d(np)));
+    double* po = static_cast<double*>(dmal(bytes_d(np * dim)));
+    int32_t* ib = static_cast<int32_t*>(dmal(4 * (3 * (n_req + 1) + seg5n.size() + row_ptr.size() + row_seg.size() +
+                                                  2 * n_req + 8)));
+    std::vector<int32_t> host_ints;
+    auto put = [&](const std::vector<int32_t>& v) {
+      const size_t o = host_ints.size();
+      host_ints.insert(host_ints.end(), v.begin(), v.end());
+      return ib + o;
+    };
+    std::vector<int32_t> qr(q_rows, q_rows + n_req);
+    const int32_t* d_qoff = put(q_off);
+    const int32_t* d_kvoff = put(kv_off);
+    const int32_t* d_qrows = put(qr);
+    const int32_t* d_seg = put(seg5n);
+    const int32_t* d_rowptr = put(row_ptr);
+    const int32_t* d_rowseg = put(row_seg);
+    const int32_t* d_s0 = put(req_seg0);
+    const int32_t* d_ns = put(req_nseg);
+    check_cuda(cudaMemcpy(ib, host_ints.data(), host_ints.size() * 4, cudaMemcpyHostToDevice), "h2d");
+    check_cuda(cudaMemcpy(dq, q, bytes_d(nq), cudaMemcpyHostToDevice), "h2d");
+    check_cuda(cudaMemcpy(dk, k, bytes_d(nk), cudaMemcpyHostToDevice), "h2d");
+    check_cuda(cudaMemcpy(dv, v, bytes_d(nk), cudaMemcpyHostToDevice), "h2d");
+    launch_toy_attention(dq, dk, dv, d_qoff, d_kvoff, d_qrows, d_seg, n_segs, d_rowptr, d_rowseg, width, d_s0, d_ns,
+                         n_req, dim, qmax, pm, pl, po, dout, nullptr);
+    check_cuda(cudaGetLastError(), "toy attention");
+    check_cuda(cudaMemcpy(out, dout, bytes_d(nq), cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+// ---------------------------------------------------------------- engine
+struct spin_ctx {
+  std::unique_ptr<Engine> eng;
+};
+
+spin_status spin_ctx_create(const spin_model_desc* target, const spin_model_desc* ssms, int32_t n_ssm,
+                            const spin_engine_opts* opts, spin_ctx** out) {
+  return guarded([&] {
+    if (!target || !ssms || !opts || !out) fail(SPIN_INPUT_ERROR, "spin_ctx_create: null argument");
+    auto ctx = std::make_unique<spin_ctx>();
+    ctx->eng = std::make_unique<Engine>(*target, ssms, n_ssm, *opts);
+    *out = ctx.release();
+  });
+}
+
+spin_status spin_ctx_destroy(spin_ctx* ctx) {
+  return guarded([&] { delete ctx; });
+}
+
+spin_status spin_prefill(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* prompt_lens,
+                         const int32_t* prompts) {
+  return guarded([&] {
+    if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
+    ctx->eng->prefill(n, slots, prompt_lens, prompts);
+  });
+}
+
+spin_status spin_round(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of, spin_round_out* out) {
+  return guarded([&] {
+    if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
+    ctx->eng->round(n, slots, ssm_of, out);
+  });
+}
+
+spin_status spin_run_rounds(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of, int32_t rounds,
+                            int64_t* emitted, float* device_ms) {
+  return guarded([&] {
+    if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
+    ctx->eng->run_rounds(n, slots, ssm_of, rounds, emitted, device_ms);
+  });
+}
+
+spin_status spin_read_tokens(spin_ctx* ctx, int32_t slot, int32_t* tokens, int32_t cap, int32_t* len) {
+  return guarded([&] {
+    if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
+    ctx->eng->read_tokens(slot, tokens, cap, len);
+  });
+}
+
+spin_status spin_read_logits(spin_ctx* ctx, float* logits, int64_t cap, int32_t* rows) {
+  return guarded([&] {
+    if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
+    ctx->eng->read_logits(logits, cap, rows);
+  });
+}
+
+spin_status spin_switch_ssm(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of) {
+  return guarded([&] {
+    if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
+    ctx->eng->switch_ssm(n, slots, ssm_of);
+  });
+}
+
+
+// Kernel-level entry for the packed ragged causal attention (device pointers).
+spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int32_t layers, int32_t slots,
+                           int32_t ctx, int32_t layer, const void* k_cache, const void* v_cache, const void* q,
+                           int32_t n_req, const int32_t* req_slot, const int32_t* req_qlen, const int32_t* req_kvlen,
+                           int32_t width, void* out) {
+  return guarded([&] {
+    if (head_dim != 64 && head_dim != 128) fail(SPIN_INPUT_ERROR, "spin_attention: head_dim must be 64 or 128");
+    if (n_req < 1) fail(SPIN_INPUT_ERROR, "spin_attention: empty batch");
+    int qmax = 1;
+    std::vector<int32_t> qstart(n_req);
+    int T = 0;
+    for (int i = 0; i < n_req; ++i) {
+      if (req_qlen[i] < 1 || req_qlen[i] > 17 || req_kvlen[i] < req_qlen[i] || req_kvlen[i] > ctx)
+        fail(SPIN_INPUT_ERROR, "spin_attention: bad request shape");
+      qstart[i] = T;
+      T += req_qlen[i];
+      qmax = std::max(qmax, req_qlen[i]);
+    }
+    const PackResult p = pack_lengths(req_kvlen, n_req, width > 0 ? width : n_req);
+    const int nseg = static_cast<int>(p.segments.size());
+    std::vector<int32_t> seg5(5 * nseg), row_ptr(p.rows + 1, 0), row_seg(nseg), s0(n_req, 0), ns(n_req, 0);
+    for (int s = 0; s < nseg; ++s) {
+      const spin_segment& g = p.segments[s];
+      seg5[5 * s] = g.request_id, seg5[5 * s + 1] = g.row, seg5[5 * s + 2] = g.col_start;
+      seg5[5 * s + 3] = g.col_end, seg5[5 * s + 4] = g.token_offset;
+      ++row_ptr[g.row + 1];
+      if (ns[g.request_id]++ == 0) s0[g.request_id] = s;
+    }
+    for (int r = 0; r < p.rows; ++r) row_ptr[r + 1] += row_ptr[r];
+    std::vector<int32_t> cur(row_ptr.begin(), row_ptr.end() - 1);
+    for (int s = 0; s < nseg; ++s) row_seg[cur[p.segments[s].row]++] = s;
+    std::vector<int32_t> ints;
+    std::vector<size_t> off;
+    auto put = [&](const int32_t* v, size_t n) {
+      off.push_back(ints.size());
+      ints.insert(ints.end(), v, v + n);
+    };
+    put(req_slot, n_req), put(qstart.data(), n_req), put(req_qlen, n_req), put(req_kvlen, n_req);
+    put(seg5.data(), seg5.size()), put(row_ptr.data(), row_ptr.size()), put(row_seg.data(), row_seg.size());
+    put(s0.data(), n_req), put(ns.data(), n_req);
+    int32_t* d_ints = nullptr;
+    float* d_part = nullptr;
+    check_cuda(cudaMalloc(&d_ints, ints.size() * 4), "malloc");
+    const size_t np = static_cast<size_t>(nseg) * n_heads * 17;
+    check_cuda(cudaMalloc(&d_part, np * (2 + head_dim) * 4), "malloc");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    check_cuda(cudaMemcpyAsync(d_ints, ints.data(), ints.size() * 4, cudaMemcpyHostToDevice, s), "h2d");
+    FwdMeta m{};
+    m.req_slot = d_ints + off[0], m.req_qstart = d_ints + off[1], m.req_qlen = d_ints + off[2];
+    m.req_kvlen = d_ints + off[3], m.seg = d_ints + off[4], m.row_ptr = d_ints + off[5], m.row_seg = d_ints + off[6];
+    m.req_seg0 = d_ints + off[7], m.req_nseg = d_ints + off[8];
+    AttnGeom g{n_heads, head_dim, slots, ctx, layer, static_cast<float>(1.0 / std::sqrt(double(head_dim))),
+               const_cast<bf16*>(static_cast<const bf16*>(k_cache)), const_cast<bf16*>(static_cast<const bf16*>(v_cache))};
+    CUtensorMap tk, tv;
+    const uint64_t rows = static_cast<uint64_t>(layers) * slots * n_heads * ctx;
+    if (!encode_tmap_bf16(&tk, k_cache, rows, head_dim, 32, 64, true) ||
+        !encode_tmap_bf16(&tv, v_cache, rows, head_dim, 32, 64, true))
+      fail(SPIN_CUDA_ERROR, "tensor map encode");
+    AttnWork w{d_part, d_part + np, d_part + 2 * np, qmax};
+    launch_attention(tk, tv, m, p.rows, n_req, g, static_cast<const float*>(q), w, static_cast<bf16*>(out), s);
+    check_cuda(cudaGetLastError(), "attention launch");
+    check_cuda(cudaStreamSynchronize(s), "attention");
+    cudaFree(d_ints);
+    cudaFree(d_part);
   });
 }
 

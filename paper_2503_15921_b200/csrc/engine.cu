@@ -1,0 +1,703 @@
+// Engine: synthetic models on the device, forward orchestration, the
+// speculate -> verify -> accept round (SlotEngine::run_slot, slot_engine.cpp:70-167)
+// captured as one CUDA graph per assignment shape, SSM drafts on their own
+// streams joined before verification.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "status.hpp"
+
+namespace spin {
+
+namespace {
+
+constexpr int kExtendRows = 512;  // rows per prefill / catch-up chunk
+constexpr int kExtendQ = 8;       // queries per virtual request in a chunk
+
+uint64_t host_splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+uint64_t host_mix_seed(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t h = host_splitmix64(seed);
+  h = host_splitmix64(h ^ a);
+  h = host_splitmix64(h ^ b);
+  return host_splitmix64(h ^ c);
+}
+
+enum { kTagEmbed = 1, kTagHead = 2, kTagQkv = 3, kTagO = 4, kTagGateUp = 5, kTagDown = 6 };
+
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    const int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+int64_t mod_inverse(int64_t a, int64_t n) {
+  int64_t t = 0, nt = 1, r = n, nr = a % n;
+  while (nr != 0) {
+    const int64_t q = r / nr, tt = t - q * nt, rr = r - q * nr;
+    t = nt, nt = tt, r = nr, nr = rr;
+  }
+  return t < 0 ? t + n : t;
+}
+
+template <typename T>
+T* dalloc(std::vector<void*>& list, size_t count) {
+  void* p = nullptr;
+  check_cuda(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+  list.push_back(p);
+  return static_cast<T*>(p);
+}
+
+void validate_desc(const spin_model_desc& d, const char* who) {
+  const std::string w(who);
+  if (d.d_model < 64 || d.n_layers < 1 || d.n_heads < 1 || d.vocab < 2 || d.ffn < 8)
+    fail(SPIN_CONFIG_ERROR, w + ": model dimensions out of range");
+  if (d.head_dim != 64 && d.head_dim != 128) fail(SPIN_CONFIG_ERROR, w + ": head_dim must be 64 or 128");
+  if (d.n_heads * d.head_dim != d.d_model) fail(SPIN_CONFIG_ERROR, w + ": n_heads * head_dim must equal d_model");
+  if (d.d_model % 64 != 0 || d.ffn % 8 != 0) fail(SPIN_CONFIG_ERROR, w + ": d_model % 64 and ffn % 8 required");
+  if (d.d_model > 8192) fail(SPIN_CONFIG_ERROR, w + ": d_model above 8192 unsupported");
+  if (!(d.rope_theta > 0.f) || !(d.rms_eps > 0.f)) fail(SPIN_CONFIG_ERROR, w + ": rope_theta / rms_eps must be > 0");
+}
+
+}  // namespace
+
+struct Engine::RoundPlan {
+  std::vector<int> key;  // [n_act, n_0 .. n_{M-1}]
+  int n_act = 0;
+  std::vector<int> n_ssm;
+  int off_list = 0, off_ssm_of = 0;
+  std::vector<int> off_ssm_list;
+  int in_ints = 0, out_ints = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+// ------------------------------------------------------------------ models
+void Engine::init_model(ModelDev& m, const spin_model_desc& d) {
+  m.d = d;
+  m.D = d.d_model, m.H = d.n_heads, m.hd = d.head_dim, m.F = d.ffn, m.V = d.vocab, m.L = d.n_layers;
+  const size_t D = m.D, F = m.F, V = m.V;
+  const size_t per_layer = 3 * D * D + D * D + 2 * F * D + D * F;
+  const size_t total = 2 * V * D + per_layer * m.L;
+  m.weight_bytes = total * 2;
+  check_cuda(cudaMalloc(&m.wbuf, m.weight_bytes), "weights");
+  m.emb = m.wbuf;
+  m.head = m.wbuf + V * D;
+  bf16* p = m.wbuf + 2 * V * D;
+  m.layers.resize(m.L);
+  for (int l = 0; l < m.L; ++l) {
+    LayerW& w = m.layers[l];
+    w.qkv = p, p += 3 * D * D;
+    w.o = p, p += D * D;
+    w.gu = p, p += 2 * F * D;
+    w.dn = p, p += D * F;
+  }
+  // Synthetic weights, same spec as oracle/llama_oracle.c.
+  auto stream_of = [&](int tag, int layer) { return host_mix_seed(d.seed, 0x5350494EULL, tag, layer); };
+  const float s_emb = static_cast<float>(std::sqrt(3.0) * d.embed_scale);
+  const float s_head = static_cast<float>(std::sqrt(3.0 / D));
+  const float s_in = static_cast<float>(std::sqrt(3.0 / D) * d.init_scale);
+  const float s_o = static_cast<float>(std::sqrt(3.0 / D) * d.resid_scale);
+  const float s_dn = static_cast<float>(std::sqrt(3.0 / F) * d.resid_scale);
+  launch_init_weights(m.emb, V, D, stream_of(kTagEmbed, 0), s_emb, nullptr, 0.f, V, 1, 0, sv_);
+  int64_t a = 7919 % static_cast<int64_t>(V);
+  if (a == 0) a = 1;
+  while (gcd64(a, V) != 1) a = (a + 1) % static_cast<int64_t>(V);
+  const int64_t cc = 12345 % static_cast<int64_t>(V);
+  const float g = static_cast<float>(static_cast<double>(d.planted_gain) / static_cast<double>(D));
+  launch_init_weights(m.head, V, D, stream_of(kTagHead, 0), s_head, d.planted_gain != 0.f ? m.emb : nullptr, g, V,
+                      mod_inverse(a, V), cc, sv_);
+  for (int l = 0; l < m.L; ++l) {
+    launch_init_weights(const_cast<bf16*>(m.layers[l].qkv), 3 * D, D, stream_of(kTagQkv, l), s_in, nullptr, 0.f, V, 1,
+                        0, sv_);
+    launch_init_weights(const_cast<bf16*>(m.layers[l].o), D, D, stream_of(kTagO, l), s_o, nullptr, 0.f, V, 1, 0, sv_);
+    launch_init_weights(const_cast<bf16*>(m.layers[l].gu), 2 * F, D, stream_of(kTagGateUp, l), s_in, nullptr, 0.f, V,
+                        1, 0, sv_);
+    launch_init_weights(const_cast<bf16*>(m.layers[l].dn), D, F, stream_of(kTagDown, l), s_dn, nullptr, 0.f, V, 1, 0,
+                        sv_);
+  }
+  check_cuda(cudaGetLastError(), "init weights");
+  // KV cache [layer][slot][head][ctx][hd], zero-filled.
+  const size_t kv = static_cast<size_t>(m.L) * opts_.max_requests * m.H * opts_.max_ctx * m.hd;
+  m.kv_bytes = 2 * kv * 2;
+  check_cuda(cudaMalloc(&m.kc, kv * 2), "k cache");
+  check_cuda(cudaMalloc(&m.vc, kv * 2), "v cache");
+  check_cuda(cudaMemsetAsync(m.kc, 0, kv * 2, sv_), "memset");
+  check_cuda(cudaMemsetAsync(m.vc, 0, kv * 2, sv_), "memset");
+  const uint64_t rows = static_cast<uint64_t>(m.L) * opts_.max_requests * m.H * opts_.max_ctx;
+  if (!encode_tmap_bf16(&m.tm_k, m.kc, rows, m.hd, 32, 64, true) ||
+      !encode_tmap_bf16(&m.tm_v, m.vc, rows, m.hd, 32, 64, true))
+    fail(SPIN_CUDA_ERROR, "KV tensor map encode failed");
+  // RoPE tables in double, rounded once (matches the oracle bit for bit).
+  const int half = m.hd / 2;
+  std::vector<float> c(static_cast<size_t>(opts_.max_ctx) * half), s(c.size());
+  for (int pos = 0; pos < opts_.max_ctx; ++pos)
+    for (int i = 0; i < half; ++i) {
+      const double inv = std::pow(static_cast<double>(d.rope_theta), -2.0 * i / static_cast<double>(m.hd));
+      const double ang = static_cast<double>(pos) * inv;
+      c[static_cast<size_t>(pos) * half + i] = static_cast<float>(std::cos(ang));
+      s[static_cast<size_t>(pos) * half + i] = static_cast<float>(std::sin(ang));
+    }
+  check_cuda(cudaMalloc(&m.rcos, c.size() * 4), "rope");
+  check_cuda(cudaMalloc(&m.rsin, s.size() * 4), "rope");
+  check_cuda(cudaMemcpy(m.rcos, c.data(), c.size() * 4, cudaMemcpyHostToDevice), "rope");
+  check_cuda(cudaMemcpy(m.rsin, s.data(), s.size() * 4, cudaMemcpyHostToDevice), "rope");
+}
+
+const GemmPlan& Engine::plan(int n_out, int k, int t, int mode) {
+  const auto key = std::make_tuple(n_out, k, t, mode);
+  auto it = plans_.find(key);
+  if (it == plans_.end()) it = plans_.emplace(key, gemm_plan(n_out, k, t, mode, num_sms_)).first;
+  return it->second;
+}
+
+void Engine::init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool logits) {
+  ln.T_cap = T_cap;
+  ln.R_cap = R_cap;
+  ln.rows_cap = R_cap;
+  ln.seg_cap = R_cap + ln.rows_cap;
+  auto& A = ln.allocs;
+  ln.meta.row_tok = dalloc<int32_t>(A, T_cap);
+  ln.meta.row_slot = dalloc<int32_t>(A, T_cap);
+  ln.meta.row_pos = dalloc<int32_t>(A, T_cap);
+  ln.meta.req_slot = dalloc<int32_t>(A, R_cap);
+  ln.meta.req_qstart = dalloc<int32_t>(A, R_cap);
+  ln.meta.req_qlen = dalloc<int32_t>(A, R_cap);
+  ln.meta.req_kvlen = dalloc<int32_t>(A, R_cap);
+  ln.meta.seg = dalloc<int32_t>(A, static_cast<size_t>(ln.seg_cap) * 5);
+  ln.meta.row_ptr = dalloc<int32_t>(A, ln.rows_cap + 1);
+  ln.meta.row_seg = dalloc<int32_t>(A, ln.seg_cap);
+  ln.meta.req_seg0 = dalloc<int32_t>(A, R_cap);
+  ln.meta.req_nseg = dalloc<int32_t>(A, R_cap);
+  ln.meta.n_seg = dalloc<int32_t>(A, 1);
+  ln.h = dalloc<float>(A, static_cast<size_t>(T_cap) * m.D);
+  ln.xn = dalloc<bf16>(A, static_cast<size_t>(T_cap) * m.D);
+  ln.q = dalloc<float>(A, static_cast<size_t>(T_cap) * m.D);
+  ln.attn = dalloc<bf16>(A, static_cast<size_t>(T_cap) * m.D);
+  ln.act = dalloc<bf16>(A, static_cast<size_t>(T_cap) * m.F);
+  size_t part = 0;
+  const int shapes[4][2] = {{3 * m.D, m.D}, {m.D, m.D}, {2 * m.F, m.D}, {m.D, m.F}};
+  for (auto& sh : shapes) {
+    for (int t = std::min(256, T_cap);; t = std::min(t + 256, T_cap)) {
+      const GemmPlan& p = plan(sh[0], sh[1], t, kGemmPartial);
+      part = std::max(part, static_cast<size_t>(p.max_pieces) * t * sh[0]);
+      if (t == T_cap) break;
+    }
+  }
+  ln.part = dalloc<float>(A, part);
+  const size_t np = static_cast<size_t>(ln.seg_cap) * m.H * 17;
+  ln.aw.part_m = dalloc<float>(A, np);
+  ln.aw.part_l = dalloc<float>(A, np);
+  ln.aw.part_o = dalloc<float>(A, np * m.hd);
+  const int tiles = (m.V + 127) / 128;
+  ln.amax_val = dalloc<float>(A, static_cast<size_t>(tiles) * T_cap);
+  ln.amax_idx = dalloc<int32_t>(A, static_cast<size_t>(tiles) * T_cap);
+  if (logits) ln.logits = dalloc<float>(A, static_cast<size_t>(T_cap) * m.V);
+}
+
+// ------------------------------------------------------------------ forward
+// head_mode: 0 no lm_head (prefill), 1 argmax, 2 argmax + fp32 logits.
+void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, int head_mode) {
+  const int T = sh.T, D = m.D, F = m.F;
+  const bool pdl = opts_.use_pdl != 0;
+  const float eps = m.d.rms_eps;
+  launch_embed_norm(m.emb, ln.meta, T, D, eps, ln.h, ln.xn, s);
+  AttnGeom g{m.H, m.hd, opts_.max_requests, opts_.max_ctx, 0, static_cast<float>(1.0 / std::sqrt(double(m.hd))),
+             m.kc, m.vc};
+  GemmEpilogue ep;
+  ep.mode = kGemmPartial;
+  ep.part = ln.part;
+  AttnWork aw = ln.aw;
+  aw.qmax = sh.qmax;
+  for (int l = 0; l < m.L; ++l) {
+    const LayerW& w = m.layers[l];
+    g.layer = l;
+    const GemmPlan& pq = plan(3 * D, D, T, kGemmPartial);
+    check_cuda(gemm_launch(pq, w.qkv, ln.xn, ep, s, pdl), "gemm qkv");
+    launch_qkv_epilogue(ln.part, pq.map, ln.meta, T, g, m.rcos, m.rsin, ln.q, s);
+    launch_attention(m.tm_k, m.tm_v, ln.meta, sh.rows, sh.R, g, ln.q, aw, ln.attn, s);
+    const GemmPlan& po = plan(D, D, T, kGemmPartial);
+    check_cuda(gemm_launch(po, w.o, ln.attn, ep, s, pdl), "gemm o");
+    launch_resid_norm(ln.part, po.map, T, D, eps, ln.h, ln.xn, s);
+    const GemmPlan& pg = plan(2 * F, D, T, kGemmPartial);
+    check_cuda(gemm_launch(pg, w.gu, ln.xn, ep, s, pdl), "gemm gate_up");
+    launch_swiglu(ln.part, pg.map, T, F, ln.act, s);
+    const GemmPlan& pd = plan(D, F, T, kGemmPartial);
+    check_cuda(gemm_launch(pd, w.dn, ln.act, ep, s, pdl), "gemm down");
+    launch_resid_norm(ln.part, pd.map, T, D, eps, ln.h, ln.xn, s);
+  }
+  if (head_mode > 0) {
+    GemmEpilogue eh;
+    eh.mode = kGemmArgmax;
+    eh.amax_val = ln.amax_val;
+    eh.amax_idx = ln.amax_idx;
+    eh.logits = head_mode == 2 ? ln.logits : nullptr;
+    check_cuda(gemm_launch(plan(m.V, D, T, kGemmArgmax), m.head, ln.xn, eh, s, pdl), "gemm lm_head");
+  }
+  check_cuda(cudaGetLastError(), "forward launch");
+}
+
+// ------------------------------------------------------------------ engine
+Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n_ssm, const spin_engine_opts& opts)
+    : opts_(opts) {
+  if (n_ssm < 1 || n_ssm > kMaxSsm) fail(SPIN_CONFIG_ERROR, "engine: need 1..8 SSMs");
+  if (opts.max_requests < 1 || opts.max_requests > 1024) fail(SPIN_CONFIG_ERROR, "engine: max_requests in 1..1024");
+  if (opts.window < 1 || opts.window > 16) fail(SPIN_CONFIG_ERROR, "engine: window must be in 1..16");
+  if (opts.max_ctx < opts.window + 4) fail(SPIN_CONFIG_ERROR, "engine: max_ctx too small");
+  validate_desc(target, "target");
+  for (int j = 0; j < n_ssm; ++j) {
+    validate_desc(ssms[j], "ssm");
+    if (ssms[j].vocab != target.vocab) fail(SPIN_CONFIG_ERROR, "ssm vocabulary must match the target's");
+  }
+  check_cuda(cudaSetDevice(opts.device), "cudaSetDevice");
+  (void)cudaGetLastError();  // drop a stale non-sticky error left by an earlier caller
+  cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, opts.device);
+  check_cuda(cudaStreamCreateWithFlags(&sv_, cudaStreamNonBlocking), "stream");
+  ss_.resize(n_ssm);
+  for (auto& s : ss_) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  init_model(target_, target);
+  ssm_.resize(n_ssm);
+  for (int j = 0; j < n_ssm; ++j) init_model(ssm_[j], ssms[j]);
+  const int R = opts.max_requests, W = opts.window;
+  init_lane(tlane_, target_, std::max(R * (W + 1), kExtendRows), std::max(R, kExtendRows), opts.debug_logits != 0);
+  slane_.resize(n_ssm);
+  for (int j = 0; j < n_ssm; ++j)
+    init_lane(slane_[j], ssm_[j], std::max(2 * R, kExtendRows), std::max(R, kExtendRows), false);
+  st_.slots = R;
+  st_.ctx = opts.max_ctx;
+  st_.window = W;
+  st_.n_ssm = n_ssm;
+  check_cuda(cudaMalloc(&st_.tokens, static_cast<size_t>(R) * opts.max_ctx * 4), "tokens");
+  check_cuda(cudaMalloc(&st_.committed, R * 4), "committed");
+  check_cuda(cudaMalloc(&st_.ssm_len, static_cast<size_t>(n_ssm) * R * 4), "ssm_len");
+  check_cuda(cudaMalloc(&st_.drafts, static_cast<size_t>(R) * W * 4), "drafts");
+  check_cuda(cudaMemset(st_.tokens, 0, static_cast<size_t>(R) * opts.max_ctx * 4), "memset");
+  check_cuda(cudaMemset(st_.committed, 0, R * 4), "memset");
+  check_cuda(cudaMemset(st_.ssm_len, 0, static_cast<size_t>(n_ssm) * R * 4), "memset");
+  check_cuda(cudaMemset(st_.drafts, 0, static_cast<size_t>(R) * W * 4), "memset");
+  h_tokens_.assign(static_cast<size_t>(R) * opts.max_ctx, 0);
+  h_committed_.assign(R, 0);
+  h_ssm_len_.assign(static_cast<size_t>(n_ssm) * R, 0);
+  in_cap_ = static_cast<size_t>(3) * R + 16;
+  out_cap_ = static_cast<size_t>(R) * (3 + 2 * W + 1) + 16;
+  check_cuda(cudaMallocHost(&pin_in_, in_cap_ * 4), "pinned");
+  check_cuda(cudaMallocHost(&pin_out_, out_cap_ * 4), "pinned");
+  check_cuda(cudaMalloc(&d_in_, in_cap_ * 4), "in");
+  check_cuda(cudaMalloc(&d_out_, out_cap_ * 4), "out");
+  check_cuda(cudaMalloc(&d_emitted_, 8), "emitted");
+  check_cuda(cudaMemset(d_emitted_, 0, 8), "memset");
+  check_cuda(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
+  check_cuda(cudaEventCreate(&ev_start_), "event");
+  check_cuda(cudaEventCreate(&ev_draft_), "event");
+  check_cuda(cudaEventCreate(&ev_end_), "event");
+  ev_join_.resize(n_ssm);
+  for (auto& e : ev_join_) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  check_cuda(cudaStreamSynchronize(sv_), "init sync");
+}
+
+Engine::~Engine() {
+  cudaDeviceSynchronize();
+  for (auto& kv : rounds_) {
+    if (kv.second->exec) cudaGraphExecDestroy(kv.second->exec);
+    if (kv.second->graph) cudaGraphDestroy(kv.second->graph);
+  }
+  auto free_model = [](ModelDev& m) {
+    cudaFree(m.wbuf), cudaFree(m.kc), cudaFree(m.vc), cudaFree(m.rcos), cudaFree(m.rsin);
+  };
+  free_model(target_);
+  for (auto& m : ssm_) free_model(m);
+  for (void* p : tlane_.allocs) cudaFree(p);
+  for (auto& l : slane_)
+    for (void* p : l.allocs) cudaFree(p);
+  cudaFree(st_.tokens), cudaFree(st_.committed), cudaFree(st_.ssm_len), cudaFree(st_.drafts);
+  cudaFreeHost(pin_in_), cudaFreeHost(pin_out_), cudaFree(d_in_), cudaFree(d_out_), cudaFree(d_emitted_);
+  cudaEventDestroy(ev_fork_), cudaEventDestroy(ev_start_), cudaEventDestroy(ev_draft_), cudaEventDestroy(ev_end_);
+  for (auto& e : ev_join_) cudaEventDestroy(e);
+  for (auto& s : ss_) cudaStreamDestroy(s);
+  cudaStreamDestroy(sv_);
+}
+
+void Engine::sync_state_from_device() {
+  if (!mirror_stale_) return;
+  check_cuda(cudaStreamSynchronize(sv_), "sync");
+  check_cuda(cudaMemcpy(h_tokens_.data(), st_.tokens, h_tokens_.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+  check_cuda(cudaMemcpy(h_committed_.data(), st_.committed, h_committed_.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+  check_cuda(cudaMemcpy(h_ssm_len_.data(), st_.ssm_len, h_ssm_len_.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+  mirror_stale_ = false;
+}
+
+// Ragged extend of one model over positions [from, to) of each slot: the
+// prompt prefill, and the KV recompute of an SSM switch (switching_cost,
+// slot_engine.cpp:12-22). Rows are cut into virtual requests of <= 8 queries.
+void Engine::extend(int model, const std::vector<std::tuple<int, int, int>>& ranges) {
+  ModelDev& m = model < 0 ? target_ : ssm_[model];
+  Lane& ln = model < 0 ? tlane_ : slane_[model];
+  std::vector<int32_t> rt, rs, rp, qs_, ql, kv, sl;
+  auto flush = [&]() {
+    if (rt.empty()) return;
+    const int T = static_cast<int>(rt.size()), R = static_cast<int>(sl.size());
+    check_cuda(cudaMemcpyAsync(ln.meta.row_tok, rt.data(), T * 4, cudaMemcpyHostToDevice, sv_), "h2d");
+    check_cuda(cudaMemcpyAsync(ln.meta.row_slot, rs.data(), T * 4, cudaMemcpyHostToDevice, sv_), "h2d");
+    check_cuda(cudaMemcpyAsync(ln.meta.row_pos, rp.data(), T * 4, cudaMemcpyHostToDevice, sv_), "h2d");
+    check_cuda(cudaMemcpyAsync(ln.meta.req_slot, sl.data(), R * 4, cudaMemcpyHostToDevice, sv_), "h2d");
+    check_cuda(cudaMemcpyAsync(ln.meta.req_qstart, qs_.data(), R * 4, cudaMemcpyHostToDevice, sv_), "h2d");
+    check_cuda(cudaMemcpyAsync(ln.meta.req_qlen, ql.data(), R * 4, cudaMemcpyHostToDevice, sv_), "h2d");
+    check_cuda(cudaMemcpyAsync(ln.meta.req_kvlen, kv.data(), R * 4, cudaMemcpyHostToDevice, sv_), "h2d");
+    MetaArgs a{};
+    a.mode = kMetaExtend;
+    a.n_req = R;
+    a.width = R;
+    launch_meta(a, st_, ln.meta, sv_);
+    forward(m, ln, FwdShape{T, R, R, kExtendQ}, sv_, 0);
+    check_cuda(cudaStreamSynchronize(sv_), "extend");  // host vectors are reused
+    rt.clear(), rs.clear(), rp.clear(), qs_.clear(), ql.clear(), kv.clear(), sl.clear();
+  };
+  for (const auto& [slot, from, to] : ranges) {
+    for (int p0 = from; p0 < to; p0 += kExtendQ) {
+      const int p1 = std::min(to, p0 + kExtendQ);
+      if (static_cast<int>(rt.size()) + (p1 - p0) > kExtendRows) flush();
+      qs_.push_back(static_cast<int32_t>(rt.size()));
+      ql.push_back(p1 - p0);
+      kv.push_back(p1);
+      sl.push_back(slot);
+      for (int p = p0; p < p1; ++p) {
+        rt.push_back(h_tokens_[static_cast<size_t>(slot) * opts_.max_ctx + p]);
+        rs.push_back(slot);
+        rp.push_back(p);
+      }
+    }
+  }
+  flush();
+}
+
+void Engine::prefill(int n, const int32_t* slots, const int32_t* lens, const int32_t* prompts) {
+  sync_state_from_device();
+  std::vector<std::tuple<int, int, int>> ranges;
+  std::vector<char> seen(opts_.max_requests, 0);
+  size_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    const int s = slots[i], L = lens[i];
+    if (s < 0 || s >= opts_.max_requests) fail(SPIN_INPUT_ERROR, "prefill: slot out of range");
+    if (seen[s]) fail(SPIN_INPUT_ERROR, "prefill: duplicate slot");
+    seen[s] = 1;
+    if (L < 2) fail(SPIN_INPUT_ERROR, "prefill: prompts need at least 2 tokens");
+    if (L + opts_.window + 1 > opts_.max_ctx) fail(SPIN_CAPACITY_ERROR, "prefill: prompt exceeds max_ctx");
+    for (int p = 0; p < L; ++p) {
+      const int32_t tok = prompts[off + p];
+      if (tok < 0 || tok >= target_.V) fail(SPIN_INPUT_ERROR, "prefill: token id out of range");
+      h_tokens_[static_cast<size_t>(s) * opts_.max_ctx + p] = tok;
+    }
+    off += L;
+    h_committed_[s] = L;
+    ranges.emplace_back(s, 0, L - 1);
+  }
+  for (int i = 0; i < n; ++i) {
+    const int s = slots[i];
+    check_cuda(cudaMemcpyAsync(st_.tokens + static_cast<size_t>(s) * opts_.max_ctx,
+                               h_tokens_.data() + static_cast<size_t>(s) * opts_.max_ctx, lens[i] * 4,
+                               cudaMemcpyHostToDevice, sv_),
+               "h2d");
+    check_cuda(cudaMemcpyAsync(st_.committed + s, h_committed_.data() + s, 4, cudaMemcpyHostToDevice, sv_), "h2d");
+  }
+  extend(-1, ranges);
+  for (int j = 0; j < static_cast<int>(ssm_.size()); ++j) {
+    extend(j, ranges);
+    for (int i = 0; i < n; ++i) {
+      const int s = slots[i];
+      h_ssm_len_[static_cast<size_t>(j) * opts_.max_requests + s] = lens[i] - 1;
+      check_cuda(cudaMemcpyAsync(st_.ssm_len + static_cast<size_t>(j) * opts_.max_requests + s,
+                                 h_ssm_len_.data() + static_cast<size_t>(j) * opts_.max_requests + s, 4,
+                                 cudaMemcpyHostToDevice, sv_),
+                 "h2d");
+    }
+  }
+  check_cuda(cudaStreamSynchronize(sv_), "prefill");
+}
+
+void Engine::switch_ssm(int n, const int32_t* slots, const int32_t* ssm_of) {
+  sync_state_from_device();
+  for (int j = 0; j < static_cast<int>(ssm_.size()); ++j) {
+    std::vector<std::tuple<int, int, int>> ranges;
+    for (int i = 0; i < n; ++i) {
+      if (ssm_of[i] != j) continue;
+      const int s = slots[i];
+      const int need = h_committed_[s] - 2;
+      int32_t& len = h_ssm_len_[static_cast<size_t>(j) * opts_.max_requests + s];
+      if (len < need) {
+        ranges.emplace_back(s, len, need);
+        len = need;
+      }
+    }
+    if (ranges.empty()) continue;
+    extend(j, ranges);
+    for (const auto& r : ranges) {
+      const int s = std::get<0>(r);
+      check_cuda(cudaMemcpyAsync(st_.ssm_len + static_cast<size_t>(j) * opts_.max_requests + s,
+                                 h_ssm_len_.data() + static_cast<size_t>(j) * opts_.max_requests + s, 4,
+                                 cudaMemcpyHostToDevice, sv_),
+                 "h2d");
+    }
+    check_cuda(cudaStreamSynchronize(sv_), "switch");
+  }
+}
+
+Engine::RoundPlan& Engine::plan_round(int n, const int32_t* slots, const int32_t* ssm_of) {
+  const int M = static_cast<int>(ssm_.size());
+  std::vector<int> key(1 + M, 0);
+  for (int i = 0; i < n; ++i)
+    if (ssm_of[i] >= 0) ++key[0], ++key[1 + ssm_of[i]];
+  auto it = rounds_.find(key);
+  if (it != rounds_.end()) return *it->second;
+  auto p = std::make_unique<RoundPlan>();
+  p->key = key;
+  p->n_act = key[0];
+  p->n_ssm.assign(key.begin() + 1, key.end());
+  p->off_list = 0;
+  p->off_ssm_of = p->n_act;
+  int off = 2 * p->n_act;
+  for (int j = 0; j < M; ++j) {
+    p->off_ssm_list.push_back(off);
+    off += p->n_ssm[j];
+  }
+  p->in_ints = off;
+  p->out_ints = p->n_act * (3 + 2 * opts_.window + 1);
+  RoundPlan& ref = *p;
+  rounds_.emplace(key, std::move(p));
+  return ref;
+}
+
+// Timing events: inside a graph capture they must be external record nodes.
+void Engine::record_timing(cudaEvent_t ev, cudaStream_t s) {
+  if (capturing_)
+    check_cuda(cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal), "event");
+  else
+    check_cuda(cudaEventRecord(ev, s), "event");
+}
+
+// Enqueues one round on sv_ (+ SSM streams); used for capture and direct runs.
+void Engine::capture_round(RoundPlan& p) {
+  const int W = opts_.window, M = static_cast<int>(ssm_.size());
+  cudaStream_t s = sv_;
+  record_timing(ev_start_, s);
+  check_cuda(cudaMemcpyAsync(d_in_, pin_in_, p.in_ints * 4, cudaMemcpyHostToDevice, s), "h2d lists");
+  check_cuda(cudaEventRecord(ev_fork_, s), "event");
+  for (int j = 0; j < M; ++j) {
+    cudaStream_t sj = ss_[j];
+    check_cuda(cudaStreamWaitEvent(sj, ev_fork_, 0), "fork");
+    const int nj = p.n_ssm[j];
+    if (nj > 0) {
+      ModelDev& m = ssm_[j];
+      Lane& ln = slane_[j];
+      const int32_t* list = d_in_ + p.off_ssm_list[j];
+      const int tiles = (m.V + 127) / 128;
+      MetaArgs a{};
+      a.mode = kMetaDraft0;
+      a.n_req = nj;
+      a.list = list;
+      a.ssm = j;
+      a.width = nj;
+      launch_meta(a, st_, ln.meta, sj);
+      forward(m, ln, FwdShape{2 * nj, nj, nj, 2}, sj, 1);
+      int prev_t = 2 * nj, prev_q = 2;
+      for (int k = 1; k <= W; ++k) {
+        MetaArgs b{};
+        b.mode = k < W ? kMetaDraftK : kMetaCollect;
+        b.n_req = nj;
+        b.list = list;
+        b.step = k;
+        b.ssm = j;
+        b.width = nj;
+        b.amax_val = ln.amax_val;
+        b.amax_idx = ln.amax_idx;
+        b.amax_tiles = tiles;
+        b.prev_t = prev_t;
+        b.prev_qlen = prev_q;
+        launch_meta(b, st_, ln.meta, sj);
+        if (k < W) forward(m, ln, FwdShape{nj, nj, nj, 1}, sj, 1);
+        prev_t = nj, prev_q = 1;
+      }
+    }
+    check_cuda(cudaEventRecord(ev_join_[j], sj), "join");
+    check_cuda(cudaStreamWaitEvent(s, ev_join_[j], 0), "join");
+  }
+  record_timing(ev_draft_, s);
+  const int n = p.n_act;
+  if (n > 0) {
+    const int T = n * (W + 1);
+    const int width = opts_.pack_width > 0 ? std::min(opts_.pack_width, n) : n;
+    MetaArgs a{};
+    a.mode = kMetaVerify;
+    a.n_req = n;
+    a.list = d_in_ + p.off_list;
+    a.width = width;
+    a.padded = opts_.packing ? 0 : 1;
+    launch_meta(a, st_, tlane_.meta, s);
+    forward(target_, tlane_, FwdShape{T, n, a.padded ? n : width, W + 1}, s, opts_.debug_logits ? 2 : 1);
+    int32_t* o = d_out_;
+    launch_accept(tlane_.meta, n, W, d_in_ + p.off_list, d_in_ + p.off_ssm_of, tlane_.amax_val, tlane_.amax_idx,
+                  (target_.V + 127) / 128, T, st_, o, o + n, o + 2 * n, o + 3 * n, o + 3 * n + n * W, d_emitted_, s);
+    check_cuda(cudaMemcpyAsync(pin_out_, d_out_, p.out_ints * 4, cudaMemcpyDeviceToHost, s), "d2h outcome");
+  }
+  record_timing(ev_end_, s);
+  check_cuda(cudaGetLastError(), "round launch");
+}
+
+void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, spin_round_out* out) {
+  sync_state_from_device();
+  const int M = static_cast<int>(ssm_.size()), W = opts_.window, R = opts_.max_requests;
+  if (n < 0 || n > R) fail(SPIN_CAPACITY_ERROR, "round: batch exceeds max_requests");
+  std::vector<char> seen(R, 0);
+  for (int i = 0; i < n; ++i) {
+    const int s = slots[i];
+    if (s < 0 || s >= R) fail(SPIN_INPUT_ERROR, "round: slot out of range");
+    if (seen[s]) fail(SPIN_INPUT_ERROR, "round: duplicate slot");
+    seen[s] = 1;
+    if (ssm_of[i] < -1 || ssm_of[i] >= M) fail(SPIN_INPUT_ERROR, "round: unknown ssm in assignment");
+    if (ssm_of[i] >= 0) {
+      if (h_committed_[s] < 2) fail(SPIN_INPUT_ERROR, "round: slot was not prefilled");
+      if (h_committed_[s] + W + 1 > opts_.max_ctx) fail(SPIN_CAPACITY_ERROR, "round: slot context is full");
+    }
+  }
+  switch_ssm(n, slots, ssm_of);
+  RoundPlan& p = plan_round(n, slots, ssm_of);
+  // stage the lists
+  std::vector<int> act;
+  for (int i = 0; i < n; ++i)
+    if (ssm_of[i] >= 0) act.push_back(i);
+  for (int a = 0; a < p.n_act; ++a) {
+    pin_in_[p.off_list + a] = slots[act[a]];
+    pin_in_[p.off_ssm_of + a] = ssm_of[act[a]];
+  }
+  std::vector<int> fill(M, 0);
+  for (int i : act) pin_in_[p.off_ssm_list[ssm_of[i]] + fill[ssm_of[i]]++] = slots[i];
+  if (opts_.use_graphs) {
+    if (!p.exec) {
+      check_cuda(cudaStreamBeginCapture(sv_, cudaStreamCaptureModeRelaxed), "capture");
+      capturing_ = true;
+      capture_round(p);
+      capturing_ = false;
+      check_cuda(cudaStreamEndCapture(sv_, &p.graph), "capture");
+      check_cuda(cudaGraphInstantiate(&p.exec, p.graph, 0), "instantiate");
+    }
+    check_cuda(cudaGraphLaunch(p.exec, sv_), "graph launch");
+  } else {
+    capture_round(p);
+  }
+  check_cuda(cudaStreamSynchronize(sv_), "round");
+  float draft_ms = 0.f, total_ms = 0.f;
+  check_cuda(cudaEventElapsedTime(&draft_ms, ev_start_, ev_draft_), "event timing");
+  check_cuda(cudaEventElapsedTime(&total_ms, ev_start_, ev_end_), "event timing");
+  const int na = p.n_act;
+  const int32_t* acc = pin_out_;
+  const int32_t* bon = pin_out_ + na;
+  const int32_t* com = pin_out_ + 2 * na;
+  const int32_t* dr = pin_out_ + 3 * na;
+  const int32_t* tg = pin_out_ + 3 * na + na * W;
+  int a = 0;
+  for (int i = 0; i < n; ++i) {
+    const int s = slots[i];
+    if (ssm_of[i] < 0) {
+      if (out && out->accepted) out->accepted[i] = 0;
+      if (out && out->bonus_token) out->bonus_token[i] = -1;
+      if (out && out->committed) out->committed[i] = h_committed_[s];
+      continue;
+    }
+    const int c = h_committed_[s];
+    int32_t* hist = h_tokens_.data() + static_cast<size_t>(s) * opts_.max_ctx;
+    for (int k = 0; k < acc[a]; ++k) hist[c + k] = dr[static_cast<size_t>(a) * W + k];
+    hist[c + acc[a]] = bon[a];
+    h_committed_[s] = com[a];
+    for (int j = 0; j < M; ++j) {
+      int32_t& len = h_ssm_len_[static_cast<size_t>(j) * R + s];
+      if (j == ssm_of[i]) len = std::min(c + W - 1, c + acc[a]);
+    }
+    if (out) {
+      if (out->accepted) out->accepted[i] = acc[a];
+      if (out->bonus_token) out->bonus_token[i] = bon[a];
+      if (out->committed) out->committed[i] = com[a];
+      if (out->drafts) std::memcpy(out->drafts + static_cast<size_t>(i) * W, dr + static_cast<size_t>(a) * W, W * 4);
+      if (out->target_tokens)
+        std::memcpy(out->target_tokens + static_cast<size_t>(i) * (W + 1), tg + static_cast<size_t>(a) * (W + 1),
+                    (W + 1) * 4);
+    }
+    ++a;
+  }
+  last_verify_rows_ = na * (W + 1);
+  if (out) {
+    out->draft_ms = draft_ms;
+    out->round_ms = total_ms;
+    out->verify_ms = total_ms - draft_ms;
+  }
+}
+
+void Engine::run_rounds(int n, const int32_t* slots, const int32_t* ssm_of, int rounds, int64_t* emitted, float* ms) {
+  if (rounds < 1) fail(SPIN_INPUT_ERROR, "run_rounds: rounds must be >= 1");
+  sync_state_from_device();
+  const int W = opts_.window;
+  for (int i = 0; i < n; ++i) {
+    if (ssm_of[i] >= 0 && h_committed_[slots[i]] + rounds * (W + 1) + 1 > opts_.max_ctx)
+      fail(SPIN_CAPACITY_ERROR, "run_rounds: context would overflow max_ctx");
+  }
+  // one host-driven round first: validates, switches SSMs, captures the graph
+  spin_round_out tmp{};
+  round(n, slots, ssm_of, &tmp);
+  RoundPlan& p = plan_round(n, slots, ssm_of);
+  std::vector<unsigned long long> counts(rounds, 0);
+  unsigned long long* d_counts = nullptr;
+  check_cuda(cudaMalloc(&d_counts, rounds * 8), "counts");
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  check_cuda(cudaMemsetAsync(d_emitted_, 0, 8, sv_), "memset");
+  check_cuda(cudaEventRecord(a, sv_), "event");
+  for (int r = 0; r < rounds; ++r) {
+    if (opts_.use_graphs)
+      check_cuda(cudaGraphLaunch(p.exec, sv_), "graph launch");
+    else
+      capture_round(p);
+    check_cuda(cudaMemcpyAsync(d_counts + r, d_emitted_, 8, cudaMemcpyDeviceToDevice, sv_), "count");
+  }
+  check_cuda(cudaEventRecord(b, sv_), "event");
+  check_cuda(cudaStreamSynchronize(sv_), "rounds");
+  float t = 0.f;
+  cudaEventElapsedTime(&t, a, b);
+  check_cuda(cudaMemcpy(counts.data(), d_counts, rounds * 8, cudaMemcpyDeviceToHost), "d2h");
+  cudaFree(d_counts);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  unsigned long long prev = 0;
+  for (int r = 0; r < rounds; ++r) {
+    if (emitted) emitted[r] = static_cast<int64_t>(counts[r] - prev);
+    prev = counts[r];
+  }
+  if (ms) *ms = t;
+  mirror_stale_ = true;
+}
+
+void Engine::read_tokens(int slot, int32_t* tokens, int cap, int32_t* len) {
+  sync_state_from_device();
+  if (slot < 0 || slot >= opts_.max_requests) fail(SPIN_INPUT_ERROR, "read_tokens: slot out of range");
+  const int c = h_committed_[slot];
+  *len = c;
+  std::memcpy(tokens, h_tokens_.data() + static_cast<size_t>(slot) * opts_.max_ctx, std::min(c, cap) * 4);
+}
+
+void Engine::read_logits(float* logits, int64_t cap, int32_t* rows) {
+  if (!opts_.debug_logits) fail(SPIN_CONFIG_ERROR, "read_logits: engine created without debug_logits");
+  const int64_t need = static_cast<int64_t>(last_verify_rows_) * target_.V;
+  if (cap < need) fail(SPIN_SIZE_ERROR, "read_logits: buffer too small");
+  check_cuda(cudaMemcpy(logits, tlane_.logits, need * 4, cudaMemcpyDeviceToHost), "d2h logits");
+  *rows = last_verify_rows_;
+}
+
+}  // namespace spin

@@ -1,0 +1,105 @@
+// Device-resident verification engine behind the C ABI (spin_ctx).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <tuple>
+#include <vector>
+
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include "spin_c.h"
+
+namespace spin {
+
+// One model (target or SSM): synthetic bf16 weights, KV cache, RoPE tables.
+struct ModelDev {
+  spin_model_desc d{};
+  int D = 0, H = 0, hd = 0, F = 0, V = 0, L = 0;
+  bf16* wbuf = nullptr;
+  bf16* emb = nullptr;
+  bf16* head = nullptr;
+  std::vector<LayerW> layers;
+  bf16* kc = nullptr;
+  bf16* vc = nullptr;
+  float* rcos = nullptr;
+  float* rsin = nullptr;
+  CUtensorMap tm_k{}, tm_v{};
+  size_t weight_bytes = 0, kv_bytes = 0;
+};
+
+// Forward workspace of one model (one stream at a time).
+struct Lane {
+  int T_cap = 0, R_cap = 0, seg_cap = 0, rows_cap = 0;
+  FwdMeta meta{};
+  float* h = nullptr;
+  bf16 *xn = nullptr, *attn = nullptr, *act = nullptr;
+  float* q = nullptr;
+  float* part = nullptr;
+  AttnWork aw{};
+  float* amax_val = nullptr;
+  int32_t* amax_idx = nullptr;
+  float* logits = nullptr;
+  std::vector<void*> allocs;
+};
+
+struct FwdShape {
+  int T, R, rows, qmax;
+};
+
+class Engine {
+ public:
+  Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n_ssm, const spin_engine_opts& opts);
+  ~Engine();
+
+  void prefill(int n, const int32_t* slots, const int32_t* lens, const int32_t* prompts);
+  void round(int n, const int32_t* slots, const int32_t* ssm_of, spin_round_out* out);
+  void run_rounds(int n, const int32_t* slots, const int32_t* ssm_of, int rounds, int64_t* emitted, float* ms);
+  void switch_ssm(int n, const int32_t* slots, const int32_t* ssm_of);
+  void read_tokens(int slot, int32_t* tokens, int cap, int32_t* len);
+  void read_logits(float* logits, int64_t cap, int32_t* rows);
+
+ private:
+  struct RoundPlan;
+  void init_model(ModelDev& m, const spin_model_desc& d);
+  void init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool logits);
+  void forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, int head_mode);
+  void extend(int model, const std::vector<std::tuple<int, int, int>>& ranges);  // (slot, from, to)
+  RoundPlan& plan_round(int n, const int32_t* slots, const int32_t* ssm_of);
+  void capture_round(RoundPlan& p);
+  void record_timing(cudaEvent_t ev, cudaStream_t s);
+  bool capturing_ = false;
+  void sync_state_from_device();
+
+  spin_engine_opts opts_{};
+  int num_sms_ = 148;
+  ModelDev target_;
+  std::vector<ModelDev> ssm_;
+  Lane tlane_;
+  std::vector<Lane> slane_;
+  SlotState st_{};
+  cudaStream_t sv_ = nullptr;
+  std::vector<cudaStream_t> ss_;
+  std::map<std::tuple<int, int, int, int>, GemmPlan> plans_;
+  const GemmPlan& plan(int n_out, int k, int t, int mode);
+
+  // host mirror of the per-slot state
+  std::vector<int32_t> h_tokens_, h_committed_, h_ssm_len_;
+  bool mirror_stale_ = false;
+
+  // round staging (pinned) + device copies
+  int32_t* pin_in_ = nullptr;   // lists
+  int32_t* pin_out_ = nullptr;  // outcomes
+  int32_t* d_in_ = nullptr;
+  int32_t* d_out_ = nullptr;
+  unsigned long long* d_emitted_ = nullptr;
+  size_t in_cap_ = 0, out_cap_ = 0;
+  cudaEvent_t ev_fork_ = nullptr, ev_start_ = nullptr, ev_draft_ = nullptr, ev_end_ = nullptr;
+  std::vector<cudaEvent_t> ev_join_;
+  std::map<std::vector<int>, std::unique_ptr<RoundPlan>> rounds_;
+  int last_verify_rows_ = 0;
+};
+
+}  // namespace spin

@@ -1,0 +1,549 @@
+// Memory-bound kernels: per-forward metadata + device request decomposition,
+// embedding/RMSNorm, split-K reductions fused with RoPE + KV append, residual +
+// RMSNorm and SwiGLU, greedy acceptance with KV rollback, synthetic weights,
+// and the fp64 toy-mode packed attention operator.
+#include <cstdio>
+
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace spin {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ float sum_pieces(const float* __restrict__ part, const PieceMap& pm, int T, int n_out,
+                                            int t, int n) {
+  const int np = pm.pieces(t, n);
+  float acc = part[static_cast<size_t>(t) * n_out + n];
+  for (int s = 1; s < np; ++s) acc = __fadd_rn(acc, part[(static_cast<size_t>(s) * T + t) * n_out + n]);
+  return acc;
+}
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32, nw = blockDim.x / 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < nw; ++i) t += red[i];
+  return t;
+}
+
+__device__ __forceinline__ void amax_better(float& v, int& i, float ov, int oi) {
+  if (ov > v || (ov == v && oi < i)) {
+    v = ov;
+    i = oi;
+  }
+}
+
+// Token id of the argmax over all lm_head tiles for one row (lowest index on ties).
+__device__ int row_argmax_warp(const float* val, const int32_t* idx, int tiles, int T, int row) {
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int tl = threadIdx.x % 32; tl < tiles; tl += 32)
+    amax_better(bv, bi, val[static_cast<size_t>(tl) * T + row], idx[static_cast<size_t>(tl) * T + row]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(kFull, bv, o);
+    const int oi = __shfl_xor_sync(kFull, bi, o);
+    amax_better(bv, bi, ov, oi);
+  }
+  return bi;
+}
+
+// ------------------------------------------------------------------ meta
+constexpr int kMetaThreads = 256;
+constexpr int kMaxReq = 1024;
+
+__global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotState st, FwdMeta m) {
+  __shared__ int s_len[kMaxReq];
+  __shared__ int s_order[kMaxReq];
+  __shared__ int s_used[kMaxReq];
+  const int n = a.n_req;
+  const int tid = threadIdx.x;
+  const int warp = tid / 32, lane = tid % 32;
+  const int W = st.window;
+
+  ptx::grid_dep_wait();
+  // ---- collect the previous draft step's argmax (one warp per request)
+  if (a.mode == kMetaDraftK || a.mode == kMetaCollect) {
+    for (int r = warp; r < n; r += kMetaThreads / 32) {
+      const int row = r * a.prev_qlen + a.prev_qlen - 1;
+      const int tok = row_argmax_warp(a.amax_val, a.amax_idx, a.amax_tiles, a.prev_t, row);
+      if (lane == 0) st.drafts[static_cast<size_t>(a.list[r]) * W + a.step - 1] = tok;
+    }
+    __syncthreads();
+  }
+  if (a.mode == kMetaCollect) {
+    for (int r = tid; r < n; r += kMetaThreads) {
+      const int slot = a.list[r];
+      st.ssm_len[static_cast<size_t>(a.ssm) * st.slots + slot] = st.committed[slot] + W - 1;
+    }
+    ptx::grid_dep_launch();
+    return;
+  }
+  // ---- rows and requests
+  for (int r = tid; r < n; r += kMetaThreads) {
+    if (a.mode == kMetaExtend) {
+      s_len[r] = m.req_kvlen[r];
+      continue;
+    }
+    const int slot = a.list[r];
+    const int c = st.committed[slot];
+    const int32_t* hist = st.tokens + static_cast<size_t>(slot) * st.ctx;
+    const int32_t* dr = st.drafts + static_cast<size_t>(slot) * W;
+    int ql, kv;
+    if (a.mode == kMetaVerify) {
+      ql = W + 1;
+      kv = c + W;
+      const int q0 = r * ql;
+      for (int j = 0; j < ql; ++j) {
+        m.row_tok[q0 + j] = j == 0 ? hist[c - 1] : dr[j - 1];
+        m.row_slot[q0 + j] = slot;
+        m.row_pos[q0 + j] = c - 1 + j;
+      }
+    } else if (a.mode == kMetaDraft0) {
+      ql = 2;
+      kv = c;
+      for (int j = 0; j < 2; ++j) {
+        m.row_tok[2 * r + j] = hist[c - 2 + j];
+        m.row_slot[2 * r + j] = slot;
+        m.row_pos[2 * r + j] = c - 2 + j;
+      }
+    } else {  // DraftK
+      ql = 1;
+      kv = c + a.step;
+      m.row_tok[r] = dr[a.step - 1];
+      m.row_slot[r] = slot;
+      m.row_pos[r] = c - 1 + a.step;
+    }
+    m.req_slot[r] = slot;
+    m.req_qstart[r] = r * ql;
+    m.req_qlen[r] = ql;
+    m.req_kvlen[r] = kv;
+    s_len[r] = kv;
+  }
+  __syncthreads();
+
+  // ---- request decomposition (packing.cpp:16-103, restated for one warp)
+  const int rows = a.padded ? n : min(a.width > 0 ? a.width : n, n);
+  if (!a.padded) {
+    for (int i = tid; i < n; i += kMetaThreads) {  // stable rank by decreasing length
+      const int li = s_len[i];
+      int rank = 0;
+      for (int j = 0; j < n; ++j) rank += (s_len[j] > li) || (s_len[j] == li && j < i);
+      s_order[rank] = i;
+    }
+    for (int r = tid; r < rows; r += kMetaThreads) s_used[r] = 0;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int nseg = 0;
+    if (a.padded) {
+      int longest = 0;
+      for (int i = lane; i < n; i += 32) longest = max(longest, s_len[i]);
+      for (int o = 16; o > 0; o >>= 1) longest = max(longest, __shfl_xor_sync(kFull, longest, o));
+      for (int i = lane; i < n; i += 32) {
+        int32_t* sg = m.seg + 5 * i;
+        sg[0] = i, sg[1] = i, sg[2] = 0, sg[3] = longest, sg[4] = 0;
+      }
+      nseg = n;
+    } else {
+      long long total = 0;
+      for (int i = lane; i < n; i += 32) total += s_len[i];
+      for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
+      // With splitting allowed the first candidate L = ceil(total / rows)
+      // always fits (capacity >= total), so the reference's upward search
+      // stops at its first iteration.
+      const int L = static_cast<int>((total + rows - 1) / rows);
+      for (int k = 0; k < n; ++k) {
+        const int id = s_order[k];
+        const int need = s_len[id];
+        int home = -1;
+        for (int base = 0; base < rows && home < 0; base += 32) {
+          const int r = base + lane;
+          const unsigned mask = __ballot_sync(kFull, r < rows && L - s_used[r] >= need);
+          if (mask) home = base + __ffs(mask) - 1;
+        }
+        if (home >= 0) {
+          if (lane == 0) {
+            int32_t* sg = m.seg + 5 * nseg;
+            sg[0] = id, sg[1] = home, sg[2] = s_used[home], sg[3] = s_used[home] + need, sg[4] = 0;
+            s_used[home] += need;
+          }
+          ++nseg;
+          __syncwarp();
+          continue;
+        }
+        int remaining = need, done = 0;
+        for (int base = 0; base < rows && remaining > 0; base += 32) {
+          const int r = base + lane;
+          const int room = r < rows ? max(0, L - s_used[r]) : 0;
+          int incl = room;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int excl = incl - room;
+          const int take = min(room, max(0, remaining - excl));
+          const unsigned mask = __ballot_sync(kFull, take > 0);
+          if (take > 0) {
+            int32_t* sg = m.seg + 5 * (nseg + __popc(mask & ((1u << lane) - 1u)));
+            sg[0] = id, sg[1] = r, sg[2] = s_used[r], sg[3] = s_used[r] + take, sg[4] = done + excl;
+            s_used[r] += take;
+          }
+          nseg += __popc(mask);
+          const int chunk = __shfl_sync(kFull, incl, 31);
+          const int taken = min(remaining, chunk);
+          remaining -= taken;
+          done += taken;
+          __syncwarp();
+        }
+      }
+    }
+    if (lane == 0) *m.n_seg = nseg;
+  }
+  __syncthreads();
+  // ---- group segments by pack row (column order) and by request
+  if (tid == 0) {
+    const int nseg = *m.n_seg;
+    for (int r = 0; r < rows; ++r) s_used[r] = 0;
+    for (int r = 0; r < n; ++r) m.req_nseg[r] = 0;
+    for (int s = 0; s < nseg; ++s) {
+      ++s_used[m.seg[5 * s + 1]];
+      const int rq = m.seg[5 * s];
+      if (m.req_nseg[rq] == 0) m.req_seg0[rq] = s;
+      ++m.req_nseg[rq];
+    }
+    int acc = 0;
+    for (int r = 0; r < rows; ++r) {
+      m.row_ptr[r] = acc;
+      acc += s_used[r];
+      s_used[r] = m.row_ptr[r];
+    }
+    m.row_ptr[rows] = acc;
+    for (int s = 0; s < nseg; ++s) m.row_seg[s_used[m.seg[5 * s + 1]]++] = s;
+  }
+  ptx::grid_dep_launch();
+}
+
+// ------------------------------------------------------------------ norms
+constexpr int kRowThreads = 256;
+constexpr int kMaxPerThread = 32;  // D <= 8192
+
+__device__ __forceinline__ void rmsnorm_store(float (&v)[kMaxPerThread], int D, float eps, bf16* xn, float* red) {
+  float ss = 0.f;
+  for (int k = 0, i = threadIdx.x; i < D; i += kRowThreads, ++k) ss += v[k] * v[k];
+  const float tot = block_sum(ss, red);
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(tot, static_cast<float>(D)), eps)));
+  for (int k = 0, i = threadIdx.x; i < D; i += kRowThreads, ++k) xn[i] = __float2bfloat16_rn(__fmul_rn(v[k], inv));
+}
+
+__global__ void __launch_bounds__(kRowThreads) embed_norm_kernel(const bf16* __restrict__ emb, const int32_t* tok,
+                                                                 int D, float eps, float* h, bf16* xn) {
+  __shared__ float red[32];
+  ptx::grid_dep_wait();
+  const int t = blockIdx.x;
+  const bf16* e = emb + static_cast<size_t>(tok[t]) * D;
+  float v[kMaxPerThread];
+  for (int k = 0, i = threadIdx.x; i < D; i += kRowThreads, ++k) {
+    v[k] = __bfloat162float(e[i]);
+    h[static_cast<size_t>(t) * D + i] = v[k];
+  }
+  ptx::grid_dep_launch();
+  rmsnorm_store(v, D, eps, xn + static_cast<size_t>(t) * D, red);
+}
+
+__global__ void __launch_bounds__(kRowThreads) resid_norm_kernel(const float* __restrict__ part, PieceMap pm, int T,
+                                                                 int D, float eps, float* h, bf16* xn) {
+  __shared__ float red[32];
+  ptx::grid_dep_wait();
+  const int t = blockIdx.x;
+  float v[kMaxPerThread];
+  for (int k = 0, i = threadIdx.x; i < D; i += kRowThreads, ++k) {
+    const size_t o = static_cast<size_t>(t) * D + i;
+    v[k] = __fadd_rn(h[o], sum_pieces(part, pm, T, D, t, i));
+    h[o] = v[k];
+  }
+  ptx::grid_dep_launch();
+  rmsnorm_store(v, D, eps, xn + static_cast<size_t>(t) * D, red);
+}
+
+__global__ void __launch_bounds__(kRowThreads) swiglu_kernel(const float* __restrict__ part, PieceMap pm, int T, int F,
+                                                             bf16* act) {
+  ptx::grid_dep_wait();
+  const int t = blockIdx.x;
+  for (int f = threadIdx.x; f < F; f += kRowThreads) {
+    const float g = sum_pieces(part, pm, T, 2 * F, t, f);
+    const float u = sum_pieces(part, pm, T, 2 * F, t, F + f);
+    const float sg = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
+    act[static_cast<size_t>(t) * F + f] = __float2bfloat16_rn(__fmul_rn(sg, u));
+  }
+  ptx::grid_dep_launch();
+}
+
+// Split-K reduction of the fused QKV projection, RoPE (rotate-half) on q and k,
+// q -> fp32 (feeds only the CUDA-core attention), k/v -> bf16 KV cache at (layer, slot, head, pos).
+__global__ void __launch_bounds__(kRowThreads) qkv_epilogue_kernel(const float* __restrict__ part, PieceMap pm,
+                                                                   FwdMeta m, int T, AttnGeom g,
+                                                                   const float* __restrict__ rcos,
+                                                                   const float* __restrict__ rsin, float* q) {
+  ptx::grid_dep_wait();
+  const int t = blockIdx.x;
+  const int H = g.n_heads, hd = g.head_dim, half = hd / 2, D = H * hd, N = 3 * D;
+  const int slot = m.row_slot[t], pos = m.row_pos[t];
+  const float* cs = rcos + static_cast<size_t>(pos) * half;
+  const float* sn = rsin + static_cast<size_t>(pos) * half;
+  for (int pi = threadIdx.x; pi < H * half; pi += kRowThreads) {
+    const int hh = pi / half, i = pi % half;
+    const int nq = hh * hd + i;
+    const float q0 = sum_pieces(part, pm, T, N, t, nq), q1 = sum_pieces(part, pm, T, N, t, nq + half);
+    const float k0 = sum_pieces(part, pm, T, N, t, D + nq), k1 = sum_pieces(part, pm, T, N, t, D + nq + half);
+    const float v0 = sum_pieces(part, pm, T, N, t, 2 * D + nq), v1 = sum_pieces(part, pm, T, N, t, 2 * D + nq + half);
+    const float c = cs[i], s = sn[i];
+    float* qo = q + static_cast<size_t>(t) * D + nq;
+    qo[0] = __fsub_rn(__fmul_rn(q0, c), __fmul_rn(q1, s));
+    qo[half] = __fadd_rn(__fmul_rn(q1, c), __fmul_rn(q0, s));
+    if (slot >= 0) {
+      const size_t kv =
+          ((((static_cast<size_t>(g.layer) * g.slots + slot) * H + hh) * g.ctx) + pos) * hd + i;
+      g.k_cache[kv] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(k0, c), __fmul_rn(k1, s)));
+      g.k_cache[kv + half] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(k1, c), __fmul_rn(k0, s)));
+      g.v_cache[kv] = __float2bfloat16_rn(v0);
+      g.v_cache[kv + half] = __float2bfloat16_rn(v1);
+    }
+  }
+  ptx::grid_dep_launch();
+}
+
+// ------------------------------------------------------------------ accept
+// One warp per request: leading run of drafts equal to the target argmax
+// (model.cpp:110-134 semantics on real tokens), bonus = target token at the
+// first mismatch (slot_engine.cpp:140), commit and KV rollback by length
+// (slot_engine.cpp:151-156; model.hpp:26-28).
+__global__ void accept_kernel(FwdMeta m, int n_req, int W, const int32_t* list, const int32_t* ssm_of_req,
+                              const float* amax_val, const int32_t* amax_idx, int tiles, int T, SlotState st,
+                              int32_t* out_acc, int32_t* out_bonus, int32_t* out_comm, int32_t* out_drafts,
+                              int32_t* out_target, unsigned long long* emitted) {
+  ptx::grid_dep_wait();
+  const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (r >= n_req) return;
+  const int slot = list[r];
+  const int c = st.committed[slot];
+  const int q0 = m.req_qstart[r];
+  const int32_t* dr = st.drafts + static_cast<size_t>(slot) * W;
+  int32_t* hist = st.tokens + static_cast<size_t>(slot) * st.ctx;
+  int a = 0;
+  bool alive = true;
+  int bonus = -1;
+  for (int k = 0; k <= W; ++k) {
+    const int y = row_argmax_warp(amax_val, amax_idx, tiles, T, q0 + k);
+    if (out_target != nullptr && lane == 0) out_target[static_cast<size_t>(r) * (W + 1) + k] = y;
+    if (alive) {
+      if (k < W && dr[k] == y) {
+        ++a;
+      } else {
+        alive = false;
+        bonus = y;
+      }
+    }
+  }
+  if (lane == 0) {
+    for (int k = 0; k < a; ++k) hist[c + k] = dr[k];
+    hist[c + a] = bonus;
+    st.committed[slot] = c + a + 1;
+    const int j = ssm_of_req[r];
+    if (j >= 0) {
+      int32_t* len = st.ssm_len + static_cast<size_t>(j) * st.slots + slot;
+      if (*len > c + a) *len = c + a;
+    }
+    if (out_acc) out_acc[r] = a;
+    if (out_bonus) out_bonus[r] = bonus;
+    if (out_comm) out_comm[r] = c + a + 1;
+    if (out_drafts)
+      for (int k = 0; k < W; ++k) out_drafts[static_cast<size_t>(r) * W + k] = dr[k];
+    if (emitted) atomicAdd(emitted, static_cast<unsigned long long>(a + 1));
+  }
+}
+
+// ------------------------------------------------------------------ weights
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+__global__ void init_weights_kernel(bf16* w, int64_t rows, int64_t cols, uint64_t stream, float scale,
+                                    const bf16* emb, float g, int64_t vocab, int64_t a_inv, int64_t cc) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float u = static_cast<float>(splitmix64(stream + static_cast<uint64_t>(e)) >> 40);
+    const float r = __fsub_rn(__fmul_rn(u, 0x1.0p-23f), 1.0f);
+    const float a = __fmul_rn(r, scale);
+    if (emb == nullptr) {
+      w[e] = __float2bfloat16_rn(a);
+    } else {
+      const int64_t row = e / cols, col = e % cols;
+      const int64_t src = (a_inv * (((row - cc) % vocab + vocab) % vocab)) % vocab;
+      const float b = __fmul_rn(g, __bfloat162float(emb[src * cols + col]));
+      w[e] = __float2bfloat16_rn(__fadd_rn(a, b));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ toy attention (fp64)
+// Block per pack row: for each segment and query, the segment's own max and
+// exp-sum (split-KV partial); the combine merges them under the request's
+// shared max, which is the aggregation of attention.cpp:128-157.
+__global__ void toy_attn_kernel(const double* q, const double* k, const double* v, const int32_t* q_off,
+                                const int32_t* kv_off, const int32_t* q_rows, const int32_t* seg,
+                                const int32_t* row_ptr, const int32_t* row_seg, int dim, int qmax, double* pm,
+                                double* pl, double* po) {
+  extern __shared__ double sh[];
+  double* red = sh;  // [blockDim]
+  const int row = blockIdx.x;
+  for (int si = row_ptr[row]; si < row_ptr[row + 1]; ++si) {
+    const int s = row_seg[si];
+    const int rq = seg[5 * s], len = seg[5 * s + 3] - seg[5 * s + 2], off = seg[5 * s + 4];
+    const double* kk = k + (static_cast<size_t>(kv_off[rq]) + off) * dim;
+    const double* vv = v + (static_cast<size_t>(kv_off[rq]) + off) * dim;
+    for (int j = 0; j < q_rows[rq]; ++j) {
+      const double* qq = q + (static_cast<size_t>(q_off[rq]) + j) * dim;
+      double mx = -INFINITY;
+      for (int key = threadIdx.x; key < len; key += blockDim.x) {
+        double d = 0.0;
+        for (int c = 0; c < dim; ++c) d += qq[c] * kk[static_cast<size_t>(key) * dim + c];
+        mx = fmax(mx, d);
+      }
+      red[threadIdx.x] = mx;
+      __syncthreads();
+      for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+        __syncthreads();
+      }
+      mx = red[0];
+      __syncthreads();
+      // each thread owns output columns; sums over keys are sequential (fixed order)
+      const size_t base = (static_cast<size_t>(s) * qmax + j);
+      double den = 0.0;
+      for (int c = threadIdx.x; c < dim; c += blockDim.x) {
+        double num = 0.0;
+        den = 0.0;
+        for (int key = 0; key < len; ++key) {
+          double d = 0.0;
+          for (int cc = 0; cc < dim; ++cc) d += qq[cc] * kk[static_cast<size_t>(key) * dim + cc];
+          const double f = exp(d - mx);
+          den += f;
+          num += f * vv[static_cast<size_t>(key) * dim + c];
+        }
+        po[base * dim + c] = num;
+      }
+      if (threadIdx.x == 0) {
+        if (dim <= 0) den = 0.0;
+        pm[base] = mx;
+      }
+      if (threadIdx.x == 0 && dim > 0) pl[base] = den;
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void toy_combine_kernel(const int32_t* q_off, const int32_t* q_rows, const int32_t* req_seg0,
+                                   const int32_t* req_nseg, int dim, int qmax, const double* pm, const double* pl,
+                                   const double* po, double* out) {
+  const int rq = blockIdx.x;
+  for (int j = 0; j < q_rows[rq]; ++j) {
+    double M = -INFINITY;
+    for (int s = req_seg0[rq]; s < req_seg0[rq] + req_nseg[rq]; ++s) M = fmax(M, pm[static_cast<size_t>(s) * qmax + j]);
+    double L = 0.0;
+    for (int s = req_seg0[rq]; s < req_seg0[rq] + req_nseg[rq]; ++s)
+      L += pl[static_cast<size_t>(s) * qmax + j] * exp(pm[static_cast<size_t>(s) * qmax + j] - M);
+    for (int c = threadIdx.x; c < dim; c += blockDim.x) {
+      double num = 0.0;
+      for (int s = req_seg0[rq]; s < req_seg0[rq] + req_nseg[rq]; ++s)
+        num += po[(static_cast<size_t>(s) * qmax + j) * dim + c] * exp(pm[static_cast<size_t>(s) * qmax + j] - M);
+      out[(static_cast<size_t>(q_off[rq]) + j) * dim + c] = num / L;
+    }
+  }
+}
+
+template <typename K, typename... Args>
+void launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+}  // namespace
+
+void launch_meta(const MetaArgs& a, const SlotState& st, const FwdMeta& m, cudaStream_t s) {
+  launch_pdl(meta_kernel, dim3(1), dim3(kMetaThreads), 0, s, a, st, m);
+}
+
+void launch_embed_norm(const bf16* emb, const FwdMeta& m, int T, int D, float eps, float* h, bf16* xn,
+                       cudaStream_t s) {
+  launch_pdl(embed_norm_kernel, dim3(T), dim3(kRowThreads), 0, s, emb, static_cast<const int32_t*>(m.row_tok), D, eps,
+             h, xn);
+}
+
+void launch_qkv_epilogue(const float* part, const PieceMap& pm, const FwdMeta& m, int T, const AttnGeom& g,
+                         const float* rcos, const float* rsin, float* q, cudaStream_t s) {
+  launch_pdl(qkv_epilogue_kernel, dim3(T), dim3(kRowThreads), 0, s, part, pm, m, T, g, rcos, rsin, q);
+}
+
+void launch_resid_norm(const float* part, const PieceMap& pm, int T, int D, float eps, float* h, bf16* xn,
+                       cudaStream_t s) {
+  launch_pdl(resid_norm_kernel, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, D, eps, h, xn);
+}
+
+void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* act, cudaStream_t s) {
+  launch_pdl(swiglu_kernel, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, F, act);
+}
+
+void launch_accept(const FwdMeta& m, int n_req, int window, const int32_t* list, const int32_t* ssm_of_req,
+                   const float* amax_val, const int32_t* amax_idx, int tiles, int T, const SlotState& st,
+                   int32_t* out_accepted, int32_t* out_bonus, int32_t* out_committed, int32_t* out_drafts,
+                   int32_t* out_target, unsigned long long* emitted, cudaStream_t s) {
+  const int per_block = 4;
+  launch_pdl(accept_kernel, dim3((n_req + per_block - 1) / per_block), dim3(32 * per_block), 0, s, m, n_req, window,
+             list, ssm_of_req, amax_val, amax_idx, tiles, T, st, out_accepted, out_bonus, out_committed, out_drafts,
+             out_target, emitted);
+}
+
+void launch_init_weights(bf16* w, int64_t rows, int64_t cols, uint64_t stream, float scale, const bf16* emb,
+                         float planted_g, int64_t vocab, int64_t A_inv, int64_t Cc, cudaStream_t s) {
+  init_weights_kernel<<<148 * 8, 256, 0, s>>>(w, rows, cols, stream, scale, emb, planted_g, vocab, A_inv, Cc);
+}
+
+void launch_toy_attention(const double* q, const double* k, const double* v, const int32_t* q_off,
+                          const int32_t* kv_off, const int32_t* q_rows, const int32_t* seg, int n_seg,
+                          const int32_t* row_ptr, const int32_t* row_seg, int n_rows, const int32_t* req_seg0,
+                          const int32_t* req_nseg, int n_req, int dim, int qmax, double* part_m, double* part_l,
+                          double* part_o, double* out, cudaStream_t s) {
+  (void)n_seg;
+  const int threads = 128;
+  if (n_rows > 0)
+    toy_attn_kernel<<<n_rows, threads, threads * sizeof(double), s>>>(q, k, v, q_off, kv_off, q_rows, seg, row_ptr,
+                                                                      row_seg, dim, qmax, part_m, part_l, part_o);
+  if (n_req > 0)
+    toy_combine_kernel<<<n_req, 128, 0, s>>>(q_off, q_rows, req_seg0, req_nseg, dim, qmax, part_m, part_l, part_o,
+                                             out);
+}
+
+}  // namespace spin

@@ -1,0 +1,118 @@
+// Memory-bound kernels of the verification / draft forward pass and the
+// device-side bookkeeping (request decomposition, acceptance, KV rollback).
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "gemm.cuh"
+
+namespace spin {
+
+using bf16 = __nv_bfloat16;
+
+constexpr int kMaxSsm = 8;
+
+// Per-forward metadata (device pointers). Rows are the token rows of the
+// forward; requests own a contiguous range of rows (their queries); segments
+// are the request-decomposition work items of the packed attention.
+struct FwdMeta {
+  int32_t* row_tok;   // [T]
+  int32_t* row_slot;  // [T]  KV slot, -1: padding row (no KV write)
+  int32_t* row_pos;   // [T]  absolute position
+  int32_t* req_slot;  // [R]
+  int32_t* req_qstart;
+  int32_t* req_qlen;
+  int32_t* req_kvlen;  // keys visible to the last query = last position + 1
+  int32_t* seg;        // [S][5] request, row, col_start, col_end, token_offset (pack order)
+  int32_t* row_ptr;    // [W+1] CSR over pack rows into row_seg
+  int32_t* row_seg;    // [S] segment ids grouped by pack row, column order
+  int32_t* req_seg0;   // [R] first segment (segments of a request are contiguous)
+  int32_t* req_nseg;   // [R]
+  int32_t* n_seg;      // [1]
+};
+
+// Persistent per-slot state on the device.
+struct SlotState {
+  int32_t* tokens;     // [slots][ctx] committed token history
+  int32_t* committed;  // [slots]
+  int32_t* ssm_len;    // [n_ssm][slots] valid KV positions of each SSM cache
+  int32_t* drafts;     // [slots][window]
+  int32_t slots, ctx, window, n_ssm;
+};
+
+enum MetaMode : int {
+  kMetaVerify = 0,   // rows: pending token + window drafts per request
+  kMetaDraft0 = 1,   // rows: last two committed tokens per request
+  kMetaDraftK = 2,   // rows: previous draft; collects previous step's argmax first
+  kMetaCollect = 3,  // only collects the final draft step's argmax
+  kMetaExtend = 4,   // rows/requests uploaded by the host; only packs
+};
+
+struct MetaArgs {
+  int mode;
+  int n_req;
+  const int32_t* list;  // [n_req] request slots in batch order
+  int step;             // draft step k (DraftK / Collect: step whose draft is collected = step-1)
+  int ssm;              // SSM index for ssm_len bookkeeping
+  int width;            // pack width (0: n_req)
+  int padded;           // 1: one row per request padded to the longest (no decomposition)
+  // previous lm_head argmax (DraftK / Collect)
+  const float* amax_val;
+  const int32_t* amax_idx;
+  int amax_tiles;
+  int prev_t;     // rows of the previous forward
+  int prev_qlen;  // rows per request in the previous forward
+};
+
+struct LayerW {
+  const bf16 *qkv, *o, *gu, *dn;
+};
+
+struct AttnGeom {
+  int n_heads, head_dim, slots, ctx, layer;
+  float scale;
+  bf16* k_cache;  // [layers][slots][heads][ctx][hd]
+  bf16* v_cache;
+};
+
+void launch_meta(const MetaArgs& a, const SlotState& st, const FwdMeta& m, cudaStream_t s);
+void launch_embed_norm(const bf16* emb, const FwdMeta& m, int T, int D, float eps, float* h, bf16* xn,
+                       cudaStream_t s);
+void launch_qkv_epilogue(const float* part, const PieceMap& pm, const FwdMeta& m, int T, const AttnGeom& g,
+                         const float* rcos, const float* rsin, float* q, cudaStream_t s);
+void launch_resid_norm(const float* part, const PieceMap& pm, int T, int D, float eps, float* h, bf16* xn,
+                       cudaStream_t s);
+void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* act, cudaStream_t s);
+
+// Packed ragged causal attention over the KV cache (TMA-staged tiles) and the
+// shared-max combine of segment partials.
+struct AttnWork {
+  float* part_m;  // [seg_cap][H][qmax]
+  float* part_l;
+  float* part_o;  // [seg_cap][H][qmax][hd]
+  int qmax;
+};
+void launch_attention(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m, int n_rows, int n_req,
+                      const AttnGeom& g, const float* q, const AttnWork& w, bf16* out, cudaStream_t s);
+
+void launch_accept(const FwdMeta& m, int n_req, int window, const int32_t* list, const int32_t* ssm_of_req,
+                   const float* amax_val, const int32_t* amax_idx, int tiles, int T, const SlotState& st,
+                   int32_t* out_accepted, int32_t* out_bonus, int32_t* out_committed, int32_t* out_drafts,
+                   int32_t* out_target, unsigned long long* emitted, cudaStream_t s);
+
+void launch_init_weights(bf16* w, int64_t rows, int64_t cols, uint64_t stream, float scale, const bf16* emb,
+                         float planted_g, int64_t vocab, int64_t A_inv, int64_t Cc, cudaStream_t s);
+
+// Toy-mode packed attention for the decomposed_attention operator (K/V laid
+// out per request, any dim, scale 1, no causal mask).
+// Computed in fp64 on the device (the reference operator is fp64).
+void launch_toy_attention(const double* q, const double* k, const double* v, const int32_t* q_off,
+                          const int32_t* kv_off, const int32_t* q_rows, const int32_t* seg, int n_seg,
+                          const int32_t* row_ptr, const int32_t* row_seg, int n_rows, const int32_t* req_seg0,
+                          const int32_t* req_nseg, int n_req, int dim, int qmax, double* part_m, double* part_l,
+                          double* part_o, double* out, cudaStream_t s);
+
+}  // namespace spin
