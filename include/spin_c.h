@@ -156,6 +156,27 @@ spin_status spin_read_logits(spin_ctx* ctx, float* logits, int64_t cap, int32_t*
  * recomputed up to the committed prefix (switching_cost, slot_engine.cpp:12-22). */
 spin_status spin_switch_ssm(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of);
 
+/* Profiling: one round run without graphs, CUDA events around every launch.
+ * Arrays have SPIN_PROF_CLASSES entries indexed by class: device ms, algorithmic
+ * bytes (GEMM classes: weights + activations in + out), and launch counts. */
+#define SPIN_PROF_CLASSES 9
+enum {
+  SPIN_PROF_TARGET_GEMM = 0,
+  SPIN_PROF_TARGET_HEAD = 1,
+  SPIN_PROF_TARGET_ATTN = 2,
+  SPIN_PROF_TARGET_EPI = 3,
+  SPIN_PROF_SSM_GEMM = 4,
+  SPIN_PROF_SSM_HEAD = 5,
+  SPIN_PROF_SSM_ATTN = 6,
+  SPIN_PROF_SSM_EPI = 7,
+  SPIN_PROF_META = 8
+};
+spin_status spin_profile_round(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of, double* ms,
+                               double* bytes, int64_t* launches);
+/* Kernels launched per round for this assignment shape (after a first round). */
+spin_status spin_round_launches(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
+                                int64_t* launches);
+
 /* ------------------------------------------------------------------------
  * Kernel-level entry points (device pointers; stream = cudaStream_t or NULL).
  * Used by the parity tests to check each kernel against a reference of the

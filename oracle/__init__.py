@@ -70,6 +70,7 @@ def load_oracle() -> C.CDLL:
         lib.so_engine_switch.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         lib.so_engine_read_tokens.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]
         lib.so_set_gemm_lanes.argtypes = [C.c_int]
+        lib.so_engine_last_timing.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         lib.so_debug_layer.argtypes = [C.c_int, C.c_void_p, C.c_int]
         lib.so_debug_inner.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int]
         lib.so_engine_verify_seconds.restype = C.c_double
@@ -160,6 +161,11 @@ class OracleEngine:
         if want_logits:
             out["logits"] = logits.reshape(act * (W + 1), self.vocab)
         return out
+
+    def last_timing(self):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        self.lib.so_engine_last_timing(C.byref(a), C.byref(b), C.byref(c))
+        return a.value, b.value, c.value
 
     def tokens(self, slot):
         import numpy as np

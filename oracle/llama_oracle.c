@@ -205,29 +205,64 @@ static void model_destroy(model* m) {
 static int g_lanes = 16;
 void so_set_gemm_lanes(int lanes) { g_lanes = lanes == 8 ? 8 : 16; }
 
-/* Y[t][n] = sum_k X[t][k] W[n][k]; fp32 with 16 fixed partial sums. */
+/* Y[t][n] = sum_k X[t][k] W[n][k]; fp32, each output accumulated in 16 fixed
+ * partial sums (k mod 16) reduced by a fixed tree. Four weight rows share each
+ * pass over an activation row; the per-output order is independent of that. */
+static float reduce16(float* acc) {
+  for (int s = 8; s > 0; s >>= 1)
+    for (int j = 0; j < s; ++j) acc[j] += acc[j + s];
+  return acc[0];
+}
+
 static void gemm(const float* X, int T, int K, const uint16_t* W, int N, float* Y) {
+  const int nblk = (N + 3) / 4;
 #pragma omp parallel
   {
-    float* wr = (float*)malloc(sizeof(float) * (K + 16));
-#pragma omp for schedule(static)
-    for (int n = 0; n < N; ++n) {
-      const uint16_t* w = W + (size_t)n * K;
-      for (int k = 0; k < K; ++k) wr[k] = bf2f(w[k]);
+    float* wr = (float*)malloc(sizeof(float) * 4 * (K + 16));
+#pragma omp for schedule(dynamic, 4)
+    for (int nb = 0; nb < nblk; ++nb) {
+      const int n0 = nb * 4, nn = N - n0 < 4 ? N - n0 : 4;
+      for (int r = 0; r < nn; ++r)
+        for (int k = 0; k < K; ++k) wr[r * (K + 16) + k] = bf2f(W[(size_t)(n0 + r) * K + k]);
       for (int t = 0; t < T; ++t) {
         const float* x = X + (size_t)t * K;
-        float acc[16] = {0};
-        int k = 0;
-        if (g_lanes == 16) {
+        if (g_lanes == 16 && nn == 4) {
+          float a0[16] = {0}, a1[16] = {0}, a2[16] = {0}, a3[16] = {0};
+          const float *w0 = wr, *w1 = wr + (K + 16), *w2 = wr + 2 * (K + 16), *w3 = wr + 3 * (K + 16);
+          int k = 0;
           for (; k + 16 <= K; k += 16)
-            for (int j = 0; j < 16; ++j) acc[j] += x[k + j] * wr[k + j];
-          for (int j = 0; k < K; ++k, ++j) acc[j] += x[k] * wr[k];
-        } else {
-          for (; k < K; ++k) acc[k & 7] += x[k] * wr[k];
+            for (int j = 0; j < 16; ++j) {
+              const float xv = x[k + j];
+              a0[j] += xv * w0[k + j];
+              a1[j] += xv * w1[k + j];
+              a2[j] += xv * w2[k + j];
+              a3[j] += xv * w3[k + j];
+            }
+          for (int j = 0; k < K; ++k, ++j) {
+            a0[j] += x[k] * w0[k];
+            a1[j] += x[k] * w1[k];
+            a2[j] += x[k] * w2[k];
+            a3[j] += x[k] * w3[k];
+          }
+          Y[(size_t)t * N + n0] = reduce16(a0);
+          Y[(size_t)t * N + n0 + 1] = reduce16(a1);
+          Y[(size_t)t * N + n0 + 2] = reduce16(a2);
+          Y[(size_t)t * N + n0 + 3] = reduce16(a3);
+          continue;
         }
-        for (int s = 8; s > 0; s >>= 1)
-          for (int j = 0; j < s; ++j) acc[j] += acc[j + s];
-        Y[(size_t)t * N + n] = acc[0];
+        for (int r = 0; r < nn; ++r) {
+          const float* w = wr + r * (K + 16);
+          float acc[16] = {0};
+          int k = 0;
+          if (g_lanes == 16) {
+            for (; k + 16 <= K; k += 16)
+              for (int j = 0; j < 16; ++j) acc[j] += x[k + j] * w[k + j];
+            for (int j = 0; k < K; ++k, ++j) acc[j] += x[k] * w[k];
+          } else {
+            for (; k < K; ++k) acc[k & 7] += x[k] * w[k];
+          }
+          Y[(size_t)t * N + n0 + r] = reduce16(acc);
+        }
       }
     }
     free(wr);
@@ -258,8 +293,16 @@ void so_debug_layer(int layer, float* out, int n) {
   memcpy(out, g_dbg[layer], sizeof(float) * (n < 4096 ? n : 4096));
 }
 
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+static double g_t_blocks = 0.0, g_t_head = 0.0; /* seconds spent in the last forward */
+
 static void model_forward(model* m, int T, const int* tok, const int* slot, const int* pos, int* amax,
                           float* logits) {
+  const double t0 = now_s();
   const so_model_desc* d = &m->d;
   const int D = d->d_model, H = d->n_heads, hd = d->head_dim, F = d->ffn, V = d->vocab, half = hd / 2;
   const float scale = (float)(1.0 / sqrt((double)hd));
@@ -341,6 +384,7 @@ static void model_forward(model* m, int T, const int* tok, const int* slot, cons
     if (l < 64) memcpy(g_dbg[l], h, sizeof(float) * ((size_t)T * D < 4096 ? (size_t)T * D : 4096));
   }
   g_dbg_n = d->n_layers;
+  const double t1 = now_s();
   rmsnorm_bf16(h, T, D, d->rms_eps, x);
   float* lg = logits ? logits : (float*)malloc(sizeof(float) * (size_t)T * V);
   gemm(x, T, D, m->head, V, lg);
@@ -353,6 +397,8 @@ static void model_forward(model* m, int T, const int* tok, const int* slot, cons
   }
   if (!logits) free(lg);
   free(h), free(x), free(y), free(q);
+  g_t_blocks = t1 - t0;
+  g_t_head = now_s() - t1;
 }
 
 /* ------------------------------------------------------------------- engine */
@@ -442,9 +488,15 @@ int so_engine_switch(so_engine* e, int n, const int* slots, const int* ssm_of) {
   return 0;
 }
 
+static double g_round_draft = 0.0, g_round_vblocks = 0.0, g_round_vhead = 0.0;
+void so_engine_last_timing(double* draft_s, double* verify_blocks_s, double* verify_head_s) {
+  *draft_s = g_round_draft, *verify_blocks_s = g_round_vblocks, *verify_head_s = g_round_vhead;
+}
+
 int so_engine_round(so_engine* e, int n, const int* slots, const int* ssm_of, int* accepted, int* bonus,
                     int* committed, int* drafts, int* target_tokens, float* logits) {
   const int g = e->window;
+  const double r0 = now_s();
   for (int i = 0; i < n; ++i) {
     if (ssm_of[i] < -1 || ssm_of[i] >= e->n_ssm) return 3;
     if (ssm_of[i] >= 0 && e->committed[slots[i]] + g + 1 > e->ctx) return 2;
@@ -485,6 +537,8 @@ int so_engine_round(so_engine* e, int n, const int* slots, const int* ssm_of, in
     }
     free(idx), free(tok), free(sl), free(ps), free(am);
   }
+  g_round_draft = now_s() - r0;
+  g_round_vblocks = g_round_vhead = 0.0;
   /* ---- verify: rows (pending, d_1..d_g) at positions c-1 .. c+g-1 */
   int act = 0;
   for (int i = 0; i < n; ++i) act += ssm_of[i] >= 0;
@@ -501,7 +555,11 @@ int so_engine_round(so_engine* e, int n, const int* slots, const int* ssm_of, in
       ++k;
     }
   }
-  if (T > 0) model_forward(e->target, T, tok, sl, ps, am, logits);
+  if (T > 0) {
+    model_forward(e->target, T, tok, sl, ps, am, logits);
+    g_round_vblocks = g_t_blocks;
+    g_round_vhead = g_t_head;
+  }
   /* ---- accept: leading run of drafts equal to the target argmax, plus bonus */
   k = 0;
   for (int i = 0; i < n; ++i) {

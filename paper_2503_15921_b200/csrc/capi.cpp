@@ -295,6 +295,22 @@ spin_status spin_read_logits(spin_ctx* ctx, float* logits, int64_t cap, int32_t*
   });
 }
 
+spin_status spin_profile_round(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of, double* ms,
+                               double* bytes, int64_t* launches) {
+  return guarded([&] {
+    if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
+    ctx->eng->profile_round(n, slots, ssm_of, ms, bytes, launches);
+  });
+}
+
+spin_status spin_round_launches(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
+                                int64_t* launches) {
+  return guarded([&] {
+    if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
+    *launches = ctx->eng->launches_per_round(n, slots, ssm_of);
+  });
+}
+
 spin_status spin_switch_ssm(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of) {
   return guarded([&] {
     if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");

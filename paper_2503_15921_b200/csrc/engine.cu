@@ -78,6 +78,7 @@ struct Engine::RoundPlan {
   int off_list = 0, off_ssm_of = 0;
   std::vector<int> off_ssm_list;
   int in_ints = 0, out_ints = 0;
+  int64_t launches = 0;  // kernels per round
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
 };
@@ -206,12 +207,33 @@ void Engine::init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool l
 }
 
 // ------------------------------------------------------------------ forward
+// Per-launch accounting: launch count (gpu_launches in bench.py) and, in a
+// profiling round, CUDA events around each launch grouped by kernel class.
+void Engine::prof_begin(int cat, cudaStream_t s) {
+  ++launches_;
+  if (!prof_ || capturing_) return;
+  ProfRec r{cat, nullptr, nullptr, 0.0};
+  check_cuda(cudaEventCreate(&r.a), "event");
+  check_cuda(cudaEventCreate(&r.b), "event");
+  check_cuda(cudaEventRecord(r.a, s), "event");
+  prof_recs_.push_back(r);
+}
+void Engine::prof_end(cudaStream_t s, double bytes) {
+  if (!prof_ || capturing_) return;
+  check_cuda(cudaEventRecord(prof_recs_.back().b, s), "event");
+  prof_recs_.back().bytes = bytes;
+}
+
 // head_mode: 0 no lm_head (prefill), 1 argmax, 2 argmax + fp32 logits.
 void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, int head_mode) {
   const int T = sh.T, D = m.D, F = m.F;
   const bool pdl = opts_.use_pdl != 0;
   const float eps = m.d.rms_eps;
+  const int base = (&m == &target_) ? kProfTargetGemm : kProfSsmGemm;  // + {0 gemm, 1 head, 2 attn, 3 epi}
+  auto gemm_bytes = [&](int n_out, int k) { return 2.0 * n_out * k + 2.0 * T * k + 2.0 * T * n_out; };
+  prof_begin(base + 3, s);
   launch_embed_norm(m.emb, ln.meta, T, D, eps, ln.h, ln.xn, s);
+  prof_end(s, 0);
   AttnGeom g{m.H, m.hd, opts_.max_requests, opts_.max_ctx, 0, static_cast<float>(1.0 / std::sqrt(double(m.hd))),
              m.kc, m.vc};
   GemmEpilogue ep;
@@ -223,18 +245,37 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     const LayerW& w = m.layers[l];
     g.layer = l;
     const GemmPlan& pq = plan(3 * D, D, T, kGemmPartial);
+    prof_begin(base, s);
     check_cuda(gemm_launch(pq, w.qkv, ln.xn, ep, s, pdl), "gemm qkv");
+    prof_end(s, gemm_bytes(3 * D, D));
+    prof_begin(base + 3, s);
     launch_qkv_epilogue(ln.part, pq.map, ln.meta, T, g, m.rcos, m.rsin, ln.q, s);
+    prof_end(s, 0);
+    prof_begin(base + 2, s);
+    ++launches_;  // attention + combine
     launch_attention(m.tm_k, m.tm_v, ln.meta, sh.rows, sh.R, g, ln.q, aw, ln.attn, s);
+    prof_end(s, 0);
     const GemmPlan& po = plan(D, D, T, kGemmPartial);
+    prof_begin(base, s);
     check_cuda(gemm_launch(po, w.o, ln.attn, ep, s, pdl), "gemm o");
+    prof_end(s, gemm_bytes(D, D));
+    prof_begin(base + 3, s);
     launch_resid_norm(ln.part, po.map, T, D, eps, ln.h, ln.xn, s);
+    prof_end(s, 0);
     const GemmPlan& pg = plan(2 * F, D, T, kGemmPartial);
+    prof_begin(base, s);
     check_cuda(gemm_launch(pg, w.gu, ln.xn, ep, s, pdl), "gemm gate_up");
+    prof_end(s, gemm_bytes(2 * F, D));
+    prof_begin(base + 3, s);
     launch_swiglu(ln.part, pg.map, T, F, ln.act, s);
+    prof_end(s, 0);
     const GemmPlan& pd = plan(D, F, T, kGemmPartial);
+    prof_begin(base, s);
     check_cuda(gemm_launch(pd, w.dn, ln.act, ep, s, pdl), "gemm down");
+    prof_end(s, gemm_bytes(D, F));
+    prof_begin(base + 3, s);
     launch_resid_norm(ln.part, pd.map, T, D, eps, ln.h, ln.xn, s);
+    prof_end(s, 0);
   }
   if (head_mode > 0) {
     GemmEpilogue eh;
@@ -242,7 +283,9 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     eh.amax_val = ln.amax_val;
     eh.amax_idx = ln.amax_idx;
     eh.logits = head_mode == 2 ? ln.logits : nullptr;
+    prof_begin(base + 1, s);
     check_cuda(gemm_launch(plan(m.V, D, T, kGemmArgmax), m.head, ln.xn, eh, s, pdl), "gemm lm_head");
+    prof_end(s, gemm_bytes(m.V, D));
   }
   check_cuda(cudaGetLastError(), "forward launch");
 }
@@ -487,6 +530,7 @@ void Engine::record_timing(cudaEvent_t ev, cudaStream_t s) {
 // Enqueues one round on sv_ (+ SSM streams); used for capture and direct runs.
 void Engine::capture_round(RoundPlan& p) {
   const int W = opts_.window, M = static_cast<int>(ssm_.size());
+  const int64_t launches_before = launches_;
   cudaStream_t s = sv_;
   record_timing(ev_start_, s);
   check_cuda(cudaMemcpyAsync(d_in_, pin_in_, p.in_ints * 4, cudaMemcpyHostToDevice, s), "h2d lists");
@@ -506,7 +550,9 @@ void Engine::capture_round(RoundPlan& p) {
       a.list = list;
       a.ssm = j;
       a.width = nj;
+      prof_begin(kProfMeta, sj);
       launch_meta(a, st_, ln.meta, sj);
+      prof_end(sj, 0);
       forward(m, ln, FwdShape{2 * nj, nj, nj, 2}, sj, 1);
       int prev_t = 2 * nj, prev_q = 2;
       for (int k = 1; k <= W; ++k) {
@@ -522,7 +568,9 @@ void Engine::capture_round(RoundPlan& p) {
         b.amax_tiles = tiles;
         b.prev_t = prev_t;
         b.prev_qlen = prev_q;
+        prof_begin(kProfMeta, sj);
         launch_meta(b, st_, ln.meta, sj);
+        prof_end(sj, 0);
         if (k < W) forward(m, ln, FwdShape{nj, nj, nj, 1}, sj, 1);
         prev_t = nj, prev_q = 1;
       }
@@ -541,15 +589,20 @@ void Engine::capture_round(RoundPlan& p) {
     a.list = d_in_ + p.off_list;
     a.width = width;
     a.padded = opts_.packing ? 0 : 1;
+    prof_begin(kProfMeta, s);
     launch_meta(a, st_, tlane_.meta, s);
+    prof_end(s, 0);
     forward(target_, tlane_, FwdShape{T, n, a.padded ? n : width, W + 1}, s, opts_.debug_logits ? 2 : 1);
     int32_t* o = d_out_;
+    prof_begin(kProfMeta, s);
     launch_accept(tlane_.meta, n, W, d_in_ + p.off_list, d_in_ + p.off_ssm_of, tlane_.amax_val, tlane_.amax_idx,
                   (target_.V + 127) / 128, T, st_, o, o + n, o + 2 * n, o + 3 * n, o + 3 * n + n * W, d_emitted_, s);
+    prof_end(s, 0);
     check_cuda(cudaMemcpyAsync(pin_out_, d_out_, p.out_ints * 4, cudaMemcpyDeviceToHost, s), "d2h outcome");
   }
   record_timing(ev_end_, s);
   check_cuda(cudaGetLastError(), "round launch");
+  p.launches = launches_ - launches_before;
 }
 
 void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, spin_round_out* out) {
@@ -682,6 +735,38 @@ void Engine::run_rounds(int n, const int32_t* slots, const int32_t* ssm_of, int 
   }
   if (ms) *ms = t;
   mirror_stale_ = true;
+}
+
+void Engine::profile_round(int n, const int32_t* slots, const int32_t* ssm_of, double* ms, double* bytes,
+                           int64_t* launches) {
+  const int saved = opts_.use_graphs;
+  opts_.use_graphs = 0;
+  prof_ = true;
+  prof_recs_.clear();
+  try {
+    round(n, slots, ssm_of, nullptr);
+  } catch (...) {
+    prof_ = false;
+    opts_.use_graphs = saved;
+    throw;
+  }
+  prof_ = false;
+  opts_.use_graphs = saved;
+  for (int c = 0; c < kProfCats; ++c) ms[c] = bytes[c] = 0.0, launches[c] = 0;
+  for (auto& r : prof_recs_) {
+    float t = 0.f;
+    check_cuda(cudaEventElapsedTime(&t, r.a, r.b), "profile timing");
+    ms[r.cat] += t;
+    bytes[r.cat] += r.bytes;
+    ++launches[r.cat];
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  prof_recs_.clear();
+}
+
+int64_t Engine::launches_per_round(int n, const int32_t* slots, const int32_t* ssm_of) {
+  return plan_round(n, slots, ssm_of).launches;
 }
 
 void Engine::read_tokens(int slot, int32_t* tokens, int cap, int32_t* len) {

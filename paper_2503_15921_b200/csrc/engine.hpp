@@ -45,6 +45,20 @@ struct Lane {
   std::vector<void*> allocs;
 };
 
+// Kernel classes of profile_round (spin_c.h SPIN_PROF_*).
+enum ProfCat : int {
+  kProfTargetGemm = 0,
+  kProfTargetHead = 1,
+  kProfTargetAttn = 2,
+  kProfTargetEpi = 3,
+  kProfSsmGemm = 4,
+  kProfSsmHead = 5,
+  kProfSsmAttn = 6,
+  kProfSsmEpi = 7,
+  kProfMeta = 8,
+  kProfCats = 9,
+};
+
 struct FwdShape {
   int T, R, rows, qmax;
 };
@@ -60,6 +74,11 @@ class Engine {
   void switch_ssm(int n, const int32_t* slots, const int32_t* ssm_of);
   void read_tokens(int slot, int32_t* tokens, int cap, int32_t* len);
   void read_logits(float* logits, int64_t cap, int32_t* rows);
+  // One round without graphs, with CUDA events around every launch; per
+  // kernel class: device ms, algorithmic bytes (GEMMs), launches.
+  void profile_round(int n, const int32_t* slots, const int32_t* ssm_of, double* ms, double* bytes,
+                     int64_t* launches);
+  int64_t launches_per_round(int n, const int32_t* slots, const int32_t* ssm_of);
 
  private:
   struct RoundPlan;
@@ -70,7 +89,17 @@ class Engine {
   RoundPlan& plan_round(int n, const int32_t* slots, const int32_t* ssm_of);
   void capture_round(RoundPlan& p);
   void record_timing(cudaEvent_t ev, cudaStream_t s);
+  void prof_begin(int cat, cudaStream_t s);
+  void prof_end(cudaStream_t s, double bytes);
   bool capturing_ = false;
+  bool prof_ = false;
+  int64_t launches_ = 0;
+  struct ProfRec {
+    int cat;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<ProfRec> prof_recs_;
   void sync_state_from_device();
 
   spin_engine_opts opts_{};

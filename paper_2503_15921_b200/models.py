@@ -147,6 +147,25 @@ class Engine:
         _lib.check(self.lib.spin_read_logits(self.ctx, buf.ctypes.data_as(_lib.P_F32), buf.size, C.byref(rows)))
         return buf[: rows.value * self.target.vocab].reshape(rows.value, self.target.vocab)
 
+    PROF_CLASSES = ("target_gemm", "target_lm_head", "target_attention", "target_epilogue", "ssm_gemm",
+                    "ssm_lm_head", "ssm_attention", "ssm_epilogue", "meta_accept")
+
+    def profile(self, slots, ssm_of):
+        """One un-graphed round with CUDA events around each launch: {class: (ms, bytes, launches)}."""
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        ssm_of = np.ascontiguousarray(ssm_of, dtype=np.int32)
+        ms, by, ln = np.zeros(9), np.zeros(9), np.zeros(9, np.int64)
+        _lib.check(self.lib.spin_profile_round(self.ctx, len(slots), _p(slots), _p(ssm_of), ms.ctypes.data_as(_lib.P_F64),
+                                               by.ctypes.data_as(_lib.P_F64), ln.ctypes.data_as(_lib.P_I64)))
+        return {k: (float(ms[i]), float(by[i]), int(ln[i])) for i, k in enumerate(self.PROF_CLASSES)}
+
+    def launches_per_round(self, slots, ssm_of) -> int:
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        ssm_of = np.ascontiguousarray(ssm_of, dtype=np.int32)
+        v = C.c_int64()
+        _lib.check(self.lib.spin_round_launches(self.ctx, len(slots), _p(slots), _p(ssm_of), C.byref(v)))
+        return v.value
+
     def switch(self, slots, ssm_of):
         slots = np.ascontiguousarray(slots, dtype=np.int32)
         ssm_of = np.ascontiguousarray(ssm_of, dtype=np.int32)
