@@ -28,30 +28,58 @@ constexpr int kAttnThreads = 32 * (kConsumerWarps + 1);
 constexpr int kTileKeys = 32;
 constexpr unsigned kFull = 0xffffffffu;
 
+// Ring stages are owned per consumer warp (warp w consumes tiles w, w+4, ...
+// from its own kPerWarp stages, in order): an mbarrier parity wait is then never
+// more than one phase ahead of the stage it waits on.
 template <int HD>
 struct AttnCfg {
   static constexpr int kBoxes = HD / 64;                 // 64-dim (128-B) boxes per key row
   static constexpr int kTileBytes = kTileKeys * HD * 2;  // one of K or V
-  static constexpr int kStages = HD == 128 ? 4 : 6;
-  static constexpr int kDpl = HD / 32;  // dims per lane in P.V
+  static constexpr int kPerWarp = HD == 128 ? 1 : 2;     // 64 KB / 32 KB ring
+  static constexpr int kStages = kConsumerWarps * kPerWarp;
+  static constexpr int kDpl = HD / 32;                   // dims per lane in P.V
 };
+
+// tile t (CTA-global count) -> ring stage and phase
+template <int HD>
+__device__ __forceinline__ int tile_stage(int t) {
+  return (t % kConsumerWarps) + kConsumerWarps * ((t / kConsumerWarps) % AttnCfg<HD>::kPerWarp);
+}
+template <int HD>
+__device__ __forceinline__ uint32_t tile_phase(int t) {
+  return static_cast<uint32_t>((t / AttnCfg<HD>::kStages) & 1);
+}
 
 template <int HD, int QMAX>
 struct AttnSmem {
+  static constexpr int kQPad = (QMAX + 3) / 4 * 4;  // p row stride (float4 reads)
   static constexpr size_t kRing = static_cast<size_t>(AttnCfg<HD>::kStages) * 2 * AttnCfg<HD>::kTileBytes;
   static constexpr size_t kQ = static_cast<size_t>(QMAX) * HD * 4;
-  static constexpr size_t kMerge = static_cast<size_t>(kConsumerWarps) * QMAX * (HD + 2) * 4;
+  // per-warp p[key][query] buffers, reused as the segment merge buffer [QMAX][HD+2]
+  static constexpr size_t kPBuf = static_cast<size_t>(kConsumerWarps) * kTileKeys * kQPad * 4;
+  static constexpr size_t kMergeBuf = static_cast<size_t>(QMAX) * (HD + 2) * 4;
+  static constexpr size_t kP = (kPBuf > kMergeBuf ? kPBuf : kMergeBuf + 15) / 16 * 16;
   static constexpr size_t kBars = 2 * 8 * 8;
-  static constexpr size_t kTotal = 1024 + kRing + kQ + kMerge + kBars;
+  static constexpr size_t kTotal = 1024 + kRing + kQ + kP + kBars;
 };
 
-__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    f[2 * i] = __uint_as_float(w[i] << 16);
-    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
-  }
+__device__ __forceinline__ uint64_t f2_bits(float2 v) { return *reinterpret_cast<uint64_t*>(&v); }
+__device__ __forceinline__ float2 bits_f2(uint64_t v) { return *reinterpret_cast<float2*>(&v); }
+
+// Blackwell packed fp32x2 FMA (FFMA2): two IEEE fp32 FMAs per instruction.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return bits_f2(d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
+}
+// bf16 pair (packed in 32 bits) -> fp32 pair
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 }
 
 template <int HD, int QMAX>
@@ -62,13 +90,15 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
   using Sm = AttnSmem<HD, QMAX>;
   constexpr int S = Cfg::kStages;
   constexpr int DPL = Cfg::kDpl;
+  constexpr int QP = Sm::kQPad;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* ring = smem;
   float* sq = reinterpret_cast<float*>(smem + Sm::kRing);
-  float* smerge = reinterpret_cast<float*>(smem + Sm::kRing + Sm::kQ);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Sm::kRing + Sm::kQ + Sm::kMerge);
+  float* sp_all = reinterpret_cast<float*>(smem + Sm::kRing + Sm::kQ);
+  float* smerge = sp_all;  // aliases the p buffers: used only between segment barriers
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Sm::kRing + Sm::kQ + Sm::kP);
   uint64_t* empty_bar = full_bar + 8;
 
   const int prow = blockIdx.x, head = blockIdx.y;
@@ -100,8 +130,8 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
         const int base = ((g.layer * g.slots + slot) * H + head) * g.ctx + off;
         const int ntiles = (len + kTileKeys - 1) / kTileKeys;
         for (int t = 0; t < ntiles; ++t, ++gt) {
-          const int st = gt % S;
-          ptx::mbar_wait(&empty_bar[st], ((gt / S) & 1) ^ 1);
+          const int st = tile_stage<HD>(gt);
+          ptx::mbar_wait(&empty_bar[st], tile_phase<HD>(gt) ^ 1);
           ptx::mbar_arrive_expect_tx(&full_bar[st], 2 * Cfg::kTileBytes);
           uint8_t* kdst = ring + static_cast<size_t>(st) * 2 * Cfg::kTileBytes;
           uint8_t* vdst = kdst + Cfg::kTileBytes;
@@ -117,6 +147,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
   }
 
   // ------------------------------------------------------------------ consumers
+  float* sp = sp_all + warp * kTileKeys * QP;  // this warp's p[key][query]
   int gt = 0;
   for (int si = seg_begin; si < seg_end; ++si) {
     const int sid = m.row_seg[si];
@@ -132,52 +163,52 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
 
-    float mrun[QMAX], lrun[QMAX], o[QMAX][DPL];
+    float mrun[QMAX], lsum[QMAX];  // running max (warp-uniform), per-lane exp-sum
+    float2 o[QMAX][DPL / 2];
 #pragma unroll
     for (int j = 0; j < QMAX; ++j) {
       mrun[j] = -INFINITY;
-      lrun[j] = 0.f;
+      lsum[j] = 0.f;
 #pragma unroll
-      for (int d = 0; d < DPL; ++d) o[j][d] = 0.f;
+      for (int d = 0; d < DPL / 2; ++d) o[j][d] = make_float2(0.f, 0.f);
     }
 
     for (int t = warp; t < ntiles; t += kConsumerWarps) {
       const int gi = gt + t;
-      const int st = gi % S;
-      ptx::mbar_wait(&full_bar[st], (gi / S) & 1);
+      const int st = tile_stage<HD>(gi);
+      ptx::mbar_wait(&full_bar[st], tile_phase<HD>(gi));
       const uint8_t* ks = ring + static_cast<size_t>(st) * 2 * Cfg::kTileBytes;
       const uint8_t* vs = ks + Cfg::kTileBytes;
       const int kidx = t * kTileKeys + lane;  // key index within the segment
       const int kpos = off + kidx;            // absolute position of this lane's key
 
-      // ---- scores: lane = key
-      float s[QMAX];
+      // ---- scores, lane = key: q.k in fp32 pairs (FFMA2)
+      float2 acc[QMAX];
 #pragma unroll
-      for (int j = 0; j < QMAX; ++j) s[j] = 0.f;
+      for (int j = 0; j < QMAX; ++j) acc[j] = make_float2(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < HD / 8; ++c) {
         const int box = c / 8, cc = c % 8;
-        const uint4 raw8 = *reinterpret_cast<const uint4*>(ks + box * 4096 + lane * 128 + ((cc ^ (lane & 7)) << 4));
-        float kf[8];
-        bf16x8_to_f32(raw8, kf);
+        const uint4 kr = *reinterpret_cast<const uint4*>(ks + box * 4096 + lane * 128 + ((cc ^ (lane & 7)) << 4));
+        const float2 k0 = bf2_to_f2(kr.x), k1 = bf2_to_f2(kr.y), k2 = bf2_to_f2(kr.z), k3 = bf2_to_f2(kr.w);
 #pragma unroll
         for (int j = 0; j < QMAX; ++j) {
           if (j < qlen) {
             const float4 qa = *reinterpret_cast<const float4*>(sq + j * HD + c * 8);
             const float4 qb = *reinterpret_cast<const float4*>(sq + j * HD + c * 8 + 4);
-            s[j] += qa.x * kf[0] + qa.y * kf[1] + qa.z * kf[2] + qa.w * kf[3] + qb.x * kf[4] + qb.y * kf[5] +
-                    qb.z * kf[6] + qb.w * kf[7];
+            acc[j] = ffma2(make_float2(qa.x, qa.y), k0, acc[j]);
+            acc[j] = ffma2(make_float2(qa.z, qa.w), k1, acc[j]);
+            acc[j] = ffma2(make_float2(qb.x, qb.y), k2, acc[j]);
+            acc[j] = ffma2(make_float2(qb.z, qb.w), k3, acc[j]);
           }
         }
       }
-      // ---- online softmax per query (warp-shuffle max / sum)
-      float p[QMAX];
+      // ---- online softmax: warp max per query, per-lane sums
 #pragma unroll
       for (int j = 0; j < QMAX; ++j) {
-        p[j] = 0.f;
         if (j < qlen) {
           const int qpos = kvlen - qlen + j;
-          const float sc = (kidx < len && kpos <= qpos) ? s[j] * g.scale : -INFINITY;
+          const float sc = (kidx < len && kpos <= qpos) ? (acc[j].x + acc[j].y) * g.scale : -INFINITY;
           float mx = sc;
 #pragma unroll
           for (int ofs = 16; ofs > 0; ofs >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, ofs));
@@ -187,40 +218,39 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
             corr = expf(mrun[j] - mnew);
             pj = expf(sc - mnew);
           }
-          float ps = pj;
-#pragma unroll
-          for (int ofs = 16; ofs > 0; ofs >>= 1) ps += __shfl_xor_sync(kFull, ps, ofs);
-          lrun[j] = lrun[j] * corr + ps;
+          lsum[j] = lsum[j] * corr + pj;
           mrun[j] = mnew;
 #pragma unroll
-          for (int d = 0; d < DPL; ++d) o[j][d] *= corr;
-          p[j] = pj;
+          for (int d = 0; d < DPL / 2; ++d) o[j][d] = fmul2(o[j][d], make_float2(corr, corr));
+          sp[lane * QP + j] = pj;
         }
       }
-      // ---- P.V: lane owns DPL consecutive dims
+      __syncwarp();
+      // ---- P.V: lane owns DPL consecutive dims, p broadcast from shared memory
       const int dim0 = lane * DPL;
       const int box = dim0 / 64, col = dim0 % 64, chunk = col / 8, inb = (col % 8) * 2;
 #pragma unroll 4
       for (int r = 0; r < kTileKeys; ++r) {
         const uint8_t* vp = vs + box * 4096 + r * 128 + ((chunk ^ (r & 7)) << 4) + inb;
-        float vf[DPL];
+        float2 v[DPL / 2];
         if constexpr (DPL == 4) {
           const uint2 u = *reinterpret_cast<const uint2*>(vp);
-          vf[0] = __uint_as_float(u.x << 16);
-          vf[1] = __uint_as_float(u.x & 0xffff0000u);
-          vf[2] = __uint_as_float(u.y << 16);
-          vf[3] = __uint_as_float(u.y & 0xffff0000u);
+          v[0] = bf2_to_f2(u.x);
+          v[1] = bf2_to_f2(u.y);
         } else {
-          const uint32_t u = *reinterpret_cast<const uint32_t*>(vp);
-          vf[0] = __uint_as_float(u << 16);
-          vf[1] = __uint_as_float(u & 0xffff0000u);
+          v[0] = bf2_to_f2(*reinterpret_cast<const uint32_t*>(vp));
+        }
+        float pr[QP];
+#pragma unroll
+        for (int j4 = 0; j4 < QP; j4 += 4) {
+          const float4 p4 = *reinterpret_cast<const float4*>(sp + r * QP + j4);
+          pr[j4] = p4.x, pr[j4 + 1] = p4.y, pr[j4 + 2] = p4.z, pr[j4 + 3] = p4.w;
         }
 #pragma unroll
         for (int j = 0; j < QMAX; ++j) {
           if (j < qlen) {
-            const float pr = __shfl_sync(kFull, p[j], r);
 #pragma unroll
-            for (int d = 0; d < DPL; ++d) o[j][d] += pr * vf[d];
+            for (int d = 0; d < DPL / 2; ++d) o[j][d] = ffma2(make_float2(pr[j], pr[j]), v[d], o[j][d]);
           }
         }
       }
@@ -229,38 +259,51 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
     }
     gt += ntiles;
 
-    // ---- merge the 4 warps' partial states, emit the segment partial
-    float* mw = smerge + static_cast<size_t>(warp) * QMAX * (HD + 2);
+    // ---- merge the 4 warps' partial states in warp order (deterministic), then
+    // emit the segment partial (max, sum, unnormalised output) per query.
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // p buffers become the merge buffer
+    for (int ww = 0; ww < kConsumerWarps; ++ww) {
+      if (warp == ww) {
 #pragma unroll
-    for (int j = 0; j < QMAX; ++j) {
-      if (j < qlen) {
+        for (int j = 0; j < QMAX; ++j) {
+          if (j < qlen) {
+            float l = lsum[j];
 #pragma unroll
-        for (int d = 0; d < DPL; ++d) mw[j * (HD + 2) + lane * DPL + d] = o[j][d];
-        if (lane == 0) {
-          mw[j * (HD + 2) + HD] = mrun[j];
-          mw[j * (HD + 2) + HD + 1] = lrun[j];
+            for (int ofs = 16; ofs > 0; ofs >>= 1) l += __shfl_xor_sync(kFull, l, ofs);
+            float* b = smerge + j * (HD + 2);
+            if (ww == 0) {
+#pragma unroll
+              for (int d = 0; d < DPL / 2; ++d) {
+                b[lane * DPL + 2 * d] = o[j][d].x;
+                b[lane * DPL + 2 * d + 1] = o[j][d].y;
+              }
+              if (lane == 0) b[HD] = mrun[j], b[HD + 1] = l;
+            } else {
+              const float mo = b[HD], M = fmaxf(mo, mrun[j]);
+              const float fo = (M == -INFINITY || mo == -INFINITY) ? 0.f : expf(mo - M);
+              const float fn = (M == -INFINITY || mrun[j] == -INFINITY) ? 0.f : expf(mrun[j] - M);
+#pragma unroll
+              for (int d = 0; d < DPL / 2; ++d) {
+                float* bd = b + lane * DPL + 2 * d;
+                bd[0] = bd[0] * fo + o[j][d].x * fn;
+                bd[1] = bd[1] * fo + o[j][d].y * fn;
+              }
+              __syncwarp();
+              if (lane == 0) b[HD] = M, b[HD + 1] = b[HD + 1] * fo + l * fn;
+            }
+          }
         }
       }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
     }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
     for (int e = threadIdx.x; e < qlen * HD; e += 32 * kConsumerWarps) {
       const int j = e / HD, d = e % HD;
-      float M = -INFINITY;
-#pragma unroll
-      for (int ww = 0; ww < kConsumerWarps; ++ww) M = fmaxf(M, smerge[(ww * QMAX + j) * (HD + 2) + HD]);
-      float O = 0.f, L = 0.f;
-#pragma unroll
-      for (int ww = 0; ww < kConsumerWarps; ++ww) {
-        const float* b = smerge + (ww * QMAX + j) * (HD + 2);
-        const float f = (M == -INFINITY || b[HD] == -INFINITY) ? 0.f : expf(b[HD] - M);
-        O += b[d] * f;
-        L += b[HD + 1] * f;
-      }
+      const float* b = smerge + j * (HD + 2);
       const size_t pi = (static_cast<size_t>(sid) * H + head) * w.qmax + j;
-      w.part_o[pi * HD + d] = O;
+      w.part_o[pi * HD + d] = b[d];
       if (d == 0) {
-        w.part_m[pi] = M;
-        w.part_l[pi] = L;
+        w.part_m[pi] = b[HD];
+        w.part_l[pi] = b[HD + 1];
       }
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");

@@ -13,11 +13,23 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ float sum_pieces(const float* __restrict__ part, const PieceMap& pm, int T, int n_out,
-                                            int t, int n) {
-  const int np = pm.pieces(t, n);
-  float acc = part[static_cast<size_t>(t) * n_out + n];
-  for (int s = 1; s < np; ++s) acc = __fadd_rn(acc, part[(static_cast<size_t>(s) * T + t) * n_out + n]);
+// Stream-K piece counts of the m-tiles a row touches, staged once per block
+// (the 64-bit divisions of PieceMap::pieces stay out of the element loop).
+constexpr int kMaxMTiles = 512;
+
+__device__ __forceinline__ void stage_pieces(const PieceMap& pm, int t, int n_begin, int n_end, uint8_t* s_np) {
+  const int m0 = n_begin / 128, m1 = (n_end + 127) / 128;
+  for (int m = m0 + static_cast<int>(threadIdx.x); m < m1; m += blockDim.x)
+    s_np[m - m0] = static_cast<uint8_t>(pm.pieces(t, m * 128));
+}
+
+__device__ __forceinline__ float sum_pieces_t(const float* __restrict__ part, const uint8_t* s_np, int m0, int T,
+                                              int n_out, int t, int n) {
+  const int np = s_np[n / 128 - m0];
+  const size_t stride = static_cast<size_t>(T) * n_out;
+  const float* p = part + static_cast<size_t>(t) * n_out + n;
+  float acc = p[0];
+  for (int s = 1; s < np; ++s) acc = __fadd_rn(acc, p[s * stride]);
   return acc;
 }
 
@@ -234,53 +246,66 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
 
 // ------------------------------------------------------------------ norms
 constexpr int kRowThreads = 256;
-constexpr int kMaxPerThread = 32;  // D <= 8192
 
-__device__ __forceinline__ void rmsnorm_store(float (&v)[kMaxPerThread], int D, float eps, bf16* xn, float* red) {
+// x = bf16(row * 1/sqrt(mean(row^2) + eps)); row staged in shared memory.
+__device__ __forceinline__ void rmsnorm_row(const float* row, int D, float eps, bf16* xn, float* red) {
   float ss = 0.f;
-  for (int k = 0, i = threadIdx.x; i < D; i += kRowThreads, ++k) ss += v[k] * v[k];
+  for (int i = threadIdx.x; i < D; i += blockDim.x) ss += row[i] * row[i];
   const float tot = block_sum(ss, red);
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(tot, static_cast<float>(D)), eps)));
-  for (int k = 0, i = threadIdx.x; i < D; i += kRowThreads, ++k) xn[i] = __float2bfloat16_rn(__fmul_rn(v[k], inv));
+  for (int i = threadIdx.x; i < D; i += blockDim.x) xn[i] = __float2bfloat16_rn(__fmul_rn(row[i], inv));
 }
 
 __global__ void __launch_bounds__(kRowThreads) embed_norm_kernel(const bf16* __restrict__ emb, const int32_t* tok,
                                                                  int D, float eps, float* h, bf16* xn) {
+  extern __shared__ float s_row[];
   __shared__ float red[32];
   ptx::grid_dep_wait();
   const int t = blockIdx.x;
   const bf16* e = emb + static_cast<size_t>(tok[t]) * D;
-  float v[kMaxPerThread];
-  for (int k = 0, i = threadIdx.x; i < D; i += kRowThreads, ++k) {
-    v[k] = __bfloat162float(e[i]);
-    h[static_cast<size_t>(t) * D + i] = v[k];
+  for (int i = threadIdx.x; i < D; i += kRowThreads) {
+    const float v = __bfloat162float(e[i]);
+    s_row[i] = v;
+    h[static_cast<size_t>(t) * D + i] = v;
   }
   ptx::grid_dep_launch();
-  rmsnorm_store(v, D, eps, xn + static_cast<size_t>(t) * D, red);
+  rmsnorm_row(s_row, D, eps, xn + static_cast<size_t>(t) * D, red);
 }
 
 __global__ void __launch_bounds__(kRowThreads) resid_norm_kernel(const float* __restrict__ part, PieceMap pm, int T,
                                                                  int D, float eps, float* h, bf16* xn) {
+  extern __shared__ float s_row[];
   __shared__ float red[32];
-  ptx::grid_dep_wait();
+  __shared__ uint8_t s_np[kMaxMTiles];
   const int t = blockIdx.x;
-  float v[kMaxPerThread];
-  for (int k = 0, i = threadIdx.x; i < D; i += kRowThreads, ++k) {
+  stage_pieces(pm, t, 0, D, s_np);
+  ptx::grid_dep_wait();
+  __syncthreads();
+  for (int i = threadIdx.x; i < D; i += kRowThreads) {
     const size_t o = static_cast<size_t>(t) * D + i;
-    v[k] = __fadd_rn(h[o], sum_pieces(part, pm, T, D, t, i));
-    h[o] = v[k];
+    const float v = __fadd_rn(h[o], sum_pieces_t(part, s_np, 0, T, D, t, i));
+    s_row[i] = v;
+    h[o] = v;
   }
   ptx::grid_dep_launch();
-  rmsnorm_store(v, D, eps, xn + static_cast<size_t>(t) * D, red);
+  rmsnorm_row(s_row, D, eps, xn + static_cast<size_t>(t) * D, red);
 }
 
+// grid (T, ceil(F / 256)): one thread per SwiGLU output.
 __global__ void __launch_bounds__(kRowThreads) swiglu_kernel(const float* __restrict__ part, PieceMap pm, int T, int F,
                                                              bf16* act) {
-  ptx::grid_dep_wait();
+  __shared__ uint8_t s_np_g[8], s_np_u[8];
   const int t = blockIdx.x;
-  for (int f = threadIdx.x; f < F; f += kRowThreads) {
-    const float g = sum_pieces(part, pm, T, 2 * F, t, f);
-    const float u = sum_pieces(part, pm, T, 2 * F, t, F + f);
+  const int f0 = blockIdx.y * kRowThreads;
+  const int f1 = min(F, f0 + kRowThreads);
+  stage_pieces(pm, t, f0, f1, s_np_g);
+  stage_pieces(pm, t, F + f0, F + f1, s_np_u);
+  ptx::grid_dep_wait();
+  __syncthreads();
+  const int f = f0 + threadIdx.x;
+  if (f < F) {
+    const float g = sum_pieces_t(part, s_np_g, f0 / 128, T, 2 * F, t, f);
+    const float u = sum_pieces_t(part, s_np_u, (F + f0) / 128, T, 2 * F, t, F + f);
     const float sg = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
     act[static_cast<size_t>(t) * F + f] = __float2bfloat16_rn(__fmul_rn(sg, u));
   }
@@ -288,30 +313,35 @@ __global__ void __launch_bounds__(kRowThreads) swiglu_kernel(const float* __rest
 }
 
 // Split-K reduction of the fused QKV projection, RoPE (rotate-half) on q and k,
-// q -> fp32 (feeds only the CUDA-core attention), k/v -> bf16 KV cache at (layer, slot, head, pos).
+// q -> fp32 (feeds only the CUDA-core attention), k/v -> bf16 KV cache at
+// (layer, slot, head, pos). grid (T, ceil(H*hd/2 / 256)): one thread per
+// rotary pair.
 __global__ void __launch_bounds__(kRowThreads) qkv_epilogue_kernel(const float* __restrict__ part, PieceMap pm,
                                                                    FwdMeta m, int T, AttnGeom g,
                                                                    const float* __restrict__ rcos,
                                                                    const float* __restrict__ rsin, float* q) {
-  ptx::grid_dep_wait();
+  __shared__ uint8_t s_np[kMaxMTiles];
   const int t = blockIdx.x;
   const int H = g.n_heads, hd = g.head_dim, half = hd / 2, D = H * hd, N = 3 * D;
-  const int slot = m.row_slot[t], pos = m.row_pos[t];
-  const float* cs = rcos + static_cast<size_t>(pos) * half;
-  const float* sn = rsin + static_cast<size_t>(pos) * half;
-  for (int pi = threadIdx.x; pi < H * half; pi += kRowThreads) {
+  stage_pieces(pm, t, 0, N, s_np);
+  ptx::grid_dep_wait();
+  __syncthreads();
+  const int pi = blockIdx.y * kRowThreads + threadIdx.x;
+  if (pi < H * half) {
+    const int slot = m.row_slot[t], pos = m.row_pos[t];
     const int hh = pi / half, i = pi % half;
     const int nq = hh * hd + i;
-    const float q0 = sum_pieces(part, pm, T, N, t, nq), q1 = sum_pieces(part, pm, T, N, t, nq + half);
-    const float k0 = sum_pieces(part, pm, T, N, t, D + nq), k1 = sum_pieces(part, pm, T, N, t, D + nq + half);
-    const float v0 = sum_pieces(part, pm, T, N, t, 2 * D + nq), v1 = sum_pieces(part, pm, T, N, t, 2 * D + nq + half);
-    const float c = cs[i], s = sn[i];
+    const float q0 = sum_pieces_t(part, s_np, 0, T, N, t, nq), q1 = sum_pieces_t(part, s_np, 0, T, N, t, nq + half);
+    const float k0 = sum_pieces_t(part, s_np, 0, T, N, t, D + nq);
+    const float k1 = sum_pieces_t(part, s_np, 0, T, N, t, D + nq + half);
+    const float v0 = sum_pieces_t(part, s_np, 0, T, N, t, 2 * D + nq);
+    const float v1 = sum_pieces_t(part, s_np, 0, T, N, t, 2 * D + nq + half);
+    const float c = rcos[static_cast<size_t>(pos) * half + i], s = rsin[static_cast<size_t>(pos) * half + i];
     float* qo = q + static_cast<size_t>(t) * D + nq;
     qo[0] = __fsub_rn(__fmul_rn(q0, c), __fmul_rn(q1, s));
     qo[half] = __fadd_rn(__fmul_rn(q1, c), __fmul_rn(q0, s));
     if (slot >= 0) {
-      const size_t kv =
-          ((((static_cast<size_t>(g.layer) * g.slots + slot) * H + hh) * g.ctx) + pos) * hd + i;
+      const size_t kv = ((((static_cast<size_t>(g.layer) * g.slots + slot) * H + hh) * g.ctx) + pos) * hd + i;
       g.k_cache[kv] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(k0, c), __fmul_rn(k1, s)));
       g.k_cache[kv + half] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(k1, c), __fmul_rn(k0, s)));
       g.v_cache[kv] = __float2bfloat16_rn(v0);
@@ -498,22 +528,25 @@ void launch_meta(const MetaArgs& a, const SlotState& st, const FwdMeta& m, cudaS
 
 void launch_embed_norm(const bf16* emb, const FwdMeta& m, int T, int D, float eps, float* h, bf16* xn,
                        cudaStream_t s) {
-  launch_pdl(embed_norm_kernel, dim3(T), dim3(kRowThreads), 0, s, emb, static_cast<const int32_t*>(m.row_tok), D, eps,
-             h, xn);
+  launch_pdl(embed_norm_kernel, dim3(T), dim3(kRowThreads), D * sizeof(float), s, emb,
+             static_cast<const int32_t*>(m.row_tok), D, eps, h, xn);
 }
 
 void launch_qkv_epilogue(const float* part, const PieceMap& pm, const FwdMeta& m, int T, const AttnGeom& g,
                          const float* rcos, const float* rsin, float* q, cudaStream_t s) {
-  launch_pdl(qkv_epilogue_kernel, dim3(T), dim3(kRowThreads), 0, s, part, pm, m, T, g, rcos, rsin, q);
+  const int pairs = g.n_heads * g.head_dim / 2;
+  launch_pdl(qkv_epilogue_kernel, dim3(T, (pairs + kRowThreads - 1) / kRowThreads), dim3(kRowThreads), 0, s, part, pm,
+             m, T, g, rcos, rsin, q);
 }
 
 void launch_resid_norm(const float* part, const PieceMap& pm, int T, int D, float eps, float* h, bf16* xn,
                        cudaStream_t s) {
-  launch_pdl(resid_norm_kernel, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, D, eps, h, xn);
+  launch_pdl(resid_norm_kernel, dim3(T), dim3(kRowThreads), D * sizeof(float), s, part, pm, T, D, eps, h, xn);
 }
 
 void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* act, cudaStream_t s) {
-  launch_pdl(swiglu_kernel, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, F, act);
+  launch_pdl(swiglu_kernel, dim3(T, (F + kRowThreads - 1) / kRowThreads), dim3(kRowThreads), 0, s, part, pm, T, F,
+             act);
 }
 
 void launch_accept(const FwdMeta& m, int n_req, int window, const int32_t* list, const int32_t* ssm_of_req,
