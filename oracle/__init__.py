@@ -70,6 +70,9 @@ def load_oracle() -> C.CDLL:
         lib.so_engine_switch.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         lib.so_engine_read_tokens.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]
         lib.so_set_gemm_lanes.argtypes = [C.c_int]
+        lib.so_engine_set_gap_outputs.argtypes = [C.c_void_p, C.c_void_p]
+        lib.so_engine_set_hints.argtypes = [C.c_void_p, C.c_void_p, C.c_float]
+        lib.so_engine_forced_count.restype = C.c_long
         lib.so_engine_last_timing.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         lib.so_debug_layer.argtypes = [C.c_int, C.c_void_p, C.c_int]
         lib.so_debug_inner.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int]
@@ -142,12 +145,24 @@ class OracleEngine:
         flat = np.concatenate(prompts).astype(np.int32)
         assert self.lib.so_engine_prefill(self.e, len(slots), slots.ctypes.data, lens.ctypes.data, flat.ctypes.data) == 0
 
-    def round(self, slots, ssm_of, want_logits=False):
+    def round(self, slots, ssm_of, want_logits=False, want_gaps=False, hints=None, tau=0.0):
+        """hints: a GPU round's output dict; near-ties within tau adopt the GPU token (counted)."""
         import numpy as np
 
         slots = np.ascontiguousarray(slots, dtype=np.int32)
         ssm_of = np.ascontiguousarray(ssm_of, dtype=np.int32)
         n, W = len(slots), self.window
+        act_rows = int((ssm_of >= 0).sum()) * (W + 1)
+        dgap = np.full(n * W, np.inf, np.float32) if want_gaps else None
+        tgap = np.full(max(act_rows, 1), np.inf, np.float32) if want_gaps else None
+        self.lib.so_engine_set_gap_outputs(dgap.ctypes.data if want_gaps else None,
+                                           tgap.ctypes.data if want_gaps else None)
+        if hints is not None:
+            dh = np.ascontiguousarray(hints["drafts"], dtype=np.int32).reshape(-1)
+            act = np.flatnonzero(ssm_of >= 0)
+            th = np.ascontiguousarray(np.asarray(hints["target"], dtype=np.int32)[act].reshape(-1))
+            self._hint_keep = (dh, th)
+            self.lib.so_engine_set_hints(dh.ctypes.data, th.ctypes.data, tau)
         acc, bonus, comm = np.zeros(n, np.int32), np.zeros(n, np.int32), np.zeros(n, np.int32)
         drafts, tgt = np.zeros(n * W, np.int32), np.zeros(n * (W + 1), np.int32)
         act = int((ssm_of >= 0).sum())
@@ -155,12 +170,20 @@ class OracleEngine:
         st = self.lib.so_engine_round(self.e, n, slots.ctypes.data, ssm_of.ctypes.data, acc.ctypes.data,
                                       bonus.ctypes.data, comm.ctypes.data, drafts.ctypes.data, tgt.ctypes.data,
                                       logits.ctypes.data if want_logits else None)
+        self.lib.so_engine_set_gap_outputs(None, None)
+        self.lib.so_engine_set_hints(None, None, 0.0)
         assert st == 0, st
         out = {"accepted": acc, "bonus": bonus, "committed": comm, "drafts": drafts.reshape(n, W),
                "target": tgt.reshape(n, W + 1)}
+        if want_gaps:
+            out["draft_gap"] = dgap.reshape(n, W)
+            out["target_gap"] = tgap[:act_rows]
         if want_logits:
             out["logits"] = logits.reshape(act * (W + 1), self.vocab)
         return out
+
+    def forced(self) -> int:
+        return int(self.lib.so_engine_forced_count())
 
     def last_timing(self):
         a, b, c = C.c_double(), C.c_double(), C.c_double()

@@ -201,6 +201,10 @@ static void model_destroy(model* m) {
   free(m);
 }
 
+/* Tie-aware argmax state (so_engine_set_hints). */
+static float g_tau = 0.0f;
+static long g_forced = 0;
+
 /* Debug knob (sensitivity experiments only): number of partial sums. */
 static int g_lanes = 16;
 void so_set_gemm_lanes(int lanes) { g_lanes = lanes == 8 ? 8 : 16; }
@@ -300,8 +304,19 @@ static double now_s(void) {
 }
 static double g_t_blocks = 0.0, g_t_head = 0.0; /* seconds spent in the last forward */
 
+static void model_forward_gap(model* m, int T, const int* tok, const int* slot, const int* pos, int* amax,
+                              float* logits, float* gap, const int* hint);
 static void model_forward(model* m, int T, const int* tok, const int* slot, const int* pos, int* amax,
                           float* logits) {
+  model_forward_gap(m, T, tok, slot, pos, amax, logits, NULL, NULL);
+}
+
+/* gap[t] (optional) = top-1 minus top-2 logit: the decision margin of row t.
+ * hint[t] >= 0 (optional): a tie-aware argmax -- the hinted token is taken when
+ * its logit is within g_tau of the maximum (a near-tie at the bf16 noise floor);
+ * every such override is counted in g_forced. */
+static void model_forward_gap(model* m, int T, const int* tok, const int* slot, const int* pos, int* amax,
+                              float* logits, float* gap, const int* hint) {
   const double t0 = now_s();
   const so_model_desc* d = &m->d;
   const int D = d->d_model, H = d->n_heads, hd = d->head_dim, F = d->ffn, V = d->vocab, half = hd / 2;
@@ -394,6 +409,16 @@ static void model_forward(model* m, int T, const int* tok, const int* slot, cons
     for (int v = 1; v < V; ++v)
       if (r[v] > r[best]) best = v;
     amax[t] = best;
+    if (hint && hint[t] >= 0 && hint[t] < V && hint[t] != best && r[hint[t]] >= r[best] - g_tau) {
+      amax[t] = hint[t];
+      ++g_forced;
+    }
+    if (gap) {
+      float second = -INFINITY;
+      for (int v = 0; v < V; ++v)
+        if (v != best && r[v] > second) second = r[v];
+      gap[t] = r[best] - second;
+    }
   }
   if (!logits) free(lg);
   free(h), free(x), free(y), free(q);
@@ -489,6 +514,20 @@ int so_engine_switch(so_engine* e, int n, const int* slots, const int* ssm_of) {
 }
 
 static double g_round_draft = 0.0, g_round_vblocks = 0.0, g_round_vhead = 0.0;
+static const int* g_draft_hint = NULL;  /* [n][window] GPU draft tokens for the next round */
+static const int* g_target_hint = NULL; /* [rows] GPU target argmax for the next round */
+void so_engine_set_hints(const int* draft_hint, const int* target_hint, float tau) {
+  g_draft_hint = draft_hint;
+  g_target_hint = target_hint;
+  g_tau = tau;
+}
+long so_engine_forced_count(void) { return g_forced; }
+static float* g_draft_gap = NULL;  /* [n][window] per next so_engine_round, optional */
+static float* g_target_gap = NULL; /* [rows] */
+void so_engine_set_gap_outputs(float* draft_gap, float* target_gap) {
+  g_draft_gap = draft_gap;
+  g_target_gap = target_gap;
+}
 void so_engine_last_timing(double* draft_s, double* verify_blocks_s, double* verify_head_s) {
   *draft_s = g_round_draft, *verify_blocks_s = g_round_vblocks, *verify_head_s = g_round_vhead;
 }
@@ -521,16 +560,31 @@ int so_engine_round(so_engine* e, int n, const int* slots, const int* ssm_of, in
         ++k;
       }
     }
-    model_forward(e->ssm[j], 2 * cnt, tok, sl, ps, am, NULL);
-    for (int b = 0; b < cnt; ++b) dr[(size_t)idx[b] * g] = am[2 * b + 1];
+    float* gp = (float*)malloc(sizeof(float) * 2 * cnt);
+    int* hn = (int*)malloc(sizeof(int) * 2 * cnt);
+    for (int b = 0; b < cnt; ++b) {
+      hn[2 * b] = -1;
+      hn[2 * b + 1] = g_draft_hint ? g_draft_hint[(size_t)idx[b] * g] : -1;
+    }
+    model_forward_gap(e->ssm[j], 2 * cnt, tok, sl, ps, am, NULL, gp, hn);
+    for (int b = 0; b < cnt; ++b) {
+      dr[(size_t)idx[b] * g] = am[2 * b + 1];
+      if (g_draft_gap) g_draft_gap[(size_t)idx[b] * g] = gp[2 * b + 1];
+    }
     for (int step = 1; step < g; ++step) {
       for (int b = 0; b < cnt; ++b) {
         const int s = slots[idx[b]];
         tok[b] = dr[(size_t)idx[b] * g + step - 1], sl[b] = s, ps[b] = e->committed[s] - 1 + step;
       }
-      model_forward(e->ssm[j], cnt, tok, sl, ps, am, NULL);
-      for (int b = 0; b < cnt; ++b) dr[(size_t)idx[b] * g + step] = am[b];
+      for (int b = 0; b < cnt; ++b) hn[b] = g_draft_hint ? g_draft_hint[(size_t)idx[b] * g + step] : -1;
+      model_forward_gap(e->ssm[j], cnt, tok, sl, ps, am, NULL, gp, hn);
+      for (int b = 0; b < cnt; ++b) {
+        dr[(size_t)idx[b] * g + step] = am[b];
+        if (g_draft_gap) g_draft_gap[(size_t)idx[b] * g + step] = gp[b];
+      }
     }
+    free(gp);
+    free(hn);
     for (int b = 0; b < cnt; ++b) {
       const int s = slots[idx[b]];
       e->ssm_len[(size_t)j * e->slots + s] = e->committed[s] + g - 1;
@@ -556,7 +610,7 @@ int so_engine_round(so_engine* e, int n, const int* slots, const int* ssm_of, in
     }
   }
   if (T > 0) {
-    model_forward(e->target, T, tok, sl, ps, am, logits);
+    model_forward_gap(e->target, T, tok, sl, ps, am, logits, g_target_gap, g_target_hint);
     g_round_vblocks = g_t_blocks;
     g_round_vhead = g_t_head;
   }

@@ -116,6 +116,7 @@ _SIGNATURES = {
     "spin_switch_ssm": [C.c_void_p, C.c_int32, P_I32, P_I32],
     "spin_profile_round": [C.c_void_p, C.c_int32, P_I32, P_I32, P_F64, P_F64, P_I64],
     "spin_round_launches": [C.c_void_p, C.c_int32, P_I32, P_I32, P_I64],
+    "spin_kernel_bench": [C.c_void_p, C.c_int32, C.c_int32, P_F64, P_F64],
     "spin_attention": [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                        C.c_void_p, C.c_void_p, C.c_int32, P_I32, P_I32, P_I32, C.c_int32, C.c_void_p],
     "spin_gemm_info": [C.c_int32, C.c_int32, C.c_int32, C.c_int32, P_I32, P_I32, P_I32],

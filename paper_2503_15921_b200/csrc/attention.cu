@@ -173,7 +173,9 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
       for (int d = 0; d < DPL / 2; ++d) o[j][d] = make_float2(0.f, 0.f);
     }
 
-    for (int t = warp; t < ntiles; t += kConsumerWarps) {
+    // warp w owns the tiles whose CTA-global index gt+t is w mod 4 (its ring stages)
+    for (int t = ((warp - gt) % kConsumerWarps + kConsumerWarps) % kConsumerWarps; t < ntiles;
+         t += kConsumerWarps) {
       const int gi = gt + t;
       const int st = tile_stage<HD>(gi);
       ptx::mbar_wait(&full_bar[st], tile_phase<HD>(gi));
@@ -310,22 +312,284 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core variant (requests with <= 8 queries): mma.sync m16n8k16 bf16
+// with fp32 accumulation, FlashAttention-2 register layout (the S accumulator
+// fragment of two 8-key tiles is the P operand fragment of one 16-key step).
+// Q is split 3-way (hi/mid/lo bf16, ~24 mantissa bits) and P 2-way, so scores
+// and outputs keep ~fp32 accuracy. Each consumer warp owns its ring stage and
+// writes its own (max, sum, output) partial per segment: no CTA barriers in the
+// main loop; the combine kernel merges segments x warps under one shared max.
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+  const uint32_t a = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+  const uint32_t b = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
+  return a | (b << 16);
+}
+__device__ __forceinline__ float bf_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+__device__ __forceinline__ void mma_bf16(float& d0, float& d1, uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+  float x2, x3;  // rows g+8 of the 16-row tile: padding queries, discarded
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%11,%12,%13};"
+      : "=f"(d0), "=f"(d1), "=f"(x2), "=f"(x3)
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1), "f"(d0), "f"(d1), "f"(0.f), "f"(0.f));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+// byte offset of (key row, 16-B chunk) inside a TMA 128-B-swizzled KV tile
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+  return static_cast<uint32_t>((chunk >> 3) * 4096 + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
+}
+
+constexpr int kMmaSub = kConsumerWarps;  // partials per (segment, head)
+
+template <int HD>
+struct MmaSmem {
+  static constexpr size_t kRing = static_cast<size_t>(AttnCfg<HD>::kStages) * 2 * AttnCfg<HD>::kTileBytes;
+  static constexpr uint32_t kQPlane = 8 * HD * 2;  // 8 query rows, bf16
+  static constexpr size_t kQ = static_cast<size_t>(kConsumerWarps) * 3 * kQPlane;
+  static constexpr size_t kTotal = 1024 + kRing + kQ + 2 * 8 * 8;
+};
+
+// byte offset of (row, 16-B chunk) in a Q plane with HD*2-byte rows, chunks XOR-swizzled by row
+template <int HD>
+__device__ __forceinline__ uint32_t qswz(int row, int chunk) {
+  return static_cast<uint32_t>(row * HD * 2 + (((chunk & 7) ^ (row & 7)) | (chunk & ~7)) * 16);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kAttnThreads) attention_mma_kernel(const __grid_constant__ CUtensorMap tm_k,
+                                                                     const __grid_constant__ CUtensorMap tm_v,
+                                                                     FwdMeta m, AttnGeom g,
+                                                                     const float* __restrict__ q, AttnWork w) {
+  using Cfg = AttnCfg<HD>;
+  constexpr int KS = HD / 16;  // 16-dim k-steps
+  constexpr int DN = HD / 8;   // 8-dim output tiles
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* ring = smem;
+  uint8_t* qplanes = smem + MmaSmem<HD>::kRing;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + MmaSmem<HD>::kRing + MmaSmem<HD>::kQ);
+  uint64_t* empty_bar = full_bar + 8;
+
+  const int prow = blockIdx.x, head = blockIdx.y;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int g8 = lane >> 2, c4 = lane & 3;
+  const int H = g.n_heads, D = H * HD;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  ptx::grid_dep_wait();
+  const int seg_begin = m.row_ptr[prow], seg_end = m.row_ptr[prow + 1];
+
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_first();
+      int gt = 0;
+      for (int si = seg_begin; si < seg_end; ++si) {
+        const int32_t* sg = m.seg + 5 * m.row_seg[si];
+        const int rq = sg[0], len = sg[3] - sg[2], off = sg[4];
+        const int base = ((g.layer * g.slots + m.req_slot[rq]) * H + head) * g.ctx + off;
+        const int ntiles = (len + kTileKeys - 1) / kTileKeys;
+        for (int t = 0; t < ntiles; ++t, ++gt) {
+          const int st = tile_stage<HD>(gt);
+          ptx::mbar_wait(&empty_bar[st], tile_phase<HD>(gt) ^ 1);
+          ptx::mbar_arrive_expect_tx(&full_bar[st], 2 * Cfg::kTileBytes);
+          uint8_t* kdst = ring + static_cast<size_t>(st) * 2 * Cfg::kTileBytes;
+#pragma unroll
+          for (int b = 0; b < Cfg::kBoxes; ++b) {
+            ptx::tma_load_2d(kdst + b * 4096, &tm_k, &full_bar[st], b * 64, base + t * kTileKeys, pol);
+            ptx::tma_load_2d(kdst + Cfg::kTileBytes + b * 4096, &tm_v, &full_bar[st], b * 64, base + t * kTileKeys,
+                             pol);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  int gt = 0;
+  for (int si = seg_begin; si < seg_end; ++si) {
+    const int sid = m.row_seg[si];
+    const int32_t* sg = m.seg + 5 * sid;
+    const int rq = sg[0], len = sg[3] - sg[2], off = sg[4];
+    const int qlen = m.req_qlen[rq], kvlen = m.req_kvlen[rq], qs = m.req_qstart[rq];
+    const int ntiles = (len + kTileKeys - 1) / kTileKeys;
+    const bool qrow = g8 < qlen;
+    const int qpos = kvlen - qlen + g8;
+
+    // Q (8 rows) split into hi/mid/lo bf16 planes in this warp's shared memory
+    const uint32_t qp_base = ptx::smem_u32(qplanes + static_cast<size_t>(warp) * 3 * MmaSmem<HD>::kQPlane);
+    __syncwarp();
+    for (int e = lane; e < 8 * HD / 8; e += 32) {  // one 16-B chunk (8 dims) per step
+      const int row = e / (HD / 8), chunk = e % (HD / 8);
+      float x[8];
+      if (row < qlen) {
+        const float4* src = reinterpret_cast<const float4*>(q + static_cast<size_t>(qs + row) * D + head * HD + chunk * 8);
+        const float4 a = src[0], b = src[1];
+        x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w, x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = 0.f;
+      }
+      uint32_t hi[4], mi[4], lo[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float h0 = bf_round(x[2 * i]), h1 = bf_round(x[2 * i + 1]);
+        const float r0 = x[2 * i] - h0, r1 = x[2 * i + 1] - h1;
+        const float m0 = bf_round(r0), m1 = bf_round(r1);
+        hi[i] = pack_bf2(h0, h1);
+        mi[i] = pack_bf2(m0, m1);
+        lo[i] = pack_bf2(r0 - m0, r1 - m1);
+      }
+      const uint32_t off = qswz<HD>(row, chunk);
+      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(qp_base + off), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]),
+                   "r"(hi[3]));
+      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(qp_base + MmaSmem<HD>::kQPlane + off), "r"(mi[0]),
+                   "r"(mi[1]), "r"(mi[2]), "r"(mi[3]));
+      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(qp_base + 2 * MmaSmem<HD>::kQPlane + off),
+                   "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]));
+    }
+    __syncwarp();
+    float mrun = -INFINITY, lsum = 0.f;
+    float2 o[DN];
+#pragma unroll
+    for (int dn = 0; dn < DN; ++dn) o[dn] = make_float2(0.f, 0.f);
+
+    // warp w owns the tiles whose CTA-global index gt+t is w mod 4 (its ring stages)
+    for (int t = ((warp - gt) % kConsumerWarps + kConsumerWarps) % kConsumerWarps; t < ntiles;
+         t += kConsumerWarps) {
+      const int gi = gt + t;
+      const int st = tile_stage<HD>(gi);
+      ptx::mbar_wait(&full_bar[st], tile_phase<HD>(gi));
+      const uint32_t ks_base = ptx::smem_u32(ring + static_cast<size_t>(st) * 2 * Cfg::kTileBytes);
+      const uint32_t vs_base = ks_base + Cfg::kTileBytes;
+      // ---- S = Q K^T for 4 tiles of 8 keys, 32 dims (two k-steps) at a time
+      float s[4][2];
+#pragma unroll
+      for (int n = 0; n < 4; ++n) s[n][0] = s[n][1] = 0.f;
+#pragma unroll
+      for (int kp = 0; kp < KS / 2; ++kp) {
+        uint32_t qa[3][4];  // per split: a0,a2 of k-step 2kp and a0,a2 of 2kp+1
+        const uint32_t qoff = qswz<HD>(lane & 7, kp * 4 + (lane >> 3));
+#pragma unroll
+        for (int sp = 0; sp < 3; ++sp)
+          ldsm_x4(qp_base + sp * MmaSmem<HD>::kQPlane + qoff, qa[sp][0], qa[sp][1], qa[sp][2], qa[sp][3]);
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(ks_base + swz(n * 8 + (lane & 7), kp * 4 + (lane >> 3)), b0, b1, b2, b3);
+#pragma unroll
+          for (int sp = 0; sp < 3; ++sp) {
+            mma_bf16(s[n][0], s[n][1], qa[sp][0], qa[sp][1], b0, b1);
+            mma_bf16(s[n][0], s[n][1], qa[sp][2], qa[sp][3], b2, b3);
+          }
+        }
+      }
+      // ---- online softmax on row g8 (quad reduction)
+      float tmax = -INFINITY;
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int kidx = t * kTileKeys + n * 8 + 2 * c4 + e;
+          const bool ok = qrow && kidx < len && off + kidx <= qpos;
+          s[n][e] = ok ? s[n][e] * g.scale : -INFINITY;
+          tmax = fmaxf(tmax, s[n][e]);
+        }
+      }
+      tmax = fmaxf(tmax, __shfl_xor_sync(kFull, tmax, 1));
+      tmax = fmaxf(tmax, __shfl_xor_sync(kFull, tmax, 2));
+      const float mnew = fmaxf(mrun, tmax);
+      const float corr = mnew == -INFINITY ? 1.f : expf(mrun - mnew);
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) s[n][e] = mnew == -INFINITY ? 0.f : expf(s[n][e] - mnew);
+      }
+      lsum = lsum * corr + (s[0][0] + s[0][1]) + (s[1][0] + s[1][1]) + (s[2][0] + s[2][1]) + (s[3][0] + s[3][1]);
+      mrun = mnew;
+#pragma unroll
+      for (int dn = 0; dn < DN; ++dn) o[dn] = fmul2(o[dn], make_float2(corr, corr));
+      // ---- O += P V over two 16-key steps, P split 2-way
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const float p00 = s[2 * kk][0], p01 = s[2 * kk][1], p10 = s[2 * kk + 1][0], p11 = s[2 * kk + 1][1];
+        const float h00 = bf_round(p00), h01 = bf_round(p01), h10 = bf_round(p10), h11 = bf_round(p11);
+        const uint32_t ah0 = pack_bf2(h00, h01), ah2 = pack_bf2(h10, h11);
+        const uint32_t al0 = pack_bf2(p00 - h00, p01 - h01), al2 = pack_bf2(p10 - h10, p11 - h11);
+        const int vrow = kk * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+        for (int dp = 0; dp < DN / 2; ++dp) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vs_base + swz(vrow, dp * 2 + (lane >> 4)), b0, b1, b2, b3);
+          mma_bf16(o[2 * dp].x, o[2 * dp].y, ah0, ah2, b0, b1);
+          mma_bf16(o[2 * dp].x, o[2 * dp].y, al0, al2, b0, b1);
+          mma_bf16(o[2 * dp + 1].x, o[2 * dp + 1].y, ah0, ah2, b2, b3);
+          mma_bf16(o[2 * dp + 1].x, o[2 * dp + 1].y, al0, al2, b2, b3);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty_bar[st]);
+    }
+    gt += ntiles;
+    // ---- this warp's partial for the segment (rows < qlen)
+    lsum += __shfl_xor_sync(kFull, lsum, 1);
+    lsum += __shfl_xor_sync(kFull, lsum, 2);
+    if (qrow) {
+      const size_t pi = ((static_cast<size_t>(sid) * H + head) * kMmaSub + warp) * w.qmax + g8;
+      if (c4 == 0) {
+        w.part_m[pi] = mrun;
+        w.part_l[pi] = lsum;
+      }
+      if (mrun != -INFINITY) {
+#pragma unroll
+        for (int dn = 0; dn < DN; ++dn) *reinterpret_cast<float2*>(w.part_o + pi * HD + dn * 8 + 2 * c4) = o[dn];
+      }
+    }
+  }
+}
+
 // Shared-max merge of a request's segment partials (attention.cpp:134-157).
 template <int HD>
-__global__ void attn_combine_kernel(FwdMeta m, AttnWork w, int H, bf16* out) {
+__global__ void attn_combine_kernel(FwdMeta m, AttnWork w, int H, int sub, bf16* out) {
   ptx::grid_dep_wait();
   const int rq = blockIdx.x, head = blockIdx.y, d = threadIdx.x;
   const int s0 = m.req_seg0[rq], ns = m.req_nseg[rq], qlen = m.req_qlen[rq], qs = m.req_qstart[rq];
+  // partials (segment, sub-partial) in a fixed order: deterministic
   for (int j = 0; j < qlen; ++j) {
     float M = -INFINITY;
-    for (int s = s0; s < s0 + ns; ++s) M = fmaxf(M, w.part_m[(static_cast<size_t>(s) * H + head) * w.qmax + j]);
+    for (int s = s0; s < s0 + ns; ++s)
+      for (int u = 0; u < sub; ++u)
+        M = fmaxf(M, w.part_m[((static_cast<size_t>(s) * H + head) * sub + u) * w.qmax + j]);
     float L = 0.f, O = 0.f;
     for (int s = s0; s < s0 + ns; ++s) {
-      const size_t pi = (static_cast<size_t>(s) * H + head) * w.qmax + j;
-      const float ms = w.part_m[pi];
-      const float f = ms == -INFINITY ? 0.f : expf(ms - M);
-      L += w.part_l[pi] * f;
-      O += w.part_o[pi * HD + d] * f;
+      for (int u = 0; u < sub; ++u) {
+        const size_t pi = ((static_cast<size_t>(s) * H + head) * sub + u) * w.qmax + j;
+        const float ms = w.part_m[pi];
+        if (ms == -INFINITY) continue;
+        const float f = expf(ms - M);
+        L += w.part_l[pi] * f;
+        O += w.part_o[pi * HD + d] * f;
+      }
     }
     out[static_cast<size_t>(qs + j) * H * HD + head * HD + d] = __float2bfloat16_rn(O / L);
   }
@@ -358,21 +622,48 @@ void launch_attn_t(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMe
   cfg.gridDim = dim3(n_req, g.n_heads);
   cfg.blockDim = dim3(HD);
   cfg.dynamicSmemBytes = 0;
-  cudaLaunchKernelEx(&cfg, attn_combine_kernel<HD>, m, ww, g.n_heads, out);
+  cudaLaunchKernelEx(&cfg, attn_combine_kernel<HD>, m, ww, g.n_heads, 1, out);
+}
+
+template <int HD>
+void launch_attn_mma(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m, int n_rows, int n_req,
+                     const AttnGeom& g, const float* q, const AttnWork& w, bf16* out, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(attention_mma_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(MmaSmem<HD>::kTotal));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.stream = s;
+  cfg.gridDim = dim3(n_rows, g.n_heads);
+  cfg.blockDim = dim3(kAttnThreads);
+  cfg.dynamicSmemBytes = MmaSmem<HD>::kTotal;
+  AttnWork ww = w;
+  ww.qmax = 8;
+  cudaLaunchKernelEx(&cfg, attention_mma_kernel<HD>, tm_k, tm_v, m, g, q, ww);
+  cfg.gridDim = dim3(n_req, g.n_heads);
+  cfg.blockDim = dim3(HD);
+  cfg.dynamicSmemBytes = 0;
+  cudaLaunchKernelEx(&cfg, attn_combine_kernel<HD>, m, ww, g.n_heads, kMmaSub, out);
 }
 
 }  // namespace
 
 void launch_attention(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m, int n_rows, int n_req,
                       const AttnGeom& g, const float* q, const AttnWork& w, bf16* out, cudaStream_t s) {
-  // w.qmax selects the instantiation: the largest query count per request.
+  // w.qmax = the largest query count per request: <= 8 runs on the tensor
+  // cores (mma.sync), 9..17 on the CUDA-core kernel.
   if (g.head_dim == 128) {
-    if (w.qmax <= 2) return launch_attn_t<128, 2>(tm_k, tm_v, m, n_rows, n_req, g, q, w, out, s);
-    if (w.qmax <= 8) return launch_attn_t<128, 8>(tm_k, tm_v, m, n_rows, n_req, g, q, w, out, s);
+    if (w.qmax <= 8) return launch_attn_mma<128>(tm_k, tm_v, m, n_rows, n_req, g, q, w, out, s);
     return launch_attn_t<128, 17>(tm_k, tm_v, m, n_rows, n_req, g, q, w, out, s);
   }
-  if (w.qmax <= 2) return launch_attn_t<64, 2>(tm_k, tm_v, m, n_rows, n_req, g, q, w, out, s);
-  if (w.qmax <= 8) return launch_attn_t<64, 8>(tm_k, tm_v, m, n_rows, n_req, g, q, w, out, s);
+  if (w.qmax <= 8) return launch_attn_mma<64>(tm_k, tm_v, m, n_rows, n_req, g, q, w, out, s);
   return launch_attn_t<64, 17>(tm_k, tm_v, m, n_rows, n_req, g, q, w, out, s);
 }
 

@@ -311,6 +311,14 @@ spin_status spin_round_launches(spin_ctx* ctx, int32_t n, const int32_t* slots, 
   });
 }
 
+spin_status spin_kernel_bench(spin_ctx* ctx, int32_t kind, int32_t iters, double* us_per_launch,
+                              double* bytes_per_launch) {
+  return guarded([&] {
+    if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
+    ctx->eng->kernel_bench(kind, iters, us_per_launch, bytes_per_launch);
+  });
+}
+
 spin_status spin_switch_ssm(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of) {
   return guarded([&] {
     if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
@@ -362,7 +370,7 @@ spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int3
     int32_t* d_ints = nullptr;
     float* d_part = nullptr;
     check_cuda(cudaMalloc(&d_ints, ints.size() * 4), "malloc");
-    const size_t np = static_cast<size_t>(nseg) * n_heads * 17;
+    const size_t np = static_cast<size_t>(nseg) * n_heads * 32;
     check_cuda(cudaMalloc(&d_part, np * (2 + head_dim) * 4), "malloc");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     check_cuda(cudaMemcpyAsync(d_ints, ints.data(), ints.size() * 4, cudaMemcpyHostToDevice, s), "h2d");

@@ -196,7 +196,7 @@ void Engine::init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool l
     }
   }
   ln.part = dalloc<float>(A, part);
-  const size_t np = static_cast<size_t>(ln.seg_cap) * m.H * 17;
+  const size_t np = static_cast<size_t>(ln.seg_cap) * m.H * 32;  // max(4 warps x 8 q, 1 x 17 q)
   ln.aw.part_m = dalloc<float>(A, np);
   ln.aw.part_l = dalloc<float>(A, np);
   ln.aw.part_o = dalloc<float>(A, np * m.hd);
@@ -763,6 +763,79 @@ void Engine::profile_round(int n, const int32_t* slots, const int32_t* ssm_of, d
     cudaEventDestroy(r.b);
   }
   prof_recs_.clear();
+}
+
+// In-situ kernel benchmark on the target's state of the last verify: kind 0
+// replays the 4 projection GEMMs of every layer, kind 1 the attention (+combine)
+// of every layer, as one CUDA graph launched `iters` times; per-launch device
+// time and algorithmic bytes (weights + activations in/out, or KV read + q/out).
+void Engine::kernel_bench(int kind, int iters, double* us_per_launch, double* bytes_per_launch) {
+  sync_state_from_device();
+  const int T = last_verify_rows_;
+  if (T <= 0) fail(SPIN_INPUT_ERROR, "kernel_bench: run a round first");
+  if (iters < 1) fail(SPIN_INPUT_ERROR, "kernel_bench: iters must be >= 1");
+  ModelDev& m = target_;
+  Lane& ln = tlane_;
+  const int D = m.D, F = m.F, n = T / (opts_.window + 1);
+  const bool pdl = opts_.use_pdl != 0;
+  double bytes = 0.0;
+  int launches = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  check_cuda(cudaStreamBeginCapture(sv_, cudaStreamCaptureModeRelaxed), "capture");
+  capturing_ = true;
+  GemmEpilogue ep;
+  ep.mode = kGemmPartial;
+  ep.part = ln.part;
+  AttnGeom g{m.H, m.hd, opts_.max_requests, opts_.max_ctx, 0, static_cast<float>(1.0 / std::sqrt(double(m.hd))),
+             m.kc, m.vc};
+  AttnWork aw = ln.aw;
+  aw.qmax = opts_.window + 1;
+  double kv_tokens = 0.0;
+  for (int l = 0; l < m.L; ++l) {
+    const LayerW& w = m.layers[l];
+    if (kind == 0) {
+      const int shapes[4][2] = {{3 * D, D}, {D, D}, {2 * F, D}, {D, F}};
+      const bf16* W[4] = {w.qkv, w.o, w.gu, w.dn};
+      const bf16* X[4] = {ln.xn, ln.attn, ln.xn, ln.act};
+      for (int k = 0; k < 4; ++k) {
+        check_cuda(gemm_launch(plan(shapes[k][0], shapes[k][1], T, kGemmPartial), W[k], X[k], ep, sv_, pdl), "gemm");
+        bytes += 2.0 * shapes[k][0] * shapes[k][1] + 2.0 * T * shapes[k][1] + 2.0 * T * shapes[k][0];
+        ++launches;
+      }
+    } else {
+      g.layer = l;
+      launch_attention(m.tm_k, m.tm_v, ln.meta, opts_.pack_width > 0 ? std::min(opts_.pack_width, n) : n, n, g, ln.q,
+                       aw, ln.attn, sv_);
+      ++launches;
+    }
+  }
+  capturing_ = false;
+  check_cuda(cudaStreamEndCapture(sv_, &graph), "capture");
+  check_cuda(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+  if (kind == 1) {
+    // KV bytes actually read: per request kv_len = committed + window at verify time
+    std::vector<int32_t> kvl(n);
+    check_cuda(cudaMemcpy(kvl.data(), ln.meta.req_kvlen, n * 4, cudaMemcpyDeviceToHost), "d2h");
+    for (int i = 0; i < n; ++i) kv_tokens += kvl[i];
+    bytes = static_cast<double>(m.L) * (kv_tokens * m.H * m.hd * 2.0 * 2.0 + T * D * 4.0 + T * D * 2.0);
+  }
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  check_cuda(cudaGraphLaunch(exec, sv_), "warm");
+  check_cuda(cudaEventRecord(a, sv_), "event");
+  for (int i = 0; i < iters; ++i) check_cuda(cudaGraphLaunch(exec, sv_), "graph");
+  check_cuda(cudaEventRecord(b, sv_), "event");
+  check_cuda(cudaStreamSynchronize(sv_), "sync");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
+  *us_per_launch = ms * 1e3 / (static_cast<double>(iters) * launches);
+  *bytes_per_launch = bytes / launches;
 }
 
 int64_t Engine::launches_per_round(int n, const int32_t* slots, const int32_t* ssm_of) {

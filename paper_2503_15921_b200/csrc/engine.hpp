@@ -79,6 +79,7 @@ class Engine {
   void profile_round(int n, const int32_t* slots, const int32_t* ssm_of, double* ms, double* bytes,
                      int64_t* launches);
   int64_t launches_per_round(int n, const int32_t* slots, const int32_t* ssm_of);
+  void kernel_bench(int kind, int iters, double* us_per_launch, double* bytes_per_launch);
 
  private:
   struct RoundPlan;

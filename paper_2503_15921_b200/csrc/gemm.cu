@@ -338,7 +338,11 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
   m.bn = p.bn;
   m.units = n_tiles * p.kb;
   if (mode == kGemmPartial) {
-    m.grid = static_cast<int>(std::min<long long>(num_sms, m.units));
+    // At least kMinUnits k-blocks (128 KiB of weights) per CTA: small draft
+    // GEMMs then use fewer SMs instead of fragmenting every tile into many
+    // partial pieces that the consumer must re-read.
+    constexpr long long kMinUnits = 8;
+    m.grid = static_cast<int>(std::min<long long>(num_sms, std::max<long long>(1, (m.units + kMinUnits - 1) / kMinUnits)));
     // Worst-case pieces per tile: a tile spans ceil(kb / per_cta) + 1 CTAs.
     int mp = 1;
     for (long long tile = 0; tile < n_tiles; ++tile) mp = std::max(mp, m.pieces(static_cast<int>((tile / p.n_mtiles) * p.bn), static_cast<int>((tile % p.n_mtiles) * kBlockM)));

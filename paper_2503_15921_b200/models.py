@@ -166,6 +166,13 @@ class Engine:
         _lib.check(self.lib.spin_round_launches(self.ctx, len(slots), _p(slots), _p(ssm_of), C.byref(v)))
         return v.value
 
+    def kernel_bench(self, kind: str, iters: int = 5):
+        """(us per launch, algorithmic bytes per launch) of the target's GEMMs ("gemm") or attention ("attention")."""
+        us, by = C.c_double(), C.c_double()
+        _lib.check(self.lib.spin_kernel_bench(self.ctx, {"gemm": 0, "attention": 1}[kind], iters, C.byref(us),
+                                              C.byref(by)))
+        return us.value, by.value
+
     def switch(self, slots, ssm_of):
         slots = np.ascontiguousarray(slots, dtype=np.int32)
         ssm_of = np.ascontiguousarray(ssm_of, dtype=np.int32)

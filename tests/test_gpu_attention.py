@@ -50,3 +50,24 @@ def test_attention_matches_torch(hd, H, width, qlen):
     assert err <= 1e-2, err  # bf16 output rounding (|o| ~ 1)
     mism = (out.float() != ref.to(torch.bfloat16).float()).float().mean().item()
     assert mism < 0.02, mism
+
+
+@pytest.mark.parametrize("hd,qlen,width", [(128, 5, 3), (128, 8, 2), (64, 2, 3), (128, 12, 2)])
+def test_attention_many_segments_per_row(hd, qlen, width):
+    """Rows holding several segments whose tile counts are not multiples of the
+    consumer-warp count (ring-stage ownership across segment boundaries)."""
+    g = torch.Generator(device="cpu").manual_seed(7 * hd + qlen)
+    H, L, S, ctx = 2, 1, 12, 1100
+    kc = torch.randn((L, S, H, ctx, hd), generator=g).to(torch.bfloat16).cuda()
+    vc = torch.randn((L, S, H, ctx, hd), generator=g).to(torch.bfloat16).cuda()
+    slots = np.arange(S, dtype=np.int32)[::-1].copy()
+    kvl = np.array([37, 101, 1033, 64, 65, 200, 300, 33, 511, 97, 129, 700], np.int32)
+    kvl = np.maximum(kvl, qlen).astype(np.int32)
+    qls = np.full(S, qlen, np.int32)
+    q = torch.randn((int(qls.sum()), H * hd), generator=g).cuda()
+    out = torch.empty((int(qls.sum()), H * hd), dtype=torch.bfloat16, device="cuda")
+    P = lambda a: a.ctypes.data_as(_lib.P_I32)
+    _lib.check(_lib.load().spin_attention(None, H, hd, L, S, ctx, 0, kc.data_ptr(), vc.data_ptr(), q.data_ptr(), S,
+                                          P(slots), P(qls), P(kvl), width, out.data_ptr()))
+    ref = torch_ref(q, kc, vc, 0, slots, qls, kvl, H, hd)
+    assert (out.float() - ref).abs().max().item() <= 1e-2
