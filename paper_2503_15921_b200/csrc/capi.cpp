@@ -382,8 +382,8 @@ spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int3
                const_cast<bf16*>(static_cast<const bf16*>(k_cache)), const_cast<bf16*>(static_cast<const bf16*>(v_cache))};
     CUtensorMap tk, tv;
     const uint64_t rows = static_cast<uint64_t>(layers) * slots * n_heads * ctx;
-    if (!encode_tmap_bf16(&tk, k_cache, rows, head_dim, 32, 64, true) ||
-        !encode_tmap_bf16(&tv, v_cache, rows, head_dim, 32, 64, true))
+    if (!encode_tmap_bf16(&tk, k_cache, rows, head_dim, 16, 64, true) ||
+        !encode_tmap_bf16(&tv, v_cache, rows, head_dim, 16, 64, true))
       fail(SPIN_CUDA_ERROR, "tensor map encode");
     AttnWork w{d_part, d_part + np, d_part + 2 * np, qmax};
     launch_attention(tk, tv, m, p.rows, n_req, g, static_cast<const float*>(q), w, static_cast<bf16*>(out), s);

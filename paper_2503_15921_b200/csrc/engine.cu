@@ -136,8 +136,8 @@ void Engine::init_model(ModelDev& m, const spin_model_desc& d) {
   check_cuda(cudaMemsetAsync(m.kc, 0, kv * 2, sv_), "memset");
   check_cuda(cudaMemsetAsync(m.vc, 0, kv * 2, sv_), "memset");
   const uint64_t rows = static_cast<uint64_t>(m.L) * opts_.max_requests * m.H * opts_.max_ctx;
-  if (!encode_tmap_bf16(&m.tm_k, m.kc, rows, m.hd, 32, 64, true) ||
-      !encode_tmap_bf16(&m.tm_v, m.vc, rows, m.hd, 32, 64, true))
+  if (!encode_tmap_bf16(&m.tm_k, m.kc, rows, m.hd, 16, 64, true) ||
+      !encode_tmap_bf16(&m.tm_v, m.vc, rows, m.hd, 16, 64, true))
     fail(SPIN_CUDA_ERROR, "KV tensor map encode failed");
   // RoPE tables in double, rounded once (matches the oracle bit for bit).
   const int half = m.hd / 2;
