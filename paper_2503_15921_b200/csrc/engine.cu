@@ -158,7 +158,17 @@ void Engine::init_model(ModelDev& m, const spin_model_desc& d) {
 const GemmPlan& Engine::plan(int n_out, int k, int t, int mode) {
   const auto key = std::make_tuple(n_out, k, t, mode);
   auto it = plans_.find(key);
-  if (it == plans_.end()) it = plans_.emplace(key, gemm_plan(n_out, k, t, mode, num_sms_)).first;
+  if (it == plans_.end()) {
+    GemmPlan p = gemm_plan(n_out, k, t, mode, num_sms_);
+    if (!p.tile_pieces.empty()) {  // device copy of the stream-K piece table (consumer kernels)
+      void* d = nullptr;
+      check_cuda(cudaMalloc(&d, p.tile_pieces.size()), "piece table");
+      check_cuda(cudaMemcpy(d, p.tile_pieces.data(), p.tile_pieces.size(), cudaMemcpyHostToDevice), "piece table");
+      p.map.tbl = static_cast<const uint8_t*>(d);
+      plan_tables_.push_back(d);
+    }
+    it = plans_.emplace(key, std::move(p)).first;
+  }
   return it->second;
 }
 
@@ -363,6 +373,7 @@ Engine::~Engine() {
   for (auto& l : slane_)
     for (void* p : l.allocs) cudaFree(p);
   cudaFree(st_.tokens), cudaFree(st_.committed), cudaFree(st_.ssm_len), cudaFree(st_.drafts);
+  for (void* p : plan_tables_) cudaFree(p);
   cudaFreeHost(pin_in_), cudaFreeHost(pin_out_), cudaFree(d_in_), cudaFree(d_out_), cudaFree(d_emitted_);
   cudaEventDestroy(ev_fork_), cudaEventDestroy(ev_start_), cudaEventDestroy(ev_draft_), cudaEventDestroy(ev_end_);
   for (auto& e : ev_join_) cudaEventDestroy(e);

@@ -114,6 +114,7 @@ class Engine {
   std::vector<cudaStream_t> ss_;
   std::map<std::tuple<int, int, int, int>, GemmPlan> plans_;
   const GemmPlan& plan(int n_out, int k, int t, int mode);
+  std::vector<void*> plan_tables_;
 
   // host mirror of the per-slot state
   std::vector<int32_t> h_tokens_, h_committed_, h_ssm_len_;

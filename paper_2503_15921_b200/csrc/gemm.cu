@@ -345,7 +345,12 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
     m.grid = static_cast<int>(std::min<long long>(num_sms, std::max<long long>(1, (m.units + kMinUnits - 1) / kMinUnits)));
     // Worst-case pieces per tile: a tile spans ceil(kb / per_cta) + 1 CTAs.
     int mp = 1;
-    for (long long tile = 0; tile < n_tiles; ++tile) mp = std::max(mp, m.pieces(static_cast<int>((tile / p.n_mtiles) * p.bn), static_cast<int>((tile % p.n_mtiles) * kBlockM)));
+    p.tile_pieces.resize(n_tiles);
+    for (long long tile = 0; tile < n_tiles; ++tile) {
+      const int np = m.pieces(static_cast<int>((tile / p.n_mtiles) * p.bn), static_cast<int>((tile % p.n_mtiles) * kBlockM));
+      p.tile_pieces[tile] = static_cast<uint8_t>(np);
+      mp = std::max(mp, np);
+    }
     p.max_pieces = mp;
   } else {
     m.grid = static_cast<int>(std::min<long long>(num_sms, n_tiles));

@@ -21,6 +21,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 namespace spin {
 
 enum GemmMode : int { kGemmPartial = 0, kGemmArgmax = 1 };
@@ -33,6 +35,7 @@ struct PieceMap {
   int n_mtiles;     // 128-row tiles over N_out
   int bn;           // token tile
   int mode;         // GemmMode
+  const uint8_t* tbl = nullptr;  // device: pieces per tile (filled by the host at plan time)
 
   // CTA that owns stream-K unit u.
   __host__ __device__ __forceinline__ int cta_of(long long u) const {
@@ -44,10 +47,12 @@ struct PieceMap {
     const long long tile = static_cast<long long>(t / bn) * n_mtiles + n / 128;
     return cta_of(tile * kb + kb - 1) - cta_of(tile * kb) + 1;
   }
+  __device__ __forceinline__ int tile_pieces(int t, int n) const { return tbl[(t / bn) * n_mtiles + n / 128]; }
 };
 
 struct GemmPlan {
   int n_out = 0, k = 0, t = 0;
+  std::vector<uint8_t> tile_pieces;  // host copy of PieceMap::tbl
   int bn = 0, n_ntiles = 0, n_mtiles = 0, kb = 0;
   int grid = 0, stages = 0, max_pieces = 1;
   size_t smem_bytes = 0;

@@ -13,23 +13,21 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// Stream-K piece counts of the m-tiles a row touches, staged once per block
-// (the 64-bit divisions of PieceMap::pieces stay out of the element loop).
-constexpr int kMaxMTiles = 512;
-
-__device__ __forceinline__ void stage_pieces(const PieceMap& pm, int t, int n_begin, int n_end, uint8_t* s_np) {
-  const int m0 = n_begin / 128, m1 = (n_end + 127) / 128;
-  for (int m = m0 + static_cast<int>(threadIdx.x); m < m1; m += blockDim.x)
-    s_np[m - m0] = static_cast<uint8_t>(pm.pieces(t, m * 128));
-}
-
-__device__ __forceinline__ float sum_pieces_t(const float* __restrict__ part, const uint8_t* s_np, int m0, int T,
-                                              int n_out, int t, int n) {
-  const int np = s_np[n / 128 - m0];
+// Fixed-order sum of the stream-K partial slots of 4 consecutive features
+// (slot 0..np-1, deterministic); np comes from the plan's host-built piece table.
+__device__ __forceinline__ float4 sum_pieces4(const float* __restrict__ part, const PieceMap& pm, int T, int n_out,
+                                              int t, int n) {
+  const int np = pm.tile_pieces(t, n);
   const size_t stride = static_cast<size_t>(T) * n_out;
   const float* p = part + static_cast<size_t>(t) * n_out + n;
-  float acc = p[0];
-  for (int s = 1; s < np; ++s) acc = __fadd_rn(acc, p[s * stride]);
+  float4 acc = __ldg(reinterpret_cast<const float4*>(p));
+  for (int s = 1; s < np; ++s) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p + s * stride));
+    acc.x = __fadd_rn(acc.x, v.x);
+    acc.y = __fadd_rn(acc.y, v.y);
+    acc.z = __fadd_rn(acc.z, v.z);
+    acc.w = __fadd_rn(acc.w, v.w);
+  }
   return acc;
 }
 
@@ -253,7 +251,15 @@ __device__ __forceinline__ void rmsnorm_row(const float* row, int D, float eps, 
   for (int i = threadIdx.x; i < D; i += blockDim.x) ss += row[i] * row[i];
   const float tot = block_sum(ss, red);
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(tot, static_cast<float>(D)), eps)));
-  for (int i = threadIdx.x; i < D; i += blockDim.x) xn[i] = __float2bfloat16_rn(__fmul_rn(row[i], inv));
+  for (int i = 4 * threadIdx.x; i < D; i += 4 * blockDim.x) {
+    const float4 v = *reinterpret_cast<const float4*>(row + i);
+    __nv_bfloat162 a = __floats2bfloat162_rn(__fmul_rn(v.x, inv), __fmul_rn(v.y, inv));
+    __nv_bfloat162 b = __floats2bfloat162_rn(__fmul_rn(v.z, inv), __fmul_rn(v.w, inv));
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(xn + i) = u;
+  }
 }
 
 __global__ void __launch_bounds__(kRowThreads) embed_norm_kernel(const bf16* __restrict__ emb, const int32_t* tok,
@@ -268,84 +274,100 @@ __global__ void __launch_bounds__(kRowThreads) embed_norm_kernel(const bf16* __r
     s_row[i] = v;
     h[static_cast<size_t>(t) * D + i] = v;
   }
+  __syncthreads();
   ptx::grid_dep_launch();
   rmsnorm_row(s_row, D, eps, xn + static_cast<size_t>(t) * D, red);
 }
 
+// h += sum of the stream-K partials; xn = bf16(rmsnorm(h)). 4 features / thread.
 __global__ void __launch_bounds__(kRowThreads) resid_norm_kernel(const float* __restrict__ part, PieceMap pm, int T,
                                                                  int D, float eps, float* h, bf16* xn) {
   extern __shared__ float s_row[];
   __shared__ float red[32];
-  __shared__ uint8_t s_np[kMaxMTiles];
-  const int t = blockIdx.x;
-  stage_pieces(pm, t, 0, D, s_np);
   ptx::grid_dep_wait();
-  __syncthreads();
-  for (int i = threadIdx.x; i < D; i += kRowThreads) {
-    const size_t o = static_cast<size_t>(t) * D + i;
-    const float v = __fadd_rn(h[o], sum_pieces_t(part, s_np, 0, T, D, t, i));
-    s_row[i] = v;
-    h[o] = v;
+  const int t = blockIdx.x;
+  for (int i = 4 * threadIdx.x; i < D; i += 4 * kRowThreads) {
+    float4* hp = reinterpret_cast<float4*>(h + static_cast<size_t>(t) * D + i);
+    const float4 y = sum_pieces4(part, pm, T, D, t, i);
+    float4 v = *hp;
+    v.x = __fadd_rn(v.x, y.x), v.y = __fadd_rn(v.y, y.y), v.z = __fadd_rn(v.z, y.z), v.w = __fadd_rn(v.w, y.w);
+    *hp = v;
+    *reinterpret_cast<float4*>(s_row + i) = v;
   }
+  __syncthreads();
   ptx::grid_dep_launch();
   rmsnorm_row(s_row, D, eps, xn + static_cast<size_t>(t) * D, red);
 }
 
-// grid (T, ceil(F / 256)): one thread per SwiGLU output.
+// grid (T, ceil(F / 1024)): 4 SwiGLU outputs per thread.
 __global__ void __launch_bounds__(kRowThreads) swiglu_kernel(const float* __restrict__ part, PieceMap pm, int T, int F,
                                                              bf16* act) {
-  __shared__ uint8_t s_np_g[8], s_np_u[8];
-  const int t = blockIdx.x;
-  const int f0 = blockIdx.y * kRowThreads;
-  const int f1 = min(F, f0 + kRowThreads);
-  stage_pieces(pm, t, f0, f1, s_np_g);
-  stage_pieces(pm, t, F + f0, F + f1, s_np_u);
   ptx::grid_dep_wait();
-  __syncthreads();
-  const int f = f0 + threadIdx.x;
+  const int t = blockIdx.x;
+  const int f = 4 * (blockIdx.y * kRowThreads + threadIdx.x);
   if (f < F) {
-    const float g = sum_pieces_t(part, s_np_g, f0 / 128, T, 2 * F, t, f);
-    const float u = sum_pieces_t(part, s_np_u, (F + f0) / 128, T, 2 * F, t, F + f);
-    const float sg = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
-    act[static_cast<size_t>(t) * F + f] = __float2bfloat16_rn(__fmul_rn(sg, u));
+    const float4 g = sum_pieces4(part, pm, T, 2 * F, t, f);
+    const float4 u = sum_pieces4(part, pm, T, 2 * F, t, F + f);
+    const float gs[4] = {g.x, g.y, g.z, g.w}, us[4] = {u.x, u.y, u.z, u.w};
+    float r[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[i] = __fmul_rn(__fdiv_rn(gs[i], __fadd_rn(1.0f, expf(-gs[i]))), us[i]);
+    __nv_bfloat162 a = __floats2bfloat162_rn(r[0], r[1]), b = __floats2bfloat162_rn(r[2], r[3]);
+    uint2 o;
+    o.x = *reinterpret_cast<uint32_t*>(&a);
+    o.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(act + static_cast<size_t>(t) * F + f) = o;
   }
   ptx::grid_dep_launch();
 }
 
 // Split-K reduction of the fused QKV projection, RoPE (rotate-half) on q and k,
 // q -> fp32 (feeds only the CUDA-core attention), k/v -> bf16 KV cache at
-// (layer, slot, head, pos). grid (T, ceil(H*hd/2 / 256)): one thread per
-// rotary pair.
+// (layer, slot, head, pos). grid (T, ceil(H*hd/2 / 1024)): 4 rotary pairs / thread.
 __global__ void __launch_bounds__(kRowThreads) qkv_epilogue_kernel(const float* __restrict__ part, PieceMap pm,
                                                                    FwdMeta m, int T, AttnGeom g,
                                                                    const float* __restrict__ rcos,
                                                                    const float* __restrict__ rsin, float* q) {
-  __shared__ uint8_t s_np[kMaxMTiles];
+  ptx::grid_dep_wait();
   const int t = blockIdx.x;
   const int H = g.n_heads, hd = g.head_dim, half = hd / 2, D = H * hd, N = 3 * D;
-  stage_pieces(pm, t, 0, N, s_np);
-  ptx::grid_dep_wait();
-  __syncthreads();
-  const int pi = blockIdx.y * kRowThreads + threadIdx.x;
-  if (pi < H * half) {
+  const int p4 = 4 * (blockIdx.y * kRowThreads + threadIdx.x);  // first of 4 rotary pairs
+  if (p4 < H * half) {
     const int slot = m.row_slot[t], pos = m.row_pos[t];
-    const int hh = pi / half, i = pi % half;
+    const int hh = p4 / half, i = p4 % half;
     const int nq = hh * hd + i;
-    const float q0 = sum_pieces_t(part, s_np, 0, T, N, t, nq), q1 = sum_pieces_t(part, s_np, 0, T, N, t, nq + half);
-    const float k0 = sum_pieces_t(part, s_np, 0, T, N, t, D + nq);
-    const float k1 = sum_pieces_t(part, s_np, 0, T, N, t, D + nq + half);
-    const float v0 = sum_pieces_t(part, s_np, 0, T, N, t, 2 * D + nq);
-    const float v1 = sum_pieces_t(part, s_np, 0, T, N, t, 2 * D + nq + half);
-    const float c = rcos[static_cast<size_t>(pos) * half + i], s = rsin[static_cast<size_t>(pos) * half + i];
+    const float4 q0 = sum_pieces4(part, pm, T, N, t, nq), q1 = sum_pieces4(part, pm, T, N, t, nq + half);
+    const float4 k0 = sum_pieces4(part, pm, T, N, t, D + nq), k1 = sum_pieces4(part, pm, T, N, t, D + nq + half);
+    const float4 v0 = sum_pieces4(part, pm, T, N, t, 2 * D + nq), v1 = sum_pieces4(part, pm, T, N, t, 2 * D + nq + half);
+    const float4 c = *reinterpret_cast<const float4*>(rcos + static_cast<size_t>(pos) * half + i);
+    const float4 s = *reinterpret_cast<const float4*>(rsin + static_cast<size_t>(pos) * half + i);
+    const float qa[4] = {q0.x, q0.y, q0.z, q0.w}, qb[4] = {q1.x, q1.y, q1.z, q1.w};
+    const float ka[4] = {k0.x, k0.y, k0.z, k0.w}, kb[4] = {k1.x, k1.y, k1.z, k1.w};
+    const float cs[4] = {c.x, c.y, c.z, c.w}, sn[4] = {s.x, s.y, s.z, s.w};
+    float qo0[4], qo1[4], ko0[4], ko1[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      qo0[e] = __fsub_rn(__fmul_rn(qa[e], cs[e]), __fmul_rn(qb[e], sn[e]));
+      qo1[e] = __fadd_rn(__fmul_rn(qb[e], cs[e]), __fmul_rn(qa[e], sn[e]));
+      ko0[e] = __fsub_rn(__fmul_rn(ka[e], cs[e]), __fmul_rn(kb[e], sn[e]));
+      ko1[e] = __fadd_rn(__fmul_rn(kb[e], cs[e]), __fmul_rn(ka[e], sn[e]));
+    }
     float* qo = q + static_cast<size_t>(t) * D + nq;
-    qo[0] = __fsub_rn(__fmul_rn(q0, c), __fmul_rn(q1, s));
-    qo[half] = __fadd_rn(__fmul_rn(q1, c), __fmul_rn(q0, s));
+    *reinterpret_cast<float4*>(qo) = make_float4(qo0[0], qo0[1], qo0[2], qo0[3]);
+    *reinterpret_cast<float4*>(qo + half) = make_float4(qo1[0], qo1[1], qo1[2], qo1[3]);
     if (slot >= 0) {
       const size_t kv = ((((static_cast<size_t>(g.layer) * g.slots + slot) * H + hh) * g.ctx) + pos) * hd + i;
-      g.k_cache[kv] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(k0, c), __fmul_rn(k1, s)));
-      g.k_cache[kv + half] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(k1, c), __fmul_rn(k0, s)));
-      g.v_cache[kv] = __float2bfloat16_rn(v0);
-      g.v_cache[kv + half] = __float2bfloat16_rn(v1);
+      auto put4 = [](bf16* dst, float a, float b, float c2, float d) {
+        __nv_bfloat162 x = __floats2bfloat162_rn(a, b), y = __floats2bfloat162_rn(c2, d);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&x);
+        u.y = *reinterpret_cast<uint32_t*>(&y);
+        *reinterpret_cast<uint2*>(dst) = u;
+      };
+      put4(g.k_cache + kv, ko0[0], ko0[1], ko0[2], ko0[3]);
+      put4(g.k_cache + kv + half, ko1[0], ko1[1], ko1[2], ko1[3]);
+      put4(g.v_cache + kv, v0.x, v0.y, v0.z, v0.w);
+      put4(g.v_cache + kv + half, v1.x, v1.y, v1.z, v1.w);
     }
   }
   ptx::grid_dep_launch();
@@ -535,8 +557,8 @@ void launch_embed_norm(const bf16* emb, const FwdMeta& m, int T, int D, float ep
 void launch_qkv_epilogue(const float* part, const PieceMap& pm, const FwdMeta& m, int T, const AttnGeom& g,
                          const float* rcos, const float* rsin, float* q, cudaStream_t s) {
   const int pairs = g.n_heads * g.head_dim / 2;
-  launch_pdl(qkv_epilogue_kernel, dim3(T, (pairs + kRowThreads - 1) / kRowThreads), dim3(kRowThreads), 0, s, part, pm,
-             m, T, g, rcos, rsin, q);
+  launch_pdl(qkv_epilogue_kernel, dim3(T, (pairs + 4 * kRowThreads - 1) / (4 * kRowThreads)), dim3(kRowThreads), 0, s,
+             part, pm, m, T, g, rcos, rsin, q);
 }
 
 void launch_resid_norm(const float* part, const PieceMap& pm, int T, int D, float eps, float* h, bf16* xn,
@@ -545,8 +567,8 @@ void launch_resid_norm(const float* part, const PieceMap& pm, int T, int D, floa
 }
 
 void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* act, cudaStream_t s) {
-  launch_pdl(swiglu_kernel, dim3(T, (F + kRowThreads - 1) / kRowThreads), dim3(kRowThreads), 0, s, part, pm, T, F,
-             act);
+  launch_pdl(swiglu_kernel, dim3(T, (F + 4 * kRowThreads - 1) / (4 * kRowThreads)), dim3(kRowThreads), 0, s, part, pm,
+             T, F, act);
 }
 
 void launch_accept(const FwdMeta& m, int n_req, int window, const int32_t* list, const int32_t* ssm_of_req,
