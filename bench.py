@@ -236,15 +236,11 @@ def main():
         dist.all_reduce(t)
         return t.item()
 
-    # per-(request, SSM) acceptance statistics, ArmEstimate{sum,count} (bandit.hpp:24-39)
-    est = torch.zeros((BATCH, 2, 2), dtype=torch.float64, device="cuda")
-    gathered = torch.zeros((world, BATCH, 2, 2), dtype=torch.float64, device="cuda")
+    # per-(request, SSM) acceptance statistics, ArmEstimate{sum,count} (bandit.hpp:24-39),
+    # all-gathered over NCCL every step (the only collective of the path)
+    from paper_2503_15921_b200.dist import AcceptanceStats
 
-    def gather_stats():
-        if dist is not None:
-            dist.all_gather_into_tensor(gathered, est)
-        else:
-            gathered[0].copy_(est)
+    stats = AcceptanceStats(BATCH * world, 2, world, rank, device="cuda")
 
     # ---- warm-up (graph capture, clocks, caches)
     for _ in range(args.warmup):
@@ -267,9 +263,8 @@ def main():
             e2e_tokens += int(out["accepted"].sum()) + BATCH
             wall = out["round_ms"] / 1e3
             for i in range(BATCH):
-                est[i, assign[i], 0] += (out["accepted"][i] + 1) / wall
-                est[i, assign[i], 1] += 1
-            gather_stats()
+                stats.add(i, int(assign[i]), (out["accepted"][i] + 1) / wall)
+            stats.gather(dist)
             verify_us.append(out["verify_ms"] * 1e3)
             draft_us.append(out["draft_ms"] * 1e3)
             committed = out["committed"]
