@@ -328,69 +328,96 @@ spin_status spin_switch_ssm(spin_ctx* ctx, int32_t n, const int32_t* slots, cons
 
 
 // Kernel-level entry for the packed ragged causal attention (device pointers).
+// The work list is built on the device by the same meta kernel the engine uses
+// (request decomposition in extend mode: requests uploaded by the host).
 spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int32_t layers, int32_t slots,
                            int32_t ctx, int32_t layer, const void* k_cache, const void* v_cache, const void* q,
                            int32_t n_req, const int32_t* req_slot, const int32_t* req_qlen, const int32_t* req_kvlen,
                            int32_t width, void* out) {
   return guarded([&] {
     if (head_dim != 64 && head_dim != 128) fail(SPIN_INPUT_ERROR, "spin_attention: head_dim must be 64 or 128");
-    if (n_req < 1) fail(SPIN_INPUT_ERROR, "spin_attention: empty batch");
+    if (n_req < 1 || n_req > 1024) fail(SPIN_INPUT_ERROR, "spin_attention: batch must be 1..1024 requests");
     int qmax = 1;
     std::vector<int32_t> qstart(n_req);
     int T = 0;
     for (int i = 0; i < n_req; ++i) {
       if (req_qlen[i] < 1 || req_qlen[i] > 17 || req_kvlen[i] < req_qlen[i] || req_kvlen[i] > ctx)
         fail(SPIN_INPUT_ERROR, "spin_attention: bad request shape");
+      if (req_slot[i] < 0 || req_slot[i] >= slots) fail(SPIN_INPUT_ERROR, "spin_attention: slot out of range");
       qstart[i] = T;
       T += req_qlen[i];
       qmax = std::max(qmax, req_qlen[i]);
     }
-    const PackResult p = pack_lengths(req_kvlen, n_req, width > 0 ? width : n_req);
-    const int nseg = static_cast<int>(p.segments.size());
-    std::vector<int32_t> seg5(5 * nseg), row_ptr(p.rows + 1, 0), row_seg(nseg), s0(n_req, 0), ns(n_req, 0);
-    for (int s = 0; s < nseg; ++s) {
-      const spin_segment& g = p.segments[s];
-      seg5[5 * s] = g.request_id, seg5[5 * s + 1] = g.row, seg5[5 * s + 2] = g.col_start;
-      seg5[5 * s + 3] = g.col_end, seg5[5 * s + 4] = g.token_offset;
-      ++row_ptr[g.row + 1];
-      if (ns[g.request_id]++ == 0) s0[g.request_id] = s;
-    }
-    for (int r = 0; r < p.rows; ++r) row_ptr[r + 1] += row_ptr[r];
-    std::vector<int32_t> cur(row_ptr.begin(), row_ptr.end() - 1);
-    for (int s = 0; s < nseg; ++s) row_seg[cur[p.segments[s].row]++] = s;
-    std::vector<int32_t> ints;
-    std::vector<size_t> off;
-    auto put = [&](const int32_t* v, size_t n) {
-      off.push_back(ints.size());
-      ints.insert(ints.end(), v, v + n);
+    int dev = 0, sms = 148;
+    check_cuda(cudaGetDevice(&dev), "device");
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int rows = width > 0 ? std::min<int>(width, n_req) : n_req;
+    const int chunks = attn_chunks(rows, n_heads, sms);
+    const int seg_cap = n_req + rows;
+    const int piece_cap = seg_cap + rows * chunks;
+    std::vector<void*> allocs;
+    auto dal = [&](size_t bytes) {
+      void* p = nullptr;
+      check_cuda(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "malloc");
+      allocs.push_back(p);
+      return p;
     };
-    put(req_slot, n_req), put(qstart.data(), n_req), put(req_qlen, n_req), put(req_kvlen, n_req);
-    put(seg5.data(), seg5.size()), put(row_ptr.data(), row_ptr.size()), put(row_seg.data(), row_seg.size());
-    put(s0.data(), n_req), put(ns.data(), n_req);
-    int32_t* d_ints = nullptr;
-    float* d_part = nullptr;
-    check_cuda(cudaMalloc(&d_ints, ints.size() * 4), "malloc");
-    const size_t np = static_cast<size_t>(nseg) * n_heads * 32;
-    check_cuda(cudaMalloc(&d_part, np * (2 + head_dim) * 4), "malloc");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    check_cuda(cudaMemcpyAsync(d_ints, ints.data(), ints.size() * 4, cudaMemcpyHostToDevice, s), "h2d");
+    struct Free {
+      std::vector<void*>* a;
+      ~Free() {
+        for (void* p : *a) cudaFree(p);
+      }
+    } freer{&allocs};
     FwdMeta m{};
-    m.req_slot = d_ints + off[0], m.req_qstart = d_ints + off[1], m.req_qlen = d_ints + off[2];
-    m.req_kvlen = d_ints + off[3], m.seg = d_ints + off[4], m.row_ptr = d_ints + off[5], m.row_seg = d_ints + off[6];
-    m.req_seg0 = d_ints + off[7], m.req_nseg = d_ints + off[8];
+    m.req_slot = static_cast<int32_t*>(dal(4 * n_req));
+    m.req_qstart = static_cast<int32_t*>(dal(4 * n_req));
+    m.req_qlen = static_cast<int32_t*>(dal(4 * n_req));
+    m.req_kvlen = static_cast<int32_t*>(dal(4 * n_req));
+    m.seg = static_cast<int32_t*>(dal(20 * seg_cap));
+    m.row_ptr = static_cast<int32_t*>(dal(4 * (rows + 1)));
+    m.row_len = static_cast<int32_t*>(dal(4 * rows));
+    m.row_seg = static_cast<int32_t*>(dal(4 * seg_cap));
+    m.req_seg0 = static_cast<int32_t*>(dal(4 * n_req));
+    m.req_nseg = static_cast<int32_t*>(dal(4 * n_req));
+    m.n_seg = static_cast<int32_t*>(dal(4));
+    m.item_ptr = static_cast<int32_t*>(dal(4 * (rows * chunks + 1)));
+    m.pieces = static_cast<int32_t*>(dal(64 * piece_cap));
+    m.req_pptr = static_cast<int32_t*>(dal(4 * (n_req + 1)));
+    m.req_plist = static_cast<int32_t*>(dal(4 * piece_cap));
+    m.n_pieces = static_cast<int32_t*>(dal(4));
+    m.piece_cap = piece_cap;
+    const int qpad = 8 * ((qmax + 7) / 8);
+    const size_t np = static_cast<size_t>(piece_cap) * n_heads * qpad;
+    AttnWork w{};
+    w.part_m = static_cast<float*>(dal(4 * np));
+    w.part_l = static_cast<float*>(dal(4 * np));
+    w.part_o = static_cast<float*>(dal(4 * np * head_dim));
+    w.counter = static_cast<int32_t*>(dal(4 * static_cast<size_t>(n_req) * n_heads));
+    w.qmax = qmax;
+    w.chunks = chunks;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    check_cuda(cudaMemsetAsync(w.counter, 0, 4 * static_cast<size_t>(n_req) * n_heads, s), "memset");
+    check_cuda(cudaMemcpyAsync(m.req_slot, req_slot, 4 * n_req, cudaMemcpyHostToDevice, s), "h2d");
+    check_cuda(cudaMemcpyAsync(m.req_qstart, qstart.data(), 4 * n_req, cudaMemcpyHostToDevice, s), "h2d");
+    check_cuda(cudaMemcpyAsync(m.req_qlen, req_qlen, 4 * n_req, cudaMemcpyHostToDevice, s), "h2d");
+    check_cuda(cudaMemcpyAsync(m.req_kvlen, req_kvlen, 4 * n_req, cudaMemcpyHostToDevice, s), "h2d");
+    MetaArgs a{};
+    a.mode = kMetaExtend;
+    a.n_req = n_req;
+    a.width = rows;
+    a.chunks = chunks;
+    SlotState st{};
+    launch_meta(a, st, m, s);
     AttnGeom g{n_heads, head_dim, slots, ctx, layer, static_cast<float>(1.0 / std::sqrt(double(head_dim))),
                const_cast<bf16*>(static_cast<const bf16*>(k_cache)), const_cast<bf16*>(static_cast<const bf16*>(v_cache))};
     CUtensorMap tk, tv;
-    const uint64_t rows = static_cast<uint64_t>(layers) * slots * n_heads * ctx;
-    if (!encode_tmap_bf16(&tk, k_cache, rows, head_dim, 16, 64, true) ||
-        !encode_tmap_bf16(&tv, v_cache, rows, head_dim, 16, 64, true))
+    const uint64_t kv_rows = static_cast<uint64_t>(layers) * slots * n_heads * ctx;
+    if (!encode_tmap_bf16(&tk, k_cache, kv_rows, head_dim, 16, 64, true) ||
+        !encode_tmap_bf16(&tv, v_cache, kv_rows, head_dim, 16, 64, true))
       fail(SPIN_CUDA_ERROR, "tensor map encode");
-    AttnWork w{d_part, d_part + np, d_part + 2 * np, qmax};
-    launch_attention(tk, tv, m, p.rows, n_req, g, static_cast<const float*>(q), w, static_cast<bf16*>(out), s);
+    launch_attention(tk, tv, m, rows, n_req, g, static_cast<const float*>(q), w, static_cast<bf16*>(out), s);
     check_cuda(cudaGetLastError(), "attention launch");
     check_cuda(cudaStreamSynchronize(s), "attention");
-    cudaFree(d_ints);
-    cudaFree(d_part);
   });
 }
 

@@ -206,10 +206,23 @@ void Engine::init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool l
     }
   }
   ln.part = dalloc<float>(A, part);
-  const size_t np = static_cast<size_t>(ln.seg_cap) * m.H * 32;  // max(4 warps x 8 q, 1 x 17 q)
+  // attention work list + split-KV partials: pieces <= segments + rows x (chunks - 1), and
+  // rows x chunks x heads ~ 8 x SMs bounds the chunk splits (attn_chunks); partial slots
+  // are 8 queries wide (extends) or up to 24 (verify with a window up to 16, few pieces)
+  ln.piece_cap = ln.seg_cap + 8 * num_sms_ / m.H + 64;
+  ln.meta.piece_cap = ln.piece_cap;
+  ln.meta.item_ptr = dalloc<int32_t>(A, static_cast<size_t>(ln.rows_cap) * 16 + 1);
+  ln.meta.pieces = dalloc<int32_t>(A, static_cast<size_t>(ln.piece_cap) * 16);
+  ln.meta.req_pptr = dalloc<int32_t>(A, R_cap + 1);
+  ln.meta.req_plist = dalloc<int32_t>(A, ln.piece_cap);
+  ln.meta.n_pieces = dalloc<int32_t>(A, 1);
+  ln.meta.row_len = dalloc<int32_t>(A, ln.rows_cap);
+  const size_t np = static_cast<size_t>(ln.piece_cap) * m.H * 8;
   ln.aw.part_m = dalloc<float>(A, np);
   ln.aw.part_l = dalloc<float>(A, np);
   ln.aw.part_o = dalloc<float>(A, np * m.hd);
+  ln.aw.counter = dalloc<int32_t>(A, static_cast<size_t>(R_cap) * m.H);
+  check_cuda(cudaMemset(ln.aw.counter, 0, static_cast<size_t>(R_cap) * m.H * 4), "memset");
   const int tiles = (m.V + 127) / 128;
   ln.amax_val = dalloc<float>(A, static_cast<size_t>(tiles) * T_cap);
   ln.amax_idx = dalloc<int32_t>(A, static_cast<size_t>(tiles) * T_cap);
@@ -251,6 +264,7 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
   ep.part = ln.part;
   AttnWork aw = ln.aw;
   aw.qmax = sh.qmax;
+  aw.chunks = attn_chunks(sh.rows, m.H, num_sms_);
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = m.layers[l];
     g.layer = l;
@@ -411,6 +425,7 @@ void Engine::extend(int model, const std::vector<std::tuple<int, int, int>>& ran
     a.mode = kMetaExtend;
     a.n_req = R;
     a.width = R;
+    a.chunks = attn_chunks(R, m.H, num_sms_);
     launch_meta(a, st_, ln.meta, sv_);
     forward(m, ln, FwdShape{T, R, R, kExtendQ}, sv_, 0);
     check_cuda(cudaStreamSynchronize(sv_), "extend");  // host vectors are reused
@@ -561,6 +576,7 @@ void Engine::capture_round(RoundPlan& p) {
       a.list = list;
       a.ssm = j;
       a.width = nj;
+      a.chunks = attn_chunks(nj, m.H, num_sms_);
       prof_begin(kProfMeta, sj);
       launch_meta(a, st_, ln.meta, sj);
       prof_end(sj, 0);
@@ -574,6 +590,7 @@ void Engine::capture_round(RoundPlan& p) {
         b.step = k;
         b.ssm = j;
         b.width = nj;
+        b.chunks = attn_chunks(nj, m.H, num_sms_);
         b.amax_val = ln.amax_val;
         b.amax_idx = ln.amax_idx;
         b.amax_tiles = tiles;
@@ -600,6 +617,7 @@ void Engine::capture_round(RoundPlan& p) {
     a.list = d_in_ + p.off_list;
     a.width = width;
     a.padded = opts_.packing ? 0 : 1;
+    a.chunks = attn_chunks(a.padded ? n : width, target_.H, num_sms_);
     prof_begin(kProfMeta, s);
     launch_meta(a, st_, tlane_.meta, s);
     prof_end(s, 0);
@@ -802,6 +820,8 @@ void Engine::kernel_bench(int kind, int iters, double* us_per_launch, double* by
              m.kc, m.vc};
   AttnWork aw = ln.aw;
   aw.qmax = opts_.window + 1;
+  const int bench_rows = opts_.packing ? (opts_.pack_width > 0 ? std::min(opts_.pack_width, n) : n) : n;
+  aw.chunks = attn_chunks(bench_rows, m.H, num_sms_);
   double kv_tokens = 0.0;
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = m.layers[l];
@@ -816,7 +836,7 @@ void Engine::kernel_bench(int kind, int iters, double* us_per_launch, double* by
       }
     } else {
       g.layer = l;
-      launch_attention(m.tm_k, m.tm_v, ln.meta, opts_.pack_width > 0 ? std::min(opts_.pack_width, n) : n, n, g, ln.q,
+      launch_attention(m.tm_k, m.tm_v, ln.meta, bench_rows, n, g, ln.q,
                        aw, ln.attn, sv_);
       ++launches;
     }

@@ -32,7 +32,7 @@ struct ModelDev {
 
 // Forward workspace of one model (one stream at a time).
 struct Lane {
-  int T_cap = 0, R_cap = 0, seg_cap = 0, rows_cap = 0;
+  int T_cap = 0, R_cap = 0, seg_cap = 0, rows_cap = 0, piece_cap = 0;
   FwdMeta meta{};
   float* h = nullptr;
   bf16 *xn = nullptr, *attn = nullptr, *act = nullptr;

@@ -66,13 +66,26 @@ __device__ int row_argmax_warp(const float* val, const int32_t* idx, int tiles, 
 }
 
 // ------------------------------------------------------------------ meta
-constexpr int kMetaThreads = 256;
+constexpr int kMetaThreads = 512;
 constexpr int kMaxReq = 1024;
+constexpr int kMaxSeg = 2 * kMaxReq;
+constexpr size_t kMetaSmem = (11 * kMaxReq + 12 + 6 * kMaxSeg) * sizeof(int);
 
 __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotState st, FwdMeta m) {
-  __shared__ int s_len[kMaxReq];
-  __shared__ int s_order[kMaxReq];
-  __shared__ int s_used[kMaxReq];
+  extern __shared__ int msm[];
+  int* s_len = msm;                   // [n] kv length per request
+  int* s_order = s_len + kMaxReq;     // [n] requests by decreasing length
+  int* s_used = s_order + kMaxReq;    // [rows] fill, later row counts
+  int* s_ptr = s_used + kMaxReq;      // [rows + 1] CSR
+  int* s_misc = s_ptr + kMaxReq + 4;  // [0] nseg
+  int* s_rlen = s_misc + kMaxReq;     // [rows] attention pieces per row
+  int* s_rs0 = s_rlen + kMaxReq;      // [n] first segment of each request
+  int* s_rns = s_rs0 + kMaxReq;       // [n] its segment count
+  int* s_np = s_rns + kMaxReq;        // [n] attention pieces per request
+  int* s_rbase = s_np + kMaxReq;      // [rows + 1] first piece of each row
+  int* s_rptr = s_rbase + kMaxReq + 4;  // [n + 1] first merge-list entry of each request
+  int* s_pofs = s_rptr + kMaxReq + 4;   // [nseg] first piece of each segment within its request
+  int* s_seg = s_pofs + kMaxSeg;        // [nseg][5]
   const int n = a.n_req;
   const int tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
@@ -158,7 +171,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
       for (int i = lane; i < n; i += 32) longest = max(longest, s_len[i]);
       for (int o = 16; o > 0; o >>= 1) longest = max(longest, __shfl_xor_sync(kFull, longest, o));
       for (int i = lane; i < n; i += 32) {
-        int32_t* sg = m.seg + 5 * i;
+        int* sg = s_seg + 5 * i;
         sg[0] = i, sg[1] = i, sg[2] = 0, sg[3] = longest, sg[4] = 0;
       }
       nseg = n;
@@ -181,7 +194,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
         }
         if (home >= 0) {
           if (lane == 0) {
-            int32_t* sg = m.seg + 5 * nseg;
+            int* sg = s_seg + 5 * nseg;
             sg[0] = id, sg[1] = home, sg[2] = s_used[home], sg[3] = s_used[home] + need, sg[4] = 0;
             s_used[home] += need;
           }
@@ -203,7 +216,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
           const int take = min(room, max(0, remaining - excl));
           const unsigned mask = __ballot_sync(kFull, take > 0);
           if (take > 0) {
-            int32_t* sg = m.seg + 5 * (nseg + __popc(mask & ((1u << lane) - 1u)));
+            int* sg = s_seg + 5 * (nseg + __popc(mask & ((1u << lane) - 1u)));
             sg[0] = id, sg[1] = r, sg[2] = s_used[r], sg[3] = s_used[r] + take, sg[4] = done + excl;
             s_used[r] += take;
           }
@@ -216,28 +229,108 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
         }
       }
     }
-    if (lane == 0) *m.n_seg = nseg;
+    if (lane == 0) s_misc[0] = nseg;
   }
   __syncthreads();
-  // ---- group segments by pack row (column order) and by request
-  if (tid == 0) {
-    const int nseg = *m.n_seg;
-    for (int r = 0; r < rows; ++r) s_used[r] = 0;
-    for (int r = 0; r < n; ++r) m.req_nseg[r] = 0;
+  const int nseg = s_misc[0];
+  const int nch = max(1, a.chunks);
+  // ---- segments out; per-request segment ranges (a request's segments are consecutive)
+  if (tid == 0) s_misc[1] = 0;
+  __syncthreads();
+  for (int s = tid; s < nseg; s += kMetaThreads) {
+#pragma unroll
+    for (int e = 0; e < 5; ++e) m.seg[5 * s + e] = s_seg[5 * s + e];
+    const int rq = s_seg[5 * s];
+    if (s == 0 || s_seg[5 * (s - 1)] != rq) {
+      int e = s + 1;
+      while (e < nseg && s_seg[5 * e] == rq) ++e;
+      m.req_seg0[rq] = s;
+      m.req_nseg[rq] = e - s;
+      s_rs0[rq] = s;
+      s_rns[rq] = e - s;
+    }
+    atomicMax(&s_misc[1], s_seg[5 * s + 3]);
+  }
+  __syncthreads();
+  // Attention work items: every pack row is cut into nch chunks of C columns;
+  // a piece = one segment's part inside one chunk (the split-KV unit).
+  const int C = max(16, ((s_misc[1] + nch - 1) / nch + 15) / 16 * 16);
+  auto touched = [&](const int* sg) { return (sg[3] - 1) / C - sg[2] / C + 1; };
+  // ---- per pack row: segment count, used length, pieces
+  for (int r = tid; r < rows; r += kMetaThreads) {
+    int c = 0, len = 0, pcs = 0;
     for (int s = 0; s < nseg; ++s) {
-      ++s_used[m.seg[5 * s + 1]];
-      const int rq = m.seg[5 * s];
-      if (m.req_nseg[rq] == 0) m.req_seg0[rq] = s;
-      ++m.req_nseg[rq];
+      const int* sg = s_seg + 5 * s;
+      if (sg[1] != r) continue;
+      ++c;
+      len = max(len, sg[3]);
+      pcs += touched(sg);
     }
-    int acc = 0;
-    for (int r = 0; r < rows; ++r) {
-      m.row_ptr[r] = acc;
-      acc += s_used[r];
-      s_used[r] = m.row_ptr[r];
+    s_used[r] = c;
+    s_rlen[r] = pcs;
+    m.row_len[r] = len;
+  }
+  // ---- per request: pieces and each segment's first piece index (token order)
+  for (int rq = tid; rq < n; rq += kMetaThreads) {
+    int run = 0;
+    for (int s = s_rs0[rq]; s < s_rs0[rq] + s_rns[rq]; ++s) {
+      s_pofs[s] = run;
+      run += touched(s_seg + 5 * s);
     }
-    m.row_ptr[rows] = acc;
-    for (int s = 0; s < nseg; ++s) m.row_seg[s_used[m.seg[5 * s + 1]]++] = s;
+    s_np[rq] = run;
+  }
+  __syncthreads();
+  // ---- exclusive scans: warp 0 row segments, warp 1 row pieces, warp 2 request pieces
+  if (warp < 3) {
+    const int* src = warp == 0 ? s_used : warp == 1 ? s_rlen : s_np;
+    int* dst = warp == 0 ? s_ptr : warp == 1 ? s_rbase : s_rptr;
+    const int cnt = warp == 2 ? n : rows;
+    int carry = 0;
+    for (int base = 0; base < cnt; base += 32) {
+      const int r = base + lane;
+      const int v = r < cnt ? src[r] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (r < cnt) dst[r] = carry + incl - v;
+      carry += __shfl_sync(kFull, incl, 31);
+    }
+    if (lane == 0) dst[cnt] = carry;
+  }
+  __syncthreads();
+  if (s_rbase[rows] > m.piece_cap) __trap();  // piece buffers sized by the engine
+  for (int r = tid; r <= rows; r += kMetaThreads) m.row_ptr[r] = s_ptr[r];
+  for (int r = tid; r <= n; r += kMetaThreads) m.req_pptr[r] = s_rptr[r];
+  if (tid == 0) {
+    m.item_ptr[rows * nch] = s_rbase[rows];
+    m.n_pieces[0] = s_rbase[rows];
+  }
+  // ---- placement (thread per row): pieces in (chunk, column) order + per-request merge lists
+  for (int r = tid; r < rows; r += kMetaThreads) {
+    int pos = s_ptr[r];
+    for (int s = 0; s < nseg; ++s)
+      if (s_seg[5 * s + 1] == r) m.row_seg[pos++] = s;
+    int pc = s_rbase[r];
+    for (int c = 0; c < nch; ++c) {
+      m.item_ptr[r * nch + c] = pc;
+      const int x0 = c * C, x1 = (c + 1) * C;
+      for (int k = s_ptr[r]; k < s_ptr[r + 1]; ++k) {
+        const int s = m.row_seg[k];
+        const int* sg = s_seg + 5 * s;
+        const int a0 = max(sg[2], x0), a1 = min(sg[3], x1);
+        if (a0 >= a1) continue;
+        const int rq = sg[0];
+        int4* rec = reinterpret_cast<int4*>(m.pieces + 16 * pc);
+        rec[0] = make_int4(rq, m.req_slot[rq], sg[4] + (a0 - sg[2]), a1 - a0);
+        rec[1] = make_int4(m.req_qstart[rq], m.req_qlen[rq], m.req_kvlen[rq], s_np[rq]);
+        rec[2] = make_int4(s_rptr[rq], 0, 0, 0);
+        m.req_plist[s_rptr[rq] + s_pofs[s] + (c - sg[2] / C)] = pc;
+        ++pc;
+      }
+    }
   }
   ptx::grid_dep_launch();
 }
@@ -545,7 +638,12 @@ void launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Ar
 }  // namespace
 
 void launch_meta(const MetaArgs& a, const SlotState& st, const FwdMeta& m, cudaStream_t s) {
-  launch_pdl(meta_kernel, dim3(1), dim3(kMetaThreads), 0, s, a, st, m);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(meta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMetaSmem));
+    configured = true;
+  }
+  launch_pdl(meta_kernel, dim3(1), dim3(kMetaThreads), kMetaSmem, s, a, st, m);
 }
 
 void launch_embed_norm(const bf16* emb, const FwdMeta& m, int T, int D, float eps, float* h, bf16* xn,

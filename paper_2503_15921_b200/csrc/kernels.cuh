@@ -28,6 +28,14 @@ struct FwdMeta {
   int32_t* req_kvlen;  // keys visible to the last query = last position + 1
   int32_t* seg;        // [S][5] request, row, col_start, col_end, token_offset (pack order)
   int32_t* row_ptr;    // [W+1] CSR over pack rows into row_seg
+  int32_t* row_len;    // [W] used columns of each pack row
+  // attention work (meta_kernel): pack row r, chunk c -> pieces [item_ptr[r*nch+c], item_ptr[r*nch+c+1])
+  int32_t* item_ptr;   // [rows * nch + 1]
+  int32_t* pieces;     // [P][16] {request, slot, token0, len | qstart, qlen, kvlen, pieces of request | merge-list start}
+  int32_t* req_pptr;   // [R + 1] CSR: each request's pieces in (segment, chunk) = token order
+  int32_t* req_plist;  // [P]
+  int32_t* n_pieces;   // [1]
+  int32_t piece_cap;   // capacity of pieces (and of the split-KV partial slots)
   int32_t* row_seg;    // [S] segment ids grouped by pack row, column order
   int32_t* req_seg0;   // [R] first segment (segments of a request are contiguous)
   int32_t* req_nseg;   // [R]
@@ -65,6 +73,7 @@ struct MetaArgs {
   int amax_tiles;
   int prev_t;     // rows of the previous forward
   int prev_qlen;  // rows per request in the previous forward
+  int chunks;     // attention chunks per pack row (attn_chunks)
 };
 
 struct LayerW {
@@ -90,11 +99,15 @@ void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* ac
 // Packed ragged causal attention over the KV cache (TMA-staged tiles) and the
 // shared-max combine of segment partials.
 struct AttnWork {
-  float* part_m;  // [seg_cap][H][qmax]
+  float* part_m;  // [pieces][H][qpad]  split-KV partials (qpad = 8 * ceil(qmax / 8))
   float* part_l;
-  float* part_o;  // [seg_cap][H][qmax][hd]
+  float* part_o;  // [pieces][H][qpad][hd]
+  int32_t* counter;  // [R_cap][H] arrivals per (request, head); zero between launches
   int qmax;
+  int chunks;     // chunks per pack row (must equal the MetaArgs.chunks that built the work list)
 };
+// Chunks per pack row so that rows x chunks x heads warps fill the GPU.
+int attn_chunks(int rows, int heads, int num_sms);
 void launch_attention(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m, int n_rows, int n_req,
                       const AttnGeom& g, const float* q, const AttnWork& w, bf16* out, cudaStream_t s);
 
