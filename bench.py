@@ -166,6 +166,58 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_c3(args):
+    """BASELINE config 3: request-decomposition sweep -- ragged draft lengths U{1..16}, batch 64,
+    packed (pack() of the true lengths) vs padded (longest window, longest KV) verification
+    of the 7B-shaped target on one B200; verify-step device us for each, plus the
+    reference's verify_batch_cost token accounting (slot_engine.cpp:24-45) for the same batch."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2503_15921_b200 import _lib
+    from paper_2503_15921_b200.models import LLAMA_7B, LLAMA_68M, Engine, synthetic_prompts
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    B, W = 64, 16
+    rng = np.random.default_rng(SEED + 3)
+    prompts = synthetic_prompts(B, PROMPT_LO, PROMPT_HI, LLAMA_7B.vocab, SEED + 3)
+    lens = rng.integers(1, W + 1, B).astype(np.int32)
+    drafts = rng.integers(0, LLAMA_7B.vocab, int(lens.sum())).astype(np.int32)
+    max_ctx = ((PROMPT_HI + W + 8 + 63) // 64) * 64
+    out = {"metric": "verify-step us, packed vs padded (c3: ragged draft lengths 1-16, batch 64)", "unit": "us",
+           "higher_is_better": False, "config": {"workload": "c3", "batch": B, "draft_len": "U{1..16}", "seed": SEED + 3,
+                                                 "target": LLAMA_7B.name}}
+    lib = _lib.load()
+    kv_lens = np.array([len(p) + int(l) for p, l in zip(prompts, lens)], np.int32)  # kv_len = committed + window
+    for width in (B, B // 2, B // 4):
+        eng = Engine(LLAMA_7B, (LLAMA_68M,), max_requests=B, max_ctx=max_ctx, window=W, pack_width=width)
+        eng.prefill(range(B), prompts)
+        slots = np.arange(B, dtype=np.int32)
+        res = {}
+        for mode, packed in (("packed", True), ("padded", False)):
+            eng.verify_bench(slots, lens, drafts, packed=packed, iters=args.warmup)
+            r = eng.verify_bench(slots, lens, drafts, packed=packed, iters=args.steps)
+            res[mode] = {k: (float(v) if k == "us" else int(v)) for k, v in r.items() if k != "target"}
+            res[mode]["target"] = r["target"]
+        agree = float((res["packed"].pop("target") == res["padded"].pop("target")).mean())
+        # reference token accounting for the same batch (verify_batch_cost, packed and padded)
+        cost = {}
+        for mode, packing in (("packed", 1), ("padded", 0)):
+            tok, pad = C.c_int64(), C.c_int64()
+            _lib.check(lib.spin_verify_batch_cost(kv_lens.ctypes.data_as(_lib.P_I32), B, W, packing, width,
+                                                  C.byref(tok), C.byref(pad)))
+            cost[mode] = {"tokens": tok.value, "padding": pad.value}
+        out.setdefault("sweep", []).append({"pack_width": width, "packed": res["packed"], "padded": res["padded"],
+                                            "speedup_padded_over_packed": res["padded"]["us"] / res["packed"]["us"],
+                                            "target_token_agreement": agree, "reference_verify_batch_cost": cost})
+        eng.close()
+    best = min(out["sweep"], key=lambda s: s["packed"]["us"])
+    out["value"] = best["packed"]["us"]
+    out["padded_us"] = best["padded"]["us"]
+    print(json.dumps(out), flush=True)
+
+
 def workload_config(eng_info):
     from paper_2503_15921_b200.models import LLAMA_7B, LLAMA_68M, LLAMA_160M
 
@@ -186,8 +238,12 @@ def main():
     ap.add_argument("--impl", default="spin", choices=["spin", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pack-width", type=int, default=0)
+    ap.add_argument("--config", default="c2", choices=["c2", "c3"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.config == "c3" and args.impl != "reference":
+        run_c3(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return

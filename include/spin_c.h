@@ -184,6 +184,22 @@ spin_status spin_round_launches(spin_ctx* ctx, int32_t n, const int32_t* slots, 
 spin_status spin_kernel_bench(spin_ctx* ctx, int32_t kind, int32_t iters, double* us_per_launch,
                               double* bytes_per_launch);
 
+/* Ragged-window verification (BASELINE config 3, request-decomposition sweep):
+ * request i verifies draft_lens[i] in 1..window drafts (drafts: host tokens, flat,
+ * sum(draft_lens) entries, or NULL for the history token). packed = 1: pack() of
+ * the true lengths (sum(len+1) query rows); 0: padded to the longest window and
+ * the longest KV (the reference's naive_padding baseline, slot_engine.cpp:37-44).
+ * Nothing is committed; `iters` graph replays are timed with CUDA events. */
+typedef struct spin_verify_stats {
+  double us;               /* device microseconds per verification step */
+  int64_t query_rows;      /* rows through the target forward (incl. padding) */
+  int64_t real_rows;       /* sum(draft_lens + 1) */
+  int64_t kv_tokens;       /* KV tokens the attention reads (incl. padding) */
+  int32_t* target_tokens;  /* optional host [sum(draft_lens + 1)]: target argmax of each real row */
+} spin_verify_stats;
+spin_status spin_verify_bench(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* draft_lens,
+                              const int32_t* drafts, int32_t packed, int32_t iters, spin_verify_stats* out);
+
 /* ------------------------------------------------------------------------
  * Kernel-level entry points (device pointers; stream = cudaStream_t or NULL).
  * Used by the parity tests to check each kernel against a reference of the

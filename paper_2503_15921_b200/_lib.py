@@ -77,6 +77,11 @@ class EngineOpts(C.Structure):
     ]
 
 
+class VerifyStats(C.Structure):
+    _fields_ = [("us", C.c_double), ("query_rows", C.c_int64), ("real_rows", C.c_int64), ("kv_tokens", C.c_int64),
+                ("target_tokens", C.POINTER(C.c_int32))]
+
+
 class RoundOut(C.Structure):
     _fields_ = [
         ("accepted", C.POINTER(C.c_int32)),
@@ -119,6 +124,7 @@ _SIGNATURES = {
     "spin_kernel_bench": [C.c_void_p, C.c_int32, C.c_int32, P_F64, P_F64],
     "spin_attention": [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                        C.c_void_p, C.c_void_p, C.c_int32, P_I32, P_I32, P_I32, C.c_int32, C.c_void_p],
+    "spin_verify_bench": [C.c_void_p, C.c_int32, P_I32, P_I32, P_I32, C.c_int32, C.c_int32, C.c_void_p],
     "spin_gemm_info": [C.c_int32, C.c_int32, C.c_int32, C.c_int32, P_I32, P_I32, P_I32],
     "spin_gemm": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                   C.c_void_p, C.c_void_p, C.c_void_p],

@@ -319,6 +319,15 @@ spin_status spin_kernel_bench(spin_ctx* ctx, int32_t kind, int32_t iters, double
   });
 }
 
+spin_status spin_verify_bench(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* draft_lens,
+                              const int32_t* drafts, int32_t packed, int32_t iters, spin_verify_stats* out) {
+  return guarded([&] {
+    if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
+    if (!slots || !draft_lens) fail(SPIN_INPUT_ERROR, "verify_bench: null arrays");
+    ctx->eng->verify_bench(n, slots, draft_lens, drafts, packed, iters, out);
+  });
+}
+
 spin_status spin_switch_ssm(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of) {
   return guarded([&] {
     if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");

@@ -869,6 +869,127 @@ void Engine::kernel_bench(int kind, int iters, double* us_per_launch, double* by
   *bytes_per_launch = bytes / launches;
 }
 
+// Ragged-window verification step (BASELINE config 3): request i verifies
+// draft_lens[i] drafts (its pending token + drafts at positions c-1 .. c-1+len).
+// packed: request decomposition of the true lengths (pack(), Sigma(len+1) query rows);
+// padded: every request padded to the longest window (n x (max+1) query rows, KV
+// padded to the longest request -- the reference's naive_padding baseline).
+// The KV rows are (re)written idempotently and nothing is committed, so the step
+// can be replayed; timing = `iters` replays of one CUDA graph (CUDA events).
+void Engine::verify_bench(int n, const int32_t* slots, const int32_t* draft_lens, const int32_t* drafts, int packed,
+                          int iters, spin_verify_stats* out) {
+  sync_state_from_device();
+  const int W = opts_.window, R = opts_.max_requests;
+  if (n < 1 || n > R) fail(SPIN_CAPACITY_ERROR, "verify_bench: batch exceeds max_requests");
+  if (iters < 1) fail(SPIN_INPUT_ERROR, "verify_bench: iters must be >= 1");
+  int gmax = 0;
+  std::vector<char> seen(R, 0);
+  for (int i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= R || seen[slots[i]]) fail(SPIN_INPUT_ERROR, "verify_bench: bad slot list");
+    seen[slots[i]] = 1;
+    if (draft_lens[i] < 1 || draft_lens[i] > W) fail(SPIN_INPUT_ERROR, "verify_bench: draft length outside 1..window");
+    if (h_committed_[slots[i]] < 2) fail(SPIN_INPUT_ERROR, "verify_bench: slot was not prefilled");
+    if (h_committed_[slots[i]] + W + 1 > opts_.max_ctx) fail(SPIN_CAPACITY_ERROR, "verify_bench: context is full");
+    gmax = std::max(gmax, draft_lens[i]);
+  }
+  // rows and requests (host-built; the meta kernel only packs)
+  std::vector<int32_t> rt, rs, rp, qs, ql, kv, sl;
+  size_t doff = 0;
+  for (int i = 0; i < n; ++i) {
+    const int s = slots[i], c = h_committed_[s], len = draft_lens[i];
+    const int q = packed ? len + 1 : gmax + 1;
+    qs.push_back(static_cast<int32_t>(rt.size()));
+    ql.push_back(q);
+    kv.push_back(c - 1 + q);  // last query position + 1
+    sl.push_back(s);
+    for (int j = 0; j < q; ++j) {
+      const bool real = j <= len;
+      int32_t tok = h_tokens_[static_cast<size_t>(s) * opts_.max_ctx + c - 1];
+      if (j > 0) tok = real && drafts ? drafts[doff + j - 1] : tok;
+      rt.push_back(tok);
+      rs.push_back(real ? s : -1);  // padding rows write no KV
+      rp.push_back(c - 1 + j);
+    }
+    doff += len;
+  }
+  const int T = static_cast<int>(rt.size());
+  Lane& ln = tlane_;
+  if (T > ln.T_cap) fail(SPIN_CAPACITY_ERROR, "verify_bench: too many query rows for this engine (raise window)");
+  check_cuda(cudaMemcpy(ln.meta.row_tok, rt.data(), T * 4, cudaMemcpyHostToDevice), "h2d");
+  check_cuda(cudaMemcpy(ln.meta.row_slot, rs.data(), T * 4, cudaMemcpyHostToDevice), "h2d");
+  check_cuda(cudaMemcpy(ln.meta.row_pos, rp.data(), T * 4, cudaMemcpyHostToDevice), "h2d");
+  check_cuda(cudaMemcpy(ln.meta.req_slot, sl.data(), n * 4, cudaMemcpyHostToDevice), "h2d");
+  check_cuda(cudaMemcpy(ln.meta.req_qstart, qs.data(), n * 4, cudaMemcpyHostToDevice), "h2d");
+  check_cuda(cudaMemcpy(ln.meta.req_qlen, ql.data(), n * 4, cudaMemcpyHostToDevice), "h2d");
+  check_cuda(cudaMemcpy(ln.meta.req_kvlen, kv.data(), n * 4, cudaMemcpyHostToDevice), "h2d");
+  const int width = opts_.pack_width > 0 ? std::min(opts_.pack_width, n) : n;
+  MetaArgs a{};
+  a.mode = kMetaExtend;
+  a.n_req = n;
+  a.width = width;
+  a.padded = packed ? 0 : 1;
+  a.chunks = attn_chunks(packed ? width : n, target_.H, num_sms_);
+  const int qmax = packed ? gmax + 1 : gmax + 1;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  check_cuda(cudaStreamBeginCapture(sv_, cudaStreamCaptureModeRelaxed), "capture");
+  capturing_ = true;
+  launch_meta(a, st_, ln.meta, sv_);
+  forward(target_, ln, FwdShape{T, n, packed ? width : n, qmax}, sv_, opts_.debug_logits ? 2 : 1);
+  capturing_ = false;
+  check_cuda(cudaStreamEndCapture(sv_, &graph), "capture");
+  check_cuda(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  check_cuda(cudaGraphLaunch(exec, sv_), "warm");
+  check_cuda(cudaEventRecord(e0, sv_), "event");
+  for (int i = 0; i < iters; ++i) check_cuda(cudaGraphLaunch(exec, sv_), "graph");
+  check_cuda(cudaEventRecord(e1, sv_), "event");
+  check_cuda(cudaStreamSynchronize(sv_), "verify_bench");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0), cudaEventDestroy(e1);
+  cudaGraphExecDestroy(exec), cudaGraphDestroy(graph);
+  // target argmax per real query row (lowest index on ties over the 128-row lm_head tiles)
+  const int tiles = (target_.V + 127) / 128;
+  std::vector<float> av(static_cast<size_t>(tiles) * T);
+  std::vector<int32_t> ai(static_cast<size_t>(tiles) * T);
+  check_cuda(cudaMemcpy(av.data(), ln.amax_val, av.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+  check_cuda(cudaMemcpy(ai.data(), ln.amax_idx, ai.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+  int64_t kv_read = 0, real_rows = 0;
+  size_t o = 0;
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j <= draft_lens[i]; ++j) {
+      const int row = qs[i] + j;
+      float bv = -INFINITY;
+      int bi = 0x7fffffff;
+      for (int tl = 0; tl < tiles; ++tl) {
+        const float v = av[static_cast<size_t>(tl) * T + row];
+        const int id = ai[static_cast<size_t>(tl) * T + row];
+        if (v > bv || (v == bv && id < bi)) bv = v, bi = id;
+      }
+      if (out && out->target_tokens) out->target_tokens[o] = bi;
+      ++o;
+    }
+    real_rows += draft_lens[i] + 1;
+  }
+  if (packed) {
+    for (int i = 0; i < n; ++i) kv_read += kv[i];
+  } else {
+    int longest = 0;
+    for (int i = 0; i < n; ++i) longest = std::max(longest, kv[i]);
+    kv_read = static_cast<int64_t>(longest) * n;
+  }
+  last_verify_rows_ = 0;  // the kernel_bench replays expect a round's layout
+  if (out) {
+    out->us = ms * 1e3 / iters;
+    out->query_rows = T;
+    out->real_rows = real_rows;
+    out->kv_tokens = kv_read;
+  }
+}
+
 int64_t Engine::launches_per_round(int n, const int32_t* slots, const int32_t* ssm_of) {
   return plan_round(n, slots, ssm_of).launches;
 }

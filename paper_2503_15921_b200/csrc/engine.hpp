@@ -80,6 +80,8 @@ class Engine {
                      int64_t* launches);
   int64_t launches_per_round(int n, const int32_t* slots, const int32_t* ssm_of);
   void kernel_bench(int kind, int iters, double* us_per_launch, double* bytes_per_launch);
+  void verify_bench(int n, const int32_t* slots, const int32_t* draft_lens, const int32_t* drafts, int packed,
+                    int iters, spin_verify_stats* out);
 
  private:
   struct RoundPlan;

@@ -173,6 +173,22 @@ class Engine:
                                               C.byref(by)))
         return us.value, by.value
 
+    def verify_bench(self, slots, draft_lens, drafts=None, packed: bool = True, iters: int = 5):
+        """Ragged-window verification step (config 3): device us per step, rows, KV tokens read,
+        and the target argmax of every real query row (concatenated per request)."""
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        lens = np.ascontiguousarray(draft_lens, dtype=np.int32)
+        tgt = np.zeros(int(lens.sum()) + len(lens), np.int32)
+        st = _lib.VerifyStats()
+        st.target_tokens = tgt.ctypes.data_as(_lib.P_I32)
+        dr = None
+        if drafts is not None:
+            dr = np.ascontiguousarray(drafts, dtype=np.int32)
+        _lib.check(self.lib.spin_verify_bench(self.ctx, len(slots), _p(slots), _p(lens),
+                                              _p(dr) if dr is not None else None, int(packed), iters, C.byref(st)))
+        return {"us": st.us, "query_rows": st.query_rows, "real_rows": st.real_rows, "kv_tokens": st.kv_tokens,
+                "target": tgt}
+
     def switch(self, slots, ssm_of):
         slots = np.ascontiguousarray(slots, dtype=np.int32)
         ssm_of = np.ascontiguousarray(ssm_of, dtype=np.int32)
