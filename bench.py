@@ -218,6 +218,69 @@ def run_c3(args):
     print(json.dumps(out), flush=True)
 
 
+def run_c4(args):
+    """BASELINE config 4: LLaMA-13B-shaped target, 3 heterogeneous SSMs (68M, 160M, 160M-b) with
+    LBSS selection on measured goodput (selector.Lbss restating bandit.cpp), the SSM drafts of a
+    slot running concurrently on their own CUDA streams. Reports accepted tokens/s of the LBSS run
+    and of every homogeneous assignment (all requests on one SSM) on the same prompts."""
+    import torch
+
+    from paper_2503_15921_b200.models import LLAMA_13B, LLAMA_68M, LLAMA_160M, LLAMA_160M_B, Engine, synthetic_prompts
+    from paper_2503_15921_b200.selector import Lbss
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    ssms = (LLAMA_68M, LLAMA_160M, LLAMA_160M_B)
+    slots_n = max(args.steps, 24)
+    rounds_cap = slots_n + 3 * 6 + 8
+    max_ctx = ((PROMPT_HI + (WINDOW + 1) * rounds_cap + 8 + 63) // 64) * 64
+    prompts = synthetic_prompts(BATCH, PROMPT_LO, PROMPT_HI, LLAMA_13B.vocab, SEED + 4)
+    slots = np.arange(BATCH, dtype=np.int32)
+    out = {"metric": "accepted tokens/sec (c4: 13B target, 3 SSMs, LBSS)", "unit": "tokens/s",
+           "higher_is_better": True, "config": {"workload": "c4", "target": LLAMA_13B.name,
+                                                "ssms": [s.name for s in ssms], "batch": BATCH, "window": WINDOW,
+                                                "slots": slots_n, "alpha": 8, "beta": 2}}
+    eng = Engine(LLAMA_13B, ssms, max_requests=BATCH, max_ctx=max_ctx, window=WINDOW)
+    eng.prefill(range(BATCH), prompts)
+    # homogeneous baselines (vanilla: every request on SSM j), 6 slots each after 2 warm-up slots
+    homo = {}
+    for j, s in enumerate(ssms):
+        assign = np.full(BATCH, j, np.int32)
+        for _ in range(2):
+            eng.round(slots, assign)
+        toks, ms = 0, 0.0
+        for _ in range(6):
+            r = eng.round(slots, assign)
+            toks += int(r["accepted"].sum()) + BATCH
+            ms += r["round_ms"]
+        homo[s.name] = {"tokens_per_s": toks / (ms / 1e3), "mean_accepted": toks / (6 * BATCH) - 1}
+    # LBSS on measured goodput
+    sel = Lbss(BATCH, [BATCH] * len(ssms), alpha=8, beta=2, seed=SEED)
+    toks, ms, wall0 = 0, 0.0, time.perf_counter()
+    explore_slots = 0
+    for _ in range(slots_n):
+        assign, explore = sel.next_slot()
+        assign = assign.astype(np.int32)
+        r = eng.round(slots, assign)
+        sec = r["round_ms"] / 1e3
+        for i in range(BATCH):
+            if assign[i] >= 0:
+                sel.add(i, int(assign[i]), (int(r["accepted"][i]) + 1) / sec)
+        toks += int(r["accepted"].sum()) + int((assign >= 0).sum())
+        ms += r["round_ms"]
+        explore_slots += int(explore)
+    wall = time.perf_counter() - wall0
+    final = sel.exploitation()
+    eng.close()
+    out["value"] = toks / (ms / 1e3)
+    out["lbss"] = {"tokens_per_s_device": toks / (ms / 1e3), "tokens_per_s_wall": toks / wall,
+                   "explore_slots": explore_slots, "epochs": sel.epoch,
+                   "final_assignment_histogram": np.bincount(final, minlength=len(ssms)).tolist()}
+    out["homogeneous"] = homo
+    out["note"] = ("wall time includes host-side SSM switches (KV recompute on the destination SSM, "
+                   "switching_cost slot_engine.cpp:12-22) and the selector")
+    print(json.dumps(out), flush=True)
+
+
 def workload_config(eng_info):
     from paper_2503_15921_b200.models import LLAMA_7B, LLAMA_68M, LLAMA_160M
 
@@ -225,6 +288,9 @@ def workload_config(eng_info):
            "batch_per_gpu": BATCH, "window": WINDOW, "prompt_len": f"U[{PROMPT_LO},{PROMPT_HI}]",
            "target": LLAMA_7B.name, "ssms": [LLAMA_68M.name, LLAMA_160M.name], "assignment": "request i -> ssm i%2",
            "l2": "no flush needed: 13.5 GB of target weights stream through the 126 MB L2 every step"}
+    if BATCH != 32:
+        cfg["workload"] = (f"c5: batch 256 sharded, {BATCH} requests per GPU; LLaMA-7B-shaped target verifying "
+                           "LLaMA-68M/160M-shaped SSM drafts, greedy")
     if eng_info:
         cfg.update(eng_info)
     return cfg
@@ -238,12 +304,19 @@ def main():
     ap.add_argument("--impl", default="spin", choices=["spin", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pack-width", type=int, default=0)
-    ap.add_argument("--config", default="c2", choices=["c2", "c3"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.config == "c3" and args.impl != "reference":
         run_c3(args)
         return
+    if args.config == "c4" and args.impl != "reference":
+        run_c4(args)
+        return
+    global BATCH
+    if args.config == "c5":  # batch 256 requests sharded over the ranks (strong scaling)
+        BATCH = 256 // int(os.environ.get("WORLD_SIZE", "1"))
+        args.no_cpu_baseline = True
     if args.impl == "reference":
         run_reference(args)
         return
@@ -358,7 +431,8 @@ def main():
             "mean_accepted_per_request": mean_acc, "per_class_ms_one_round": {k: v[0] for k, v in prof.items()},
             "per_class_launches": {k: v[2] for k, v in prof.items()}}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round_ms, "higher_is_better": True,
+            "scaling": "strong" if args.config == "c5" else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded random-init weights, planted bigram)",
             "config": workload_config(info),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
