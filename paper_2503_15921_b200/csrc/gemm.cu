@@ -338,10 +338,11 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
   m.bn = p.bn;
   m.units = n_tiles * p.kb;
   if (mode == kGemmPartial) {
-    // At least kMinUnits k-blocks (128 KiB of weights) per CTA: small draft
+    // At least kMinUnits k-blocks (64 KiB of weights) per CTA: small draft
     // GEMMs then use fewer SMs instead of fragmenting every tile into many
-    // partial pieces that the consumer must re-read.
-    constexpr long long kMinUnits = 8;
+    // partial pieces that the consumer must re-read (4 measured best of 1/2/4/8
+    // on the config-2 draft loop).
+    constexpr long long kMinUnits = 4;
     m.grid = static_cast<int>(std::min<long long>(num_sms, std::max<long long>(1, (m.units + kMinUnits - 1) / kMinUnits)));
     // Worst-case pieces per tile: a tile spans ceil(kb / per_cta) + 1 CTAs.
     int mp = 1;
