@@ -227,6 +227,7 @@ def run_c4(args):
 
     from paper_2503_15921_b200.models import LLAMA_13B, LLAMA_68M, LLAMA_160M, LLAMA_160M_B, Engine, synthetic_prompts
     from paper_2503_15921_b200.selector import Lbss
+    from paper_2503_15921_b200.trace import RoundTrace
 
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     ssms = (LLAMA_68M, LLAMA_160M, LLAMA_160M_B)
@@ -255,12 +256,14 @@ def run_c4(args):
         homo[s.name] = {"tokens_per_s": toks / (ms / 1e3), "mean_accepted": toks / (6 * BATCH) - 1}
     # LBSS on measured goodput
     sel = Lbss(BATCH, [BATCH] * len(ssms), alpha=8, beta=2, seed=SEED)
+    trace = RoundTrace()  # the LBSS run's event trace in the reference schema (trace_io.cpp)
     toks, ms, wall0 = 0, 0.0, time.perf_counter()
     explore_slots = 0
     for _ in range(slots_n):
         assign, explore = sel.next_slot()
         assign = assign.astype(np.int32)
         r = eng.round(slots, assign)
+        trace.record(eng, assign, r)
         sec = r["round_ms"] / 1e3
         for i in range(BATCH):
             if assign[i] >= 0:
@@ -270,10 +273,14 @@ def run_c4(args):
         explore_slots += int(explore)
     wall = time.perf_counter() - wall0
     final = sel.exploitation()
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "c4_trace.csv"), "w") as f:
+        f.write(trace.csv())
     eng.close()
     out["value"] = toks / (ms / 1e3)
     out["lbss"] = {"tokens_per_s_device": toks / (ms / 1e3), "tokens_per_s_wall": toks / wall,
                    "explore_slots": explore_slots, "epochs": sel.epoch,
+                   "llm_busy_sec": trace.llm_busy, "llm_idle_sec": trace.llm_idle,
                    "final_assignment_histogram": np.bincount(final, minlength=len(ssms)).tolist()}
     out["homogeneous"] = homo
     out["note"] = ("wall time includes host-side SSM switches (KV recompute on the destination SSM, "

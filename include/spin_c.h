@@ -184,6 +184,12 @@ spin_status spin_round_launches(spin_ctx* ctx, int32_t n, const int32_t* slots, 
 spin_status spin_kernel_bench(spin_ctx* ctx, int32_t kind, int32_t iters, double* us_per_launch,
                               double* bytes_per_launch);
 
+/* Event trace of the last spin_round: per-SSM draft end, device ms after the
+ * round start (-1 for an SSM without requests). With draft_ms (= verify start),
+ * round_ms (= verify end) of spin_round_out this yields the reference's
+ * EventTrace (pipeline.hpp:14-30): spec_start/spec_end per SSM, verify_start/end. */
+spin_status spin_last_round_trace(spin_ctx* ctx, float* spec_end_ms, int32_t cap);
+
 /* Ragged-window verification (BASELINE config 3, request-decomposition sweep):
  * request i verifies draft_lens[i] in 1..window drafts (drafts: host tokens, flat,
  * sum(draft_lens) entries, or NULL for the history token). packed = 1: pack() of

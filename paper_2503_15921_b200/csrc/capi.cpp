@@ -328,6 +328,13 @@ spin_status spin_verify_bench(spin_ctx* ctx, int32_t n, const int32_t* slots, co
   });
 }
 
+spin_status spin_last_round_trace(spin_ctx* ctx, float* spec_end_ms, int32_t cap) {
+  return guarded([&] {
+    if (!ctx || !spec_end_ms) fail(SPIN_INPUT_ERROR, "last_round_trace: null argument");
+    ctx->eng->last_round_trace(spec_end_ms, cap);
+  });
+}
+
 spin_status spin_switch_ssm(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of) {
   return guarded([&] {
     if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");

@@ -369,6 +369,9 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
   check_cuda(cudaEventCreate(&ev_end_), "event");
   ev_join_.resize(n_ssm);
   for (auto& e : ev_join_) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  ev_spec_end_.resize(n_ssm);  // per-SSM draft end (timing; the event trace)
+  for (auto& e : ev_spec_end_) check_cuda(cudaEventCreate(&e), "event");
+  last_spec_ms_.assign(n_ssm, -1.f);
   check_cuda(cudaStreamSynchronize(sv_), "init sync");
 }
 
@@ -391,6 +394,7 @@ Engine::~Engine() {
   cudaFreeHost(pin_in_), cudaFreeHost(pin_out_), cudaFree(d_in_), cudaFree(d_out_), cudaFree(d_emitted_);
   cudaEventDestroy(ev_fork_), cudaEventDestroy(ev_start_), cudaEventDestroy(ev_draft_), cudaEventDestroy(ev_end_);
   for (auto& e : ev_join_) cudaEventDestroy(e);
+  for (auto& e : ev_spec_end_) cudaEventDestroy(e);
   for (auto& s : ss_) cudaStreamDestroy(s);
   cudaStreamDestroy(sv_);
 }
@@ -603,6 +607,7 @@ void Engine::capture_round(RoundPlan& p) {
         prev_t = nj, prev_q = 1;
       }
     }
+    if (p.n_ssm[j] > 0) record_timing(ev_spec_end_[j], sj);
     check_cuda(cudaEventRecord(ev_join_[j], sj), "join");
     check_cuda(cudaStreamWaitEvent(s, ev_join_[j], 0), "join");
   }
@@ -679,6 +684,10 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, spin_roun
   float draft_ms = 0.f, total_ms = 0.f;
   check_cuda(cudaEventElapsedTime(&draft_ms, ev_start_, ev_draft_), "event timing");
   check_cuda(cudaEventElapsedTime(&total_ms, ev_start_, ev_end_), "event timing");
+  for (int j = 0; j < M; ++j) {
+    last_spec_ms_[j] = -1.f;
+    if (p.n_ssm[j] > 0) check_cuda(cudaEventElapsedTime(&last_spec_ms_[j], ev_start_, ev_spec_end_[j]), "event timing");
+  }
   const int na = p.n_act;
   const int32_t* acc = pin_out_;
   const int32_t* bon = pin_out_ + na;
@@ -988,6 +997,10 @@ void Engine::verify_bench(int n, const int32_t* slots, const int32_t* draft_lens
     out->real_rows = real_rows;
     out->kv_tokens = kv_read;
   }
+}
+
+void Engine::last_round_trace(float* spec_end_ms, int cap) const {
+  for (int j = 0; j < cap && j < static_cast<int>(last_spec_ms_.size()); ++j) spec_end_ms[j] = last_spec_ms_[j];
 }
 
 int64_t Engine::launches_per_round(int n, const int32_t* slots, const int32_t* ssm_of) {

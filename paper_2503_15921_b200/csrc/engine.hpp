@@ -79,6 +79,8 @@ class Engine {
   void profile_round(int n, const int32_t* slots, const int32_t* ssm_of, double* ms, double* bytes,
                      int64_t* launches);
   int64_t launches_per_round(int n, const int32_t* slots, const int32_t* ssm_of);
+  // Per-SSM draft end of the last round, ms after the round start (-1: SSM idle).
+  void last_round_trace(float* spec_end_ms, int cap) const;
   void kernel_bench(int kind, int iters, double* us_per_launch, double* bytes_per_launch);
   void verify_bench(int n, const int32_t* slots, const int32_t* draft_lens, const int32_t* drafts, int packed,
                     int iters, spin_verify_stats* out);
@@ -130,7 +132,8 @@ class Engine {
   unsigned long long* d_emitted_ = nullptr;
   size_t in_cap_ = 0, out_cap_ = 0;
   cudaEvent_t ev_fork_ = nullptr, ev_start_ = nullptr, ev_draft_ = nullptr, ev_end_ = nullptr;
-  std::vector<cudaEvent_t> ev_join_;
+  std::vector<cudaEvent_t> ev_join_, ev_spec_end_;
+  std::vector<float> last_spec_ms_;
   std::map<std::vector<int>, std::unique_ptr<RoundPlan>> rounds_;
   int last_verify_rows_ = 0;
 };
