@@ -178,7 +178,7 @@ spin_status spin_round_launches(spin_ctx* ctx, int32_t n, const int32_t* slots, 
                                 int64_t* launches);
 
 /* In-situ kernel timing on the target state of the last verify: kind 0 = the
- * four projection GEMMs of every layer, kind 1 = attention (+combine) of every
+ * four projection GEMMs of every layer, kind 1 = attention (split-KV merge in-kernel) of every
  * layer, replayed as one CUDA graph `iters` times (CUDA events). Outputs the
  * average device time per launch and algorithmic bytes per launch. */
 spin_status spin_kernel_bench(spin_ctx* ctx, int32_t kind, int32_t iters, double* us_per_launch,
