@@ -213,8 +213,9 @@ spin_status spin_verify_bench(spin_ctx* ctx, int32_t n, const int32_t* slots, co
  * ---------------------------------------------------------------------- */
 spin_status spin_gemm_info(int32_t n_out, int32_t k, int32_t t, int32_t mode, int32_t* max_pieces,
                            int32_t* grid, int32_t* bn);
-/* mode 0: part[max_pieces][t][n_out] partial sums (caller zero-fills, sums slots);
- * mode 1: amax_val/amax_idx [ceil(n_out/128)][t], logits [t][n_out] optional. */
+/* w: row-major [n_out][k] bf16 (converted to the tiled GEMM weight layout internally); x: [t][k].
+ * mode 0: part[max_pieces][t][n_out] partial sums (caller zero-fills, sums slots);
+ * mode 1: amax_val/amax_idx [ceil(n_out/128)][t], logits [t][n_out] optional. Synchronous. */
 spin_status spin_gemm(void* stream, const void* w, const void* x, int32_t n_out, int32_t k, int32_t t,
                       int32_t mode, float* part, float* amax_val, int32_t* amax_idx, float* logits);
 

@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 namespace spin {
 
@@ -404,7 +405,11 @@ void launch_hd(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& 
 
 int attn_chunks(int rows, int heads, int num_sms) {
   // ~8 warps of work per SM (2 CTAs x 4 warps): rows x chunks x heads ~= 8 x SMs
-  const double want = 8.0 * num_sms / std::max(1, rows * heads);
+  static const double wps = [] {
+    const char* e = std::getenv("SPIN_ATTN_WPS");  // experiments only
+    return e ? std::atof(e) : 8.0;
+  }();
+  const double want = wps * num_sms / std::max(1, rows * heads);
   return std::max(1, std::min(16, static_cast<int>(std::lround(want))));
 }
 

@@ -84,6 +84,11 @@ spin_status spin_gemm(void* stream, const void* w, const void* x, int32_t n_out,
     if (n_out < 1 || k < 1 || t < 1) fail(SPIN_INPUT_ERROR, "spin_gemm: empty shape");
     if (k % 8 != 0) fail(SPIN_INPUT_ERROR, "spin_gemm: K must be a multiple of 8 (16-B rows)");
     const GemmPlan p = gemm_plan(n_out, k, t, mode, num_sms_cached());
+    // row-major caller weights -> the tiled GEMM layout
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    void* wt = nullptr;
+    check_cuda(cudaMalloc(&wt, tiled_weight_elems(n_out, k) * 2), "malloc");
+    launch_tile_weights(static_cast<const bf16*>(w), static_cast<bf16*>(wt), n_out, k, st);
     GemmEpilogue e;
     e.mode = mode;
     e.part = part;
@@ -93,8 +98,11 @@ spin_status spin_gemm(void* stream, const void* w, const void* x, int32_t n_out,
     if (mode == kGemmPartial && part == nullptr) fail(SPIN_INPUT_ERROR, "spin_gemm: partial buffer missing");
     if (mode == kGemmArgmax && (amax_val == nullptr || amax_idx == nullptr))
       fail(SPIN_INPUT_ERROR, "spin_gemm: argmax buffers missing");
-    check_cuda(gemm_launch(p, w, x, e, static_cast<cudaStream_t>(stream), false), "gemm launch");
-    check_cuda(cudaGetLastError(), "gemm launch");
+    const cudaError_t err = gemm_launch(p, wt, x, e, st, false);
+    const cudaError_t err2 = cudaStreamSynchronize(st);
+    cudaFree(wt);
+    check_cuda(err, "gemm launch");
+    check_cuda(err2, "gemm");
   });
 }
 

@@ -88,20 +88,23 @@ void Engine::init_model(ModelDev& m, const spin_model_desc& d) {
   m.d = d;
   m.D = d.d_model, m.H = d.n_heads, m.hd = d.head_dim, m.F = d.ffn, m.V = d.vocab, m.L = d.n_layers;
   const size_t D = m.D, F = m.F, V = m.V;
-  const size_t per_layer = 3 * D * D + D * D + 2 * F * D + D * F;
-  const size_t total = 2 * V * D + per_layer * m.L;
+  // GEMM weights in the tiled layout (gemm.cuh); the embedding stays row-major (gathered)
+  const size_t n_qkv = tiled_weight_elems(3 * D, D), n_o = tiled_weight_elems(D, D);
+  const size_t n_gu = tiled_weight_elems(2 * F, D), n_dn = tiled_weight_elems(D, F);
+  const size_t per_layer = n_qkv + n_o + n_gu + n_dn;
+  const size_t total = V * D + tiled_weight_elems(V, D) + per_layer * m.L;
   m.weight_bytes = total * 2;
   check_cuda(cudaMalloc(&m.wbuf, m.weight_bytes), "weights");
   m.emb = m.wbuf;
   m.head = m.wbuf + V * D;
-  bf16* p = m.wbuf + 2 * V * D;
+  bf16* p = m.head + tiled_weight_elems(V, D);
   m.layers.resize(m.L);
   for (int l = 0; l < m.L; ++l) {
     LayerW& w = m.layers[l];
-    w.qkv = p, p += 3 * D * D;
-    w.o = p, p += D * D;
-    w.gu = p, p += 2 * F * D;
-    w.dn = p, p += D * F;
+    w.qkv = p, p += n_qkv;
+    w.o = p, p += n_o;
+    w.gu = p, p += n_gu;
+    w.dn = p, p += n_dn;
   }
   // Synthetic weights, same spec as oracle/llama_oracle.c.
   auto stream_of = [&](int tag, int layer) { return host_mix_seed(d.seed, 0x5350494EULL, tag, layer); };
@@ -110,22 +113,23 @@ void Engine::init_model(ModelDev& m, const spin_model_desc& d) {
   const float s_in = static_cast<float>(std::sqrt(3.0 / D) * d.init_scale);
   const float s_o = static_cast<float>(std::sqrt(3.0 / D) * d.resid_scale);
   const float s_dn = static_cast<float>(std::sqrt(3.0 / F) * d.resid_scale);
-  launch_init_weights(m.emb, V, D, stream_of(kTagEmbed, 0), s_emb, nullptr, 0.f, V, 1, 0, sv_);
+  launch_init_weights(m.emb, V, D, stream_of(kTagEmbed, 0), s_emb, nullptr, 0.f, V, 1, 0, 0, sv_);
   int64_t a = 7919 % static_cast<int64_t>(V);
   if (a == 0) a = 1;
   while (gcd64(a, V) != 1) a = (a + 1) % static_cast<int64_t>(V);
   const int64_t cc = 12345 % static_cast<int64_t>(V);
   const float g = static_cast<float>(static_cast<double>(d.planted_gain) / static_cast<double>(D));
   launch_init_weights(m.head, V, D, stream_of(kTagHead, 0), s_head, d.planted_gain != 0.f ? m.emb : nullptr, g, V,
-                      mod_inverse(a, V), cc, sv_);
+                      mod_inverse(a, V), cc, 1, sv_);
   for (int l = 0; l < m.L; ++l) {
     launch_init_weights(const_cast<bf16*>(m.layers[l].qkv), 3 * D, D, stream_of(kTagQkv, l), s_in, nullptr, 0.f, V, 1,
-                        0, sv_);
-    launch_init_weights(const_cast<bf16*>(m.layers[l].o), D, D, stream_of(kTagO, l), s_o, nullptr, 0.f, V, 1, 0, sv_);
-    launch_init_weights(const_cast<bf16*>(m.layers[l].gu), 2 * F, D, stream_of(kTagGateUp, l), s_in, nullptr, 0.f, V,
-                        1, 0, sv_);
-    launch_init_weights(const_cast<bf16*>(m.layers[l].dn), D, F, stream_of(kTagDown, l), s_dn, nullptr, 0.f, V, 1, 0,
+                        0, 1, sv_);
+    launch_init_weights(const_cast<bf16*>(m.layers[l].o), D, D, stream_of(kTagO, l), s_o, nullptr, 0.f, V, 1, 0, 1,
                         sv_);
+    launch_init_weights(const_cast<bf16*>(m.layers[l].gu), 2 * F, D, stream_of(kTagGateUp, l), s_in, nullptr, 0.f, V,
+                        1, 0, 1, sv_);
+    launch_init_weights(const_cast<bf16*>(m.layers[l].dn), D, F, stream_of(kTagDown, l), s_dn, nullptr, 0.f, V, 1, 0,
+                        1, sv_);
   }
   check_cuda(cudaGetLastError(), "init weights");
   // KV cache [layer][slot][head][ctx][hd], zero-filled.

@@ -1,7 +1,8 @@
 // tcgen05 / TMEM / TMA weight-streaming GEMM (see gemm.cuh for the contract).
 //
 // CTA = 8 warps, one CTA per SM (persistent):
-//   warp 0      TMA producer (one elected lane): W tile 128x64 + X tile bn x64 per stage
+//   warp 0      TMA producer (one elected lane): W tile 128x64 (1-D bulk copy of a
+//               pre-tiled 16-KiB atom) + X tile bn x64 (2-D tensor map) per stage
 //   warp 1      MMA issuer (lane 0): 4 x tcgen05.mma 128 x bn x 16 per stage
 //   warp 2      TMEM allocator (2 accumulator buffers of bn fp32 columns)
 //   warps 4..7  epilogue: tcgen05.ld 32 lanes each -> partial store / argmax
@@ -11,6 +12,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 
@@ -71,8 +73,9 @@ __device__ __forceinline__ void argmax_merge(float& v, int& i, float ov, int oi)
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-                   PieceMap pm, GemmEpilogue epi, int n_out, int t_total, int stages) {
+    gemm_tc_kernel(const __nv_bfloat16* __restrict__ w_tiled, const __grid_constant__ CUtensorMap tm_x,
+                   const __grid_constant__ CUtensorMap tm_part, PieceMap pm, GemmEpilogue epi, int n_out, int t_total,
+                   int stages, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
@@ -95,10 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(2 * bn)) tmem_cols <<= 1;
 
-  if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch_desc(&tm_w);
-    ptx::tma_prefetch_desc(&tm_x);
-  }
+  if (warp == 0 && lane == 0) ptx::tma_prefetch_desc(&tm_x);
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
@@ -137,9 +137,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (s < stages && pre.next(pm, n_tiles, q)) {
           const int mt = q.tile % pm.n_mtiles;
           for (int kb = q.kb0; kb < q.kb1 && s < stages; ++kb, ++s) {
-            ptx::mbar_arrive_expect_tx(&full_bar[s], kTileABytes + tile_b_bytes);
-            ptx::tma_load_2d(smem_a + static_cast<size_t>(s) * kTileABytes, &tm_w, &full_bar[s], kb * kBlockK,
-                             mt * kBlockM, pol_w);
+            ptx::mbar_arrive_expect_tx(&full_bar[s], kTileABytes + ((dbg & 1) ? 0u : tile_b_bytes));
+            ptx::bulk_load(smem_a + static_cast<size_t>(s) * kTileABytes,
+                           w_tiled + (static_cast<size_t>(mt) * pm.kb + kb) * (kBlockM * kBlockK), kTileABytes,
+                           &full_bar[s], pol_w);
           }
         }
         prefetched = s;
@@ -153,12 +154,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = p.kb0; kb < p.kb1; ++kb) {
           if (issued >= prefetched) {
             ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-            ptx::mbar_arrive_expect_tx(&full_bar[stage], kTileABytes + tile_b_bytes);
-            ptx::tma_load_2d(smem_a + static_cast<size_t>(stage) * kTileABytes, &tm_w, &full_bar[stage],
-                             kb * kBlockK, mt * kBlockM, pol_w);
+            ptx::mbar_arrive_expect_tx(&full_bar[stage], kTileABytes + ((dbg & 1) ? 0u : tile_b_bytes));
+            ptx::bulk_load(smem_a + static_cast<size_t>(stage) * kTileABytes,
+                           w_tiled + (static_cast<size_t>(mt) * pm.kb + kb) * (kBlockM * kBlockK), kTileABytes,
+                           &full_bar[stage], pol_w);
           }
-          ptx::tma_load_2d(smem_b + static_cast<size_t>(stage) * tile_b_bytes, &tm_x, &full_bar[stage],
-                           kb * kBlockK, nt * bn, pol_x);
+          if (!(dbg & 1))
+            ptx::tma_load_2d(smem_b + static_cast<size_t>(stage) * tile_b_bytes, &tm_x, &full_bar[stage],
+                             kb * kBlockK, nt * bn, pol_x);
           ++issued;
           if (++stage == stages) {
             stage = 0;
@@ -188,10 +191,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           const uint64_t da = ptx::smem_desc_sw128(smem_a + static_cast<size_t>(stage) * kTileABytes);
           const uint64_t db = ptx::smem_desc_sw128(smem_b + static_cast<size_t>(stage) * tile_b_bytes);
+          if (!(dbg & 2)) {
 #pragma unroll
-          for (int k = 0; k < kBlockK / 16; ++k) {
-            // +32 bytes per 16-element K step inside the 128-B swizzle atom.
-            ptx::umma_bf16(d_addr, da + 2 * k, db + 2 * k, idesc, (kb > p.kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kBlockK / 16; ++k) {
+              // +32 bytes per 16-element K step inside the 128-B swizzle atom.
+              ptx::umma_bf16(d_addr, da + 2 * k, db + 2 * k, idesc, (kb > p.kb0 || k > 0) ? 1u : 0u);
+            }
           }
           ptx::umma_commit(&empty_bar[stage]);
           if (kb + 1 == p.kb1) ptx::umma_commit(&tfull_bar[acc]);
@@ -224,7 +229,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n = mt * kBlockM + row;
       const bool n_ok = n < n_out;
       const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * bn);
-      if (epi.mode == kGemmPartial) {
+      PieceIter ahead = it;
+      Piece pn;
+      const bool last_piece = !ahead.next(pm, n_tiles, pn);
+      if (epi.mode == kGemmPartial && last_piece && !(dbg & 8)) {
+        // The CTA's last piece: every MMA is done, so the stage ring is free. Stage the
+        // fp32 tile as [t][128 features] and write it with one TMA tensor store.
+        float* stg = reinterpret_cast<float*>(smem);
+        for (int c0 = 0; c0 < bn; c0 += 16) {
+          float v[16];
+          ptx::tmem_ld16(t_addr + c0, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) stg[(c0 + j) * kBlockM + row] = v[j];
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+        ptx::fence_proxy_async_smem();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (ew == 0 && lane == 0) {
+          ptx::tma_store_3d(&tm_part, stg, mt * kBlockM, nt * bn, p.slot);
+          ptx::bulk_commit();
+          ptx::bulk_wait0();  // the consumer kernel reads the partial after this grid completes
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      } else if (epi.mode == kGemmPartial) {
         float* dst = epi.part + static_cast<size_t>(p.slot) * t_total * n_out;
         for (int c0 = 0; c0 < bn; c0 += 16) {
           float v[16];
@@ -232,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int t = nt * bn + c0 + j;
-            if (n_ok && t < t_total) dst[static_cast<size_t>(t) * n_out + n] = v[j];
+            if (n_ok && t < t_total && !(dbg & 4)) dst[static_cast<size_t>(t) * n_out + n] = v[j];
           }
         }
         ptx::tc_fence_before();
@@ -363,9 +392,22 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
 
 cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, const GemmEpilogue& epi,
                         cudaStream_t stream, bool pdl) {
-  CUtensorMap tm_w, tm_x;
-  if (!encode_tmap_bf16(&tm_w, W, plan.n_out, plan.k, kBlockM, kBlockK, true)) return cudaErrorInvalidValue;
+  CUtensorMap tm_x, tm_part{};
   if (!encode_tmap_bf16(&tm_x, X, plan.t, plan.k, plan.bn, kBlockK, true)) return cudaErrorInvalidValue;
+  if (epi.mode == kGemmPartial) {
+    // part[slot][t][n_out] fp32 as a 3-D tensor (clips rows t >= T and features n >= n_out)
+    auto fn = get_encode_fn();
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(plan.n_out), static_cast<cuuint64_t>(plan.t),
+                          static_cast<cuuint64_t>(plan.max_pieces)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(plan.n_out) * 4, static_cast<cuuint64_t>(plan.n_out) * plan.t * 4};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(kBlockM), static_cast<cuuint32_t>(plan.bn), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (fn == nullptr || (plan.n_out * 4) % 16 != 0 ||
+        fn(&tm_part, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, epi.part, dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -381,7 +423,12 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   GemmEpilogue e = epi;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel, tm_w, tm_x, plan.map, e, plan.n_out, plan.t, plan.stages);
+  static const int dbg = [] {
+    const char* s = std::getenv("SPIN_GEMM_DBG");  // timing experiments only: 1 no X, 2 no MMA, 4 no stores
+    return s ? std::atoi(s) : 0;
+  }();
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel, static_cast<const __nv_bfloat16*>(W), tm_x, tm_part, plan.map, e,
+                            plan.n_out, plan.t, plan.stages, dbg);
 }
 
 }  // namespace spin

@@ -67,11 +67,20 @@ struct GemmEpilogue {
   float* logits = nullptr;   // ARGMAX (optional): [t][n_out]
 };
 
+// Weights are stored TILED: [ceil(N/128)][ceil(K/64)] atoms of 128 x 64 bf16, each a
+// contiguous 16-KiB block that already is the 128-B-swizzled shared-memory image the
+// tensor core reads, streamed with 1-D bulk copies: contiguous 16-KiB copies reach
+// ~7 TB/s where 2-D boxes over row-major weights (128 B from each of 128 rows 2K bytes
+// apart) cap near 5.4 TB/s (profiles/r01_stream_probe.txt).
+inline size_t tiled_weight_elems(int64_t rows, int64_t cols) {
+  return static_cast<size_t>((rows + 127) / 128) * ((cols + 63) / 64) * 128 * 64;
+}
+
 // Plans a launch for the given shape on `num_sms` SMs.
 GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms);
 
-// Encodes the two TMA descriptors (weights box 64x128, activations box 64xbn)
-// and launches. `pdl` enables programmatic dependent launch.
+// Launches with W in the tiled layout and X row-major [t][k] (TMA box 64 x bn).
+// `pdl` enables programmatic dependent launch.
 cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, const GemmEpilogue& epi,
                         cudaStream_t stream, bool pdl);
 

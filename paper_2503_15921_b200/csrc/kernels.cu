@@ -525,22 +525,57 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+// Synthetic weights, written in physical order.
+//   tiled = 1: GEMM weight layout -- [ceil(rows/128)][ceil(cols/64)] atoms of 128 x 64 bf16,
+//              each a contiguous 16-KiB block holding the 128-B-swizzled shared-memory image
+//              (16-B chunk c of row r at c ^ (r % 8)); padding rows / columns are zero;
+//   tiled = 0: row-major (the embedding, gathered by token).
+// Values depend only on the logical (row, col): the oracle restates them row-major.
 __global__ void init_weights_kernel(bf16* w, int64_t rows, int64_t cols, uint64_t stream, float scale,
-                                    const bf16* emb, float g, int64_t vocab, int64_t a_inv, int64_t cc) {
-  const int64_t total = rows * cols;
+                                    const bf16* emb, float g, int64_t vocab, int64_t a_inv, int64_t cc, int tiled) {
+  const int64_t katoms = (cols + 63) / 64;
+  const int64_t prow = tiled ? (rows + 127) / 128 * 128 : rows, pcols = tiled ? katoms * 64 : cols;
+  const int64_t total = prow * pcols;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float u = static_cast<float>(splitmix64(stream + static_cast<uint64_t>(e)) >> 40);
+    int64_t row, col;
+    if (tiled) {
+      const int64_t atom = e >> 13, within = e & 8191;
+      const int64_t r = within >> 6, pc = within & 63;
+      row = (atom / katoms) * 128 + r;
+      col = (atom % katoms) * 64 + ((((pc >> 3) ^ (r & 7)) << 3) | (pc & 7));
+    } else {
+      row = e / cols, col = e % cols;
+    }
+    if (row >= rows || col >= cols) {
+      w[e] = __float2bfloat16_rn(0.f);
+      continue;
+    }
+    const int64_t le = row * cols + col;  // logical element index
+    const float u = static_cast<float>(splitmix64(stream + static_cast<uint64_t>(le)) >> 40);
     const float r = __fsub_rn(__fmul_rn(u, 0x1.0p-23f), 1.0f);
     const float a = __fmul_rn(r, scale);
     if (emb == nullptr) {
       w[e] = __float2bfloat16_rn(a);
     } else {
-      const int64_t row = e / cols, col = e % cols;
       const int64_t src = (a_inv * (((row - cc) % vocab + vocab) % vocab)) % vocab;
       const float b = __fmul_rn(g, __bfloat162float(emb[src * cols + col]));
       w[e] = __float2bfloat16_rn(__fadd_rn(a, b));
     }
+  }
+}
+
+// Row-major [rows][cols] bf16 -> tiled GEMM weight layout (kernel tests, external weights).
+__global__ void tile_weights_kernel(const bf16* __restrict__ src, bf16* __restrict__ dst, int64_t rows, int64_t cols) {
+  const int64_t katoms = (cols + 63) / 64;
+  const int64_t total = (rows + 127) / 128 * 128 * katoms * 64;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t atom = e >> 13, within = e & 8191;
+    const int64_t r = within >> 6, pc = within & 63;
+    const int64_t p = (atom / katoms) * 128 + r;
+    const int64_t col = (atom % katoms) * 64 + ((((pc >> 3) ^ (r & 7)) << 3) | (pc & 7));
+    dst[e] = (p < rows && col < cols) ? src[p * cols + col] : __float2bfloat16_rn(0.f);
   }
 }
 
@@ -680,8 +715,12 @@ void launch_accept(const FwdMeta& m, int n_req, int window, const int32_t* list,
 }
 
 void launch_init_weights(bf16* w, int64_t rows, int64_t cols, uint64_t stream, float scale, const bf16* emb,
-                         float planted_g, int64_t vocab, int64_t A_inv, int64_t Cc, cudaStream_t s) {
-  init_weights_kernel<<<148 * 8, 256, 0, s>>>(w, rows, cols, stream, scale, emb, planted_g, vocab, A_inv, Cc);
+                         float planted_g, int64_t vocab, int64_t A_inv, int64_t Cc, int tiled, cudaStream_t s) {
+  init_weights_kernel<<<148 * 8, 256, 0, s>>>(w, rows, cols, stream, scale, emb, planted_g, vocab, A_inv, Cc, tiled);
+}
+
+void launch_tile_weights(const bf16* src, bf16* dst, int64_t rows, int64_t cols, cudaStream_t s) {
+  tile_weights_kernel<<<148 * 8, 256, 0, s>>>(src, dst, rows, cols);
 }
 
 void launch_toy_attention(const double* q, const double* k, const double* v, const int32_t* q_off,

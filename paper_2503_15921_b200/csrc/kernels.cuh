@@ -116,8 +116,11 @@ void launch_accept(const FwdMeta& m, int n_req, int window, const int32_t* list,
                    int32_t* out_accepted, int32_t* out_bonus, int32_t* out_committed, int32_t* out_drafts,
                    int32_t* out_target, unsigned long long* emitted, cudaStream_t s);
 
+// tiled = 1: the GEMM weight layout (gemm.cuh tiled_weight_elems); 0: row-major (embedding).
 void launch_init_weights(bf16* w, int64_t rows, int64_t cols, uint64_t stream, float scale, const bf16* emb,
-                         float planted_g, int64_t vocab, int64_t A_inv, int64_t Cc, cudaStream_t s);
+                         float planted_g, int64_t vocab, int64_t A_inv, int64_t Cc, int tiled, cudaStream_t s);
+// Row-major [rows][cols] -> tiled GEMM weight layout.
+void launch_tile_weights(const bf16* src, bf16* dst, int64_t rows, int64_t cols, cudaStream_t s);
 
 // Toy-mode packed attention for the decomposed_attention operator (K/V laid
 // out per request, any dim, scale 1, no causal mask).
