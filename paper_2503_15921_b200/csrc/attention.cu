@@ -9,7 +9,7 @@
 // per-slot KV cache in place (zero-copy packing).
 //
 // One WARP per (row, chunk, head), no CTA-level synchronisation: the warp owns
-// a ring of 16-key K/V tiles (TMA, 128-B swizzle, lane 0 issues ahead across
+// a ring of 16-key K/V tiles (1-D bulk copies of the pre-swizzled cache rows, lane 0 issues ahead across
 // its pieces) and computes the TRANSPOSED scores S^T = K Q^T on the tensor
 // cores (mma.sync m16n8k16: 16 keys are M, the request's <= 8 queries per
 // n-tile are N), an online softmax per query column, and O^T += V^T P^T (head
@@ -68,9 +68,12 @@ __device__ __forceinline__ uint32_t movm_t(uint32_t x) {
   return y;
 }
 
-// byte offset of (key row, 16-B chunk) in a 16-key TMA tile: 64-dim boxes of 2 KiB, 128-B swizzle
-__device__ __forceinline__ uint32_t kswz(int row, int chunk) {
-  return static_cast<uint32_t>((chunk >> 3) * 2048 + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
+// byte offset of (key row, 16-B chunk) in a 16-key tile bulk-copied from the swizzled
+// cache (kv_swz): rows of HD*2 bytes, chunk c of absolute key p at c ^ (p % 8) within
+// its 128-B span; `base` = absolute key of row 0 (mod 8).
+template <int HD>
+__device__ __forceinline__ uint32_t kvoff(int row, int chunk, int base) {
+  return static_cast<uint32_t>(row * (HD * 2) + (chunk >> 3) * 128 + (((chunk & 7) ^ ((row + base) & 7)) << 4));
 }
 
 template <int HD, int NQT>
@@ -143,14 +146,12 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
         if (lane == 0) {
           const int st = issued % S;
           uint8_t* dst = ring + st * C::kStage;
-          const int r0 = ((kv_base + ph.slot * H + head) * g.ctx) + ph.tok0 + it * 16;
+          const size_t r0 = (static_cast<size_t>(kv_base + ph.slot * H + head) * g.ctx) + ph.tok0 + it * 16;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           ptx::mbar_arrive_expect_tx(&bar[st], C::kStage);
-#pragma unroll
-          for (int bx = 0; bx < HD / 64; ++bx) {
-            ptx::tma_load_2d(dst + bx * 2048, &tm_k, &bar[st], bx * 64, r0, pol);
-            ptx::tma_load_2d(dst + C::kHalf + bx * 2048, &tm_v, &bar[st], bx * 64, r0, pol);
-          }
+          // 16 consecutive keys are one contiguous, pre-swizzled block of K and of V
+          ptx::bulk_load(dst, g.k_cache + r0 * HD, C::kHalf, &bar[st], pol);
+          ptx::bulk_load(dst + C::kHalf, g.v_cache + r0 * HD, C::kHalf, &bar[st], pol);
         }
         ++issued;
         ++it;
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
 #pragma unroll
         for (int kt = 0; kt < DT; ++kt) {
           uint32_t a[4];
-          ldsm_x4(kb + kswz((lane & 7) + ((lane >> 3) & 1) * 8, 2 * kt + (lane >> 4)), a);
+          ldsm_x4(kb + kvoff<HD>((lane & 7) + ((lane >> 3) & 1) * 8, 2 * kt + (lane >> 4), ph.tok0), a);
 #pragma unroll
           for (int nt = 0; nt < NQT; ++nt) {
             mma16816(s[nt], a, qh[nt][kt][0], qh[nt][kt][1]);
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
 #pragma unroll
         for (int dt = 0; dt < DT; ++dt) {
           uint32_t a[4];
-          ldsm_x4_t(vb + kswz((lane & 7) + ((lane >> 4) & 1) * 8, 2 * dt + ((lane >> 3) & 1)), a);
+          ldsm_x4_t(vb + kvoff<HD>((lane & 7) + ((lane >> 4) & 1) * 8, 2 * dt + ((lane >> 3) & 1), ph.tok0), a);
 #pragma unroll
           for (int nt = 0; nt < NQT; ++nt) {
             float* oo = o + (nt * DT + dt) * 4;

@@ -432,13 +432,14 @@ spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int3
     a.chunks = chunks;
     SlotState st{};
     launch_meta(a, st, m, s);
-    AttnGeom g{n_heads, head_dim, slots, ctx, layer, static_cast<float>(1.0 / std::sqrt(double(head_dim))),
-               const_cast<bf16*>(static_cast<const bf16*>(k_cache)), const_cast<bf16*>(static_cast<const bf16*>(v_cache))};
-    CUtensorMap tk, tv;
-    const uint64_t kv_rows = static_cast<uint64_t>(layers) * slots * n_heads * ctx;
-    if (!encode_tmap_bf16(&tk, k_cache, kv_rows, head_dim, 16, 64, true) ||
-        !encode_tmap_bf16(&tv, v_cache, kv_rows, head_dim, 16, 64, true))
-      fail(SPIN_CUDA_ERROR, "tensor map encode");
+    // caller caches are in the standard [..][ctx][hd] layout: swizzled copies (kv_swz) + 16 padding rows
+    const int64_t kv_rows = static_cast<int64_t>(layers) * slots * n_heads * ctx;
+    bf16* ks = static_cast<bf16*>(dal((kv_rows + 16) * head_dim * 2));
+    bf16* vs = static_cast<bf16*>(dal((kv_rows + 16) * head_dim * 2));
+    launch_swizzle_kv(static_cast<const bf16*>(k_cache), ks, kv_rows, head_dim, ctx, s);
+    launch_swizzle_kv(static_cast<const bf16*>(v_cache), vs, kv_rows, head_dim, ctx, s);
+    AttnGeom g{n_heads, head_dim, slots, ctx, layer, static_cast<float>(1.0 / std::sqrt(double(head_dim))), ks, vs};
+    CUtensorMap tk{}, tv{};  // unused by the bulk-copy attention
     launch_attention(tk, tv, m, rows, n_req, g, static_cast<const float*>(q), w, static_cast<bf16*>(out), s);
     check_cuda(cudaGetLastError(), "attention launch");
     check_cuda(cudaStreamSynchronize(s), "attention");

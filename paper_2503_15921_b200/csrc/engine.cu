@@ -134,11 +134,13 @@ void Engine::init_model(ModelDev& m, const spin_model_desc& d) {
   check_cuda(cudaGetLastError(), "init weights");
   // KV cache [layer][slot][head][ctx][hd], zero-filled.
   const size_t kv = static_cast<size_t>(m.L) * opts_.max_requests * m.H * opts_.max_ctx * m.hd;
-  m.kv_bytes = 2 * kv * 2;
-  check_cuda(cudaMalloc(&m.kc, kv * 2), "k cache");
-  check_cuda(cudaMalloc(&m.vc, kv * 2), "v cache");
-  check_cuda(cudaMemsetAsync(m.kc, 0, kv * 2, sv_), "memset");
-  check_cuda(cudaMemsetAsync(m.vc, 0, kv * 2, sv_), "memset");
+  // + 16 padding rows: a 16-key tile starting near the end of the last context stays in bounds
+  const size_t kv_alloc = kv + static_cast<size_t>(16) * m.hd;
+  m.kv_bytes = 2 * kv_alloc * 2;
+  check_cuda(cudaMalloc(&m.kc, kv_alloc * 2), "k cache");
+  check_cuda(cudaMalloc(&m.vc, kv_alloc * 2), "v cache");
+  check_cuda(cudaMemsetAsync(m.kc, 0, kv_alloc * 2, sv_), "memset");
+  check_cuda(cudaMemsetAsync(m.vc, 0, kv_alloc * 2, sv_), "memset");
   const uint64_t rows = static_cast<uint64_t>(m.L) * opts_.max_requests * m.H * opts_.max_ctx;
   if (!encode_tmap_bf16(&m.tm_k, m.kc, rows, m.hd, 16, 64, true) ||
       !encode_tmap_bf16(&m.tm_v, m.vc, rows, m.hd, 16, 64, true))

@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kRowThreads) qkv_epilogue_kernel(const float* 
     *reinterpret_cast<float4*>(qo) = make_float4(qo0[0], qo0[1], qo0[2], qo0[3]);
     *reinterpret_cast<float4*>(qo + half) = make_float4(qo1[0], qo1[1], qo1[2], qo1[3]);
     if (slot >= 0) {
-      const size_t kv = ((((static_cast<size_t>(g.layer) * g.slots + slot) * H + hh) * g.ctx) + pos) * hd + i;
+      const size_t kv = ((((static_cast<size_t>(g.layer) * g.slots + slot) * H + hh) * g.ctx) + pos) * hd;
       auto put4 = [](bf16* dst, float a, float b, float c2, float d) {
         __nv_bfloat162 x = __floats2bfloat162_rn(a, b), y = __floats2bfloat162_rn(c2, d);
         uint2 u;
@@ -457,10 +457,11 @@ __global__ void __launch_bounds__(kRowThreads) qkv_epilogue_kernel(const float* 
         u.y = *reinterpret_cast<uint32_t*>(&y);
         *reinterpret_cast<uint2*>(dst) = u;
       };
-      put4(g.k_cache + kv, ko0[0], ko0[1], ko0[2], ko0[3]);
-      put4(g.k_cache + kv + half, ko1[0], ko1[1], ko1[2], ko1[3]);
-      put4(g.v_cache + kv, v0.x, v0.y, v0.z, v0.w);
-      put4(g.v_cache + kv + half, v1.x, v1.y, v1.z, v1.w);
+      // 4 consecutive dims stay inside one 16-B chunk: swizzle the chunk (kv_swz)
+      put4(g.k_cache + kv + kv_swz(pos, i), ko0[0], ko0[1], ko0[2], ko0[3]);
+      put4(g.k_cache + kv + kv_swz(pos, i + half), ko1[0], ko1[1], ko1[2], ko1[3]);
+      put4(g.v_cache + kv + kv_swz(pos, i), v0.x, v0.y, v0.z, v0.w);
+      put4(g.v_cache + kv + kv_swz(pos, i + half), v1.x, v1.y, v1.z, v1.w);
     }
   }
   ptx::grid_dep_launch();
@@ -712,6 +713,21 @@ void launch_accept(const FwdMeta& m, int n_req, int window, const int32_t* list,
   launch_pdl(accept_kernel, dim3((n_req + per_block - 1) / per_block), dim3(32 * per_block), 0, s, m, n_req, window,
              list, ssm_of_req, amax_val, amax_idx, tiles, T, st, out_accepted, out_bonus, out_committed, out_drafts,
              out_target, emitted);
+}
+
+__global__ void swizzle_kv_kernel(const bf16* __restrict__ src, bf16* __restrict__ dst, int64_t rows, int hd,
+                                  int ctx) {
+  const int64_t total = rows * hd;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / hd;
+    const int d = static_cast<int>(e % hd);
+    dst[r * hd + kv_swz(static_cast<int>(r % ctx), d)] = src[e];
+  }
+}
+
+void launch_swizzle_kv(const bf16* src, bf16* dst, int64_t rows, int hd, int ctx, cudaStream_t s) {
+  swizzle_kv_kernel<<<148 * 8, 256, 0, s>>>(src, dst, rows, hd, ctx);
 }
 
 void launch_init_weights(bf16* w, int64_t rows, int64_t cols, uint64_t stream, float scale, const bf16* emb,

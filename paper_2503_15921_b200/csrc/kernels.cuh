@@ -80,10 +80,17 @@ struct LayerW {
   const bf16 *qkv, *o, *gu, *dn;
 };
 
+// KV cache rows are stored pre-swizzled so that a contiguous range of keys, bulk-copied
+// into shared memory, is already bank-conflict free for ldmatrix: inside every 128-B
+// span of a key row, 16-B chunk c of key position p sits at chunk c ^ (p % 8).
+__host__ __device__ __forceinline__ int kv_swz(int pos, int d) {
+  return (d & ~63) | ((((d >> 3) & 7) ^ (pos & 7)) << 3) | (d & 7);
+}
+
 struct AttnGeom {
   int n_heads, head_dim, slots, ctx, layer;
   float scale;
-  bf16* k_cache;  // [layers][slots][heads][ctx][hd]
+  bf16* k_cache;  // [layers][slots][heads][ctx][hd], rows swizzled by kv_swz (+16 padding rows at the end)
   bf16* v_cache;
 };
 
@@ -117,6 +124,8 @@ void launch_accept(const FwdMeta& m, int n_req, int window, const int32_t* list,
                    int32_t* out_target, unsigned long long* emitted, cudaStream_t s);
 
 // tiled = 1: the GEMM weight layout (gemm.cuh tiled_weight_elems); 0: row-major (embedding).
+// Standard-layout [rows][hd] KV rows -> the swizzled cache layout (kernel tests).
+void launch_swizzle_kv(const bf16* src, bf16* dst, int64_t rows, int hd, int ctx, cudaStream_t s);
 void launch_init_weights(bf16* w, int64_t rows, int64_t cols, uint64_t stream, float scale, const bf16* emb,
                          float planted_g, int64_t vocab, int64_t A_inv, int64_t Cc, int tiled, cudaStream_t s);
 // Row-major [rows][cols] -> tiled GEMM weight layout.
