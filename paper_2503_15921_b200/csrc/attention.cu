@@ -189,9 +189,9 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
           ql[nt][kt][hh] = pack_bf2(x - hx, y - hy);
         }
       }
-      float o[NR];
+      float o[NR], olo[NR];
 #pragma unroll
-      for (int i = 0; i < NR; ++i) o[i] = 0.f;
+      for (int i = 0; i < NR; ++i) o[i] = olo[i] = 0.f;
       float mrun[NQT][2], lsum[NQT][2];
 #pragma unroll
       for (int nt = 0; nt < NQT; ++nt) mrun[nt][0] = mrun[nt][1] = -INFINITY, lsum[nt][0] = lsum[nt][1] = 0.f;
@@ -202,19 +202,29 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
         ptx::mbar_wait(&bar[st], static_cast<uint32_t>((consumed / S) & 1));
         const uint32_t kb = ptx::smem_u32(ring + st * C::kStage);
         const uint32_t vb = kb + C::kHalf;
-        // ---- S^T = K Q^T : 16 keys x 8 queries per n-tile
+        // ---- S^T = K Q^T : 16 keys x 8 queries per n-tile. Four independent accumulator
+        // chains (k-step parity x hi/lo plane) keep the mma.sync pipeline full; summed at the end.
         float s[NQT][4];
+        {
+          float sc[NQT][4][4];
 #pragma unroll
-        for (int nt = 0; nt < NQT; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+          for (int nt = 0; nt < NQT; ++nt)
 #pragma unroll
-        for (int kt = 0; kt < DT; ++kt) {
-          uint32_t a[4];
-          ldsm_x4(kb + kvoff<HD>((lane & 7) + ((lane >> 3) & 1) * 8, 2 * kt + (lane >> 4), ph.tok0), a);
+            for (int c = 0; c < 4; ++c) sc[nt][c][0] = sc[nt][c][1] = sc[nt][c][2] = sc[nt][c][3] = 0.f;
 #pragma unroll
-          for (int nt = 0; nt < NQT; ++nt) {
-            mma16816(s[nt], a, qh[nt][kt][0], qh[nt][kt][1]);
-            mma16816(s[nt], a, ql[nt][kt][0], ql[nt][kt][1]);
+          for (int kt = 0; kt < DT; ++kt) {
+            uint32_t a[4];
+            ldsm_x4(kb + kvoff<HD>((lane & 7) + ((lane >> 3) & 1) * 8, 2 * kt + (lane >> 4), ph.tok0), a);
+#pragma unroll
+            for (int nt = 0; nt < NQT; ++nt) {
+              mma16816(sc[nt][kt & 1], a, qh[nt][kt][0], qh[nt][kt][1]);
+              mma16816(sc[nt][2 + (kt & 1)], a, ql[nt][kt][0], ql[nt][kt][1]);
+            }
           }
+#pragma unroll
+          for (int nt = 0; nt < NQT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) s[nt][e] = (sc[nt][0][e] + sc[nt][1][e]) + (sc[nt][2][e] + sc[nt][3][e]);
         }
         // ---- mask + online softmax per query column (keys gq, gq+8; queries 2cq, 2cq+1)
         const int key0 = ph.tok0 + t * 16 + gq;
@@ -247,6 +257,8 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
           for (int dt = 0; dt < DT; ++dt) {
             float* oo = o + (nt * DT + dt) * 4;
             oo[0] *= corr[0], oo[1] *= corr[1], oo[2] *= corr[0], oo[3] *= corr[1];
+            float* ol = olo + (nt * DT + dt) * 4;
+            ol[0] *= corr[0], ol[1] *= corr[1], ol[2] *= corr[0], ol[3] *= corr[1];
           }
           // P^T as the B operand: movmatrix turns the (key g, queries 2c..2c+1)
           // accumulator pairs into (query g, keys 2c..2c+1) fragments
@@ -257,16 +269,15 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
           pl_[nt][0] = movm_t(pack_bf2(s[nt][0] - h0, s[nt][1] - h1));
           pl_[nt][1] = movm_t(pack_bf2(s[nt][2] - h2, s[nt][3] - h3));
         }
-        // ---- O^T += V^T P^T
+        // ---- O^T += V^T P^T (the lo plane accumulates into its own registers: no serial chain)
 #pragma unroll
         for (int dt = 0; dt < DT; ++dt) {
           uint32_t a[4];
           ldsm_x4_t(vb + kvoff<HD>((lane & 7) + ((lane >> 4) & 1) * 8, 2 * dt + ((lane >> 3) & 1), ph.tok0), a);
 #pragma unroll
           for (int nt = 0; nt < NQT; ++nt) {
-            float* oo = o + (nt * DT + dt) * 4;
-            mma16816(oo, a, ph_[nt][0], ph_[nt][1]);
-            mma16816(oo, a, pl_[nt][0], pl_[nt][1]);
+            mma16816(o + (nt * DT + dt) * 4, a, ph_[nt][0], ph_[nt][1]);
+            mma16816(olo + (nt * DT + dt) * 4, a, pl_[nt][0], pl_[nt][1]);
           }
         }
         ++consumed;
@@ -274,6 +285,8 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
         try_issue();
       }
 
+#pragma unroll
+      for (int i = 0; i < NR; ++i) o[i] += olo[i];
       // ---- piece epilogue: column sums, then the output (single piece) or a split-KV partial
 #pragma unroll
       for (int nt = 0; nt < NQT; ++nt)
