@@ -118,7 +118,17 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
     ptx::fence_mbar_init();
   }
   __syncwarp();
-  ptx::grid_dep_wait();
+  // w.early (verify / draft forwards, where a request's only new KV rows are its query
+  // positions): the work list (meta_kernel) and the KV rows older than the queries are
+  // complete before this grid starts (every kernel of the chain waits on its predecessor
+  // before triggering us), so pieces are staged and those K/V tiles issued BEFORE the
+  // dependency wait; only q and the tiles holding this forward's new keys wait for the
+  // projection kernel. Extends (virtual requests reading keys written earlier in the
+  // same forward) wait first.
+  const bool stamp = w.st != nullptr && threadIdx.x == 0;
+  if (stamp) w.st[4 * blockIdx.x] = ptx::globaltimer();
+  bool dep_done = false;
+  if (!w.early) ptx::grid_dep_wait(), dep_done = true;
   if (item >= n_items * H) return;
   const int head = item % H, rc = item / H;
   const int p_lo = m.item_ptr[rc], p_hi = m.item_ptr[rc + 1];
@@ -143,6 +153,7 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
           ++ik, it = 0;
           continue;
         }
+        if (!dep_done && ph.tok0 + it * 16 + 16 > ph.kvlen - ph.qlen) break;
         if (lane == 0) {
           const int st = issued % S;
           uint8_t* dst = ring + st * C::kStage;
@@ -158,6 +169,12 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
       }
     };
     try_issue();
+    if (!dep_done) {
+      ptx::grid_dep_wait();
+      dep_done = true;
+      if (stamp) w.st[4 * blockIdx.x + 1] = ptx::globaltimer();
+      try_issue();
+    }
 
     for (int k = 0; k < np; ++k) {
       const Piece ph = pcs[k];
@@ -380,6 +397,7 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
       }
     }
   }
+  if (stamp) w.st[4 * blockIdx.x + 3] = ptx::globaltimer();
   ptx::grid_dep_launch();
 }
 
@@ -394,6 +412,12 @@ void launch_t(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m
     configured = true;
   }
   const int n_items = n_rows * std::max(1, w.chunks);
+  static const int early = [] {
+    const char* e = std::getenv("SPIN_ATTN_EARLY");  // experiments only: 0 disables
+    return e ? std::atoi(e) : 1;
+  }();
+  AttnWork wk = w;
+  wk.early = w.early && early;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -404,7 +428,7 @@ void launch_t(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m
   cfg.gridDim = dim3((n_items * g.n_heads + kNW - 1) / kNW);  // one warp per (row, chunk, head)
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::kTotal;
-  cudaLaunchKernelEx(&cfg, attn_kernel<HD, NQT>, tm_k, tm_v, m, g, q, w, out, n_items);
+  cudaLaunchKernelEx(&cfg, attn_kernel<HD, NQT>, tm_k, tm_v, m, g, q, wk, out, n_items);
 }
 
 template <int HD>
@@ -416,6 +440,10 @@ void launch_hd(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& 
 }
 
 }  // namespace
+
+int attn_ctas(int n_rows, int chunks, int heads) {
+  return (n_rows * std::max(1, chunks) * heads + kNW - 1) / kNW;
+}
 
 int attn_chunks(int rows, int heads, int num_sms) {
   // ~8 warps of work per SM (2 CTAs x 4 warps): rows x chunks x heads ~= 8 x SMs

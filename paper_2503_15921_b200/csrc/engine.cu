@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -84,7 +86,7 @@ struct Engine::RoundPlan {
 };
 
 // ------------------------------------------------------------------ models
-void Engine::init_model(ModelDev& m, const spin_model_desc& d) {
+void Engine::init_model(ModelDev& m, const spin_model_desc& d, bool draft) {
   m.d = d;
   m.D = d.d_model, m.H = d.n_heads, m.hd = d.head_dim, m.F = d.ffn, m.V = d.vocab, m.L = d.n_layers;
   const size_t D = m.D, F = m.F, V = m.V;
@@ -132,6 +134,22 @@ void Engine::init_model(ModelDev& m, const spin_model_desc& d) {
                         1, sv_);
   }
   check_cuda(cudaGetLastError(), "init weights");
+  // SSMs on the fused draft path also keep unit-contiguous slab copies (draft.cu)
+  if (draft && draft_fused_ && draft_fused_supported(m.D, m.H, m.hd, m.F, 1)) {
+    const size_t sq = draft_slab_elems(3 * D, D), so = draft_slab_elems(D, D);
+    const size_t sg = draft_slab_elems(2 * F, D), sd = draft_slab_elems(D, F);
+    check_cuda(cudaMalloc(&m.sbuf, (sq + so + sg + sd) * m.L * 2), "draft slabs");
+    m.weight_bytes += (sq + so + sg + sd) * m.L * 2;
+    bf16* q = m.sbuf;
+    for (int l = 0; l < m.L; ++l) {
+      LayerW& w = m.layers[l];
+      launch_slab_weights(w.qkv, q, kDpQkv, 3 * D, D, m.hd, sv_), w.sqkv = q, q += sq;
+      launch_slab_weights(w.o, q, kDpResid, D, D, m.hd, sv_), w.so = q, q += so;
+      launch_slab_weights(w.gu, q, kDpGateUp, 2 * F, D, m.hd, sv_), w.sgu = q, q += sg;
+      launch_slab_weights(w.dn, q, kDpResid, D, F, m.hd, sv_), w.sdn = q, q += sd;
+    }
+    check_cuda(cudaGetLastError(), "draft slabs");
+  }
   // KV cache [layer][slot][head][ctx][hd], zero-filled.
   const size_t kv = static_cast<size_t>(m.L) * opts_.max_requests * m.H * opts_.max_ctx * m.hd;
   // + 16 padding rows: a 16-key tile starting near the end of the last context stays in bounds
@@ -202,6 +220,7 @@ void Engine::init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool l
   ln.q = dalloc<float>(A, static_cast<size_t>(T_cap) * m.D);
   ln.attn = dalloc<bf16>(A, static_cast<size_t>(T_cap) * m.D);
   ln.act = dalloc<bf16>(A, static_cast<size_t>(T_cap) * m.F);
+  ln.ssp = dalloc<float>(A, static_cast<size_t>(m.D / 16 + 1) * std::min(T_cap, kDraftMaxT));
   size_t part = 0;
   const int shapes[4][2] = {{3 * m.D, m.D}, {m.D, m.D}, {2 * m.F, m.D}, {m.D, m.F}};
   for (auto& sh : shapes) {
@@ -260,17 +279,22 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
   const float eps = m.d.rms_eps;
   const int base = (&m == &target_) ? kProfTargetGemm : kProfSsmGemm;  // + {0 gemm, 1 head, 2 attn, 3 epi}
   auto gemm_bytes = [&](int n_out, int k) { return 2.0 * n_out * k + 2.0 * T * k + 2.0 * T * n_out; };
+  AttnGeom g{m.H, m.hd, opts_.max_requests, opts_.max_ctx, 0, static_cast<float>(1.0 / std::sqrt(double(m.hd))),
+             m.kc, m.vc};
+  if (m.sbuf != nullptr && head_mode != 2 && draft_fused_supported(D, m.H, m.hd, F, T)) {
+    forward_draft(m, ln, sh, g, s, head_mode);
+    return;
+  }
   prof_begin(base + 3, s);
   launch_embed_norm(m.emb, ln.meta, T, D, eps, ln.h, ln.xn, s);
   prof_end(s, 0);
-  AttnGeom g{m.H, m.hd, opts_.max_requests, opts_.max_ctx, 0, static_cast<float>(1.0 / std::sqrt(double(m.hd))),
-             m.kc, m.vc};
   GemmEpilogue ep;
   ep.mode = kGemmPartial;
   ep.part = ln.part;
   AttnWork aw = ln.aw;
   aw.qmax = sh.qmax;
   aw.chunks = attn_chunks(sh.rows, m.H, num_sms_);
+  aw.early = sh.early;
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = m.layers[l];
     g.layer = l;
@@ -320,6 +344,116 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
   check_cuda(cudaGetLastError(), "forward launch");
 }
 
+// Draft-step forward of an SSM over few rows (draft.cu): five launches per layer,
+// epilogues inside the projections, RMSNorm folded into the consumers.
+void Engine::forward_draft(ModelDev& m, Lane& ln, const FwdShape& sh, AttnGeom g, cudaStream_t s, int head_mode) {
+  const int T = sh.T, D = m.D, F = m.F;
+  const float eps = m.d.rms_eps;
+  const int base = kProfSsmGemm;
+  auto wbytes = [&](int n_out, int k) { return 2.0 * n_out * k + 2.0 * T * k + 2.0 * T * n_out; };
+  prof_begin(base + 3, s);
+  launch_embed_ss(m.emb, ln.meta, T, D, ln.h, ln.ssp, s);
+  prof_end(s, 0);
+  int n_ssp = 1;
+  AttnWork aw = ln.aw;
+  aw.qmax = sh.qmax;
+  aw.chunks = attn_chunks(sh.rows, m.H, num_sms_);
+  aw.early = sh.early;
+  DraftProj a{};
+  a.T = T;
+  a.eps = eps;
+  a.row_slot = ln.meta.row_slot;
+  a.row_pos = ln.meta.row_pos;
+  a.rcos = m.rcos;
+  a.rsin = m.rsin;
+  a.h = ln.h;
+  a.q = ln.q;
+  a.act = ln.act;
+  static const int skip = [] {  // timing experiments only: skip kernels (results invalid)
+    const char* e = std::getenv("SPIN_DRAFT_SKIP");
+    return e ? std::atoi(e) : 0;
+  }();
+  for (int l = 0; l < m.L; ++l) {
+    const LayerW& w = m.layers[l];
+    g.layer = l;
+    a.g = g;
+    a.mode = kDpQkv, a.w = w.sqkv, a.n_out = 3 * D, a.K = D, a.ssp = ln.ssp, a.n_ssp = n_ssp;
+    if (!(skip & 2)) {
+      prof_begin(base, s);
+      a.st = stamp_slot(0, draft_proj_units(a));
+      check_cuda(launch_draft_proj(a, s), "draft qkv");
+      prof_end(s, wbytes(3 * D, D));
+    }
+    if (!(skip & 1)) {
+      prof_begin(base + 2, s);
+      aw.st = stamp_slot(1, attn_ctas(sh.rows, aw.chunks, m.H));
+      launch_attention(m.tm_k, m.tm_v, ln.meta, sh.rows, sh.R, g, ln.q, aw, ln.attn, s);
+      prof_end(s, 0);
+    }
+    a.mode = kDpResid, a.w = w.so, a.n_out = D, a.K = D, a.x = ln.attn, a.ssp_out = ln.ssp;
+    if (!(skip & 4)) {
+      prof_begin(base, s);
+      a.st = stamp_slot(2, draft_proj_units(a));
+      check_cuda(launch_draft_proj(a, s), "draft o");
+      prof_end(s, wbytes(D, D));
+    }
+    n_ssp = D / 16;
+    a.mode = kDpGateUp, a.w = w.sgu, a.n_out = 2 * F, a.K = D, a.ssp = ln.ssp, a.n_ssp = n_ssp;
+    if (!(skip & 8)) {
+      prof_begin(base, s);
+      a.st = stamp_slot(3, draft_proj_units(a));
+      check_cuda(launch_draft_proj(a, s), "draft gate_up");
+      prof_end(s, wbytes(2 * F, D));
+    }
+    a.mode = kDpResid, a.w = w.sdn, a.n_out = D, a.K = F, a.x = ln.act, a.ssp_out = ln.ssp;
+    if (!(skip & 16)) {
+      prof_begin(base, s);
+      a.st = stamp_slot(4, draft_proj_units(a));
+      check_cuda(launch_draft_proj(a, s), "draft down");
+      prof_end(s, wbytes(D, F));
+    }
+  }
+  if (head_mode > 0) {
+    prof_begin(base + 3, s);
+    launch_norm_ss(ln.h, ln.ssp, n_ssp, T, D, eps, ln.xn, s);
+    prof_end(s, 0);
+    GemmEpilogue eh;
+    eh.mode = kGemmArgmax;
+    eh.amax_val = ln.amax_val;
+    eh.amax_idx = ln.amax_idx;
+    prof_begin(base + 1, s);
+    check_cuda(gemm_launch(plan(m.V, D, T, kGemmArgmax), m.head, ln.xn, eh, s, opts_.use_pdl != 0),
+               "gemm lm_head");
+    prof_end(s, wbytes(m.V, D));
+  }
+  check_cuda(cudaGetLastError(), "draft forward launch");
+}
+
+unsigned long long* Engine::stamp_slot(int kind, int ctas) {
+  if (!stamps_ || stamp_used_ + size_t(4) * ctas > stamp_cap_) return nullptr;
+  stamp_tab_.push_back({kind, ctas, static_cast<int>(stamp_used_)});
+  unsigned long long* p = stamps_ + stamp_used_;
+  stamp_used_ += size_t(4) * ctas;
+  return p;
+}
+
+void Engine::dump_stamps() {
+  if (!stamps_ || stamp_tab_.empty()) return;
+  std::vector<unsigned long long> h(stamp_used_);
+  check_cuda(cudaMemcpy(h.data(), stamps_, stamp_used_ * 8, cudaMemcpyDeviceToHost), "stamps");
+  FILE* f = std::fopen(stamp_path_.c_str(), "w");
+  if (!f) return;
+  std::fprintf(f, "launch,kind,cta,t0,t1,t2,t3\n");
+  for (size_t l = 0; l < stamp_tab_.size(); ++l) {
+    const auto& e = stamp_tab_[l];
+    for (int c = 0; c < e[1]; ++c) {
+      const unsigned long long* t = h.data() + e[2] + 4 * c;
+      std::fprintf(f, "%zu,%d,%d,%llu,%llu,%llu,%llu\n", l, e[0], c, t[0], t[1], t[2], t[3]);
+    }
+  }
+  std::fclose(f);
+}
+
 // ------------------------------------------------------------------ engine
 Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n_ssm, const spin_engine_opts& opts)
     : opts_(opts) {
@@ -335,12 +469,19 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
   check_cuda(cudaSetDevice(opts.device), "cudaSetDevice");
   (void)cudaGetLastError();  // drop a stale non-sticky error left by an earlier caller
   cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, opts.device);
+  if (const char* e = std::getenv("SPIN_DRAFT_FUSED")) draft_fused_ = std::atoi(e) != 0;  // A/B switch
+  if (const char* e = std::getenv("SPIN_STAMPS")) {
+    stamp_path_ = e;
+    stamp_cap_ = size_t(8) << 20;
+    check_cuda(cudaMalloc(&stamps_, stamp_cap_ * 8), "stamps");
+    check_cuda(cudaMemset(stamps_, 0, stamp_cap_ * 8), "stamps");
+  }
   check_cuda(cudaStreamCreateWithFlags(&sv_, cudaStreamNonBlocking), "stream");
   ss_.resize(n_ssm);
   for (auto& s : ss_) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-  init_model(target_, target);
+  init_model(target_, target, false);
   ssm_.resize(n_ssm);
-  for (int j = 0; j < n_ssm; ++j) init_model(ssm_[j], ssms[j]);
+  for (int j = 0; j < n_ssm; ++j) init_model(ssm_[j], ssms[j], true);
   const int R = opts.max_requests, W = opts.window;
   init_lane(tlane_, target_, std::max(R * (W + 1), kExtendRows), std::max(R, kExtendRows), opts.debug_logits != 0);
   slane_.resize(n_ssm);
@@ -388,7 +529,7 @@ Engine::~Engine() {
     if (kv.second->graph) cudaGraphDestroy(kv.second->graph);
   }
   auto free_model = [](ModelDev& m) {
-    cudaFree(m.wbuf), cudaFree(m.kc), cudaFree(m.vc), cudaFree(m.rcos), cudaFree(m.rsin);
+    cudaFree(m.wbuf), cudaFree(m.sbuf), cudaFree(m.kc), cudaFree(m.vc), cudaFree(m.rcos), cudaFree(m.rsin);
   };
   free_model(target_);
   for (auto& m : ssm_) free_model(m);
@@ -397,6 +538,7 @@ Engine::~Engine() {
     for (void* p : l.allocs) cudaFree(p);
   cudaFree(st_.tokens), cudaFree(st_.committed), cudaFree(st_.ssm_len), cudaFree(st_.drafts);
   for (void* p : plan_tables_) cudaFree(p);
+  if (stamps_) cudaFree(stamps_);
   cudaFreeHost(pin_in_), cudaFreeHost(pin_out_), cudaFree(d_in_), cudaFree(d_out_), cudaFree(d_emitted_);
   cudaEventDestroy(ev_fork_), cudaEventDestroy(ev_start_), cudaEventDestroy(ev_draft_), cudaEventDestroy(ev_end_);
   for (auto& e : ev_join_) cudaEventDestroy(e);
@@ -567,6 +709,8 @@ void Engine::record_timing(cudaEvent_t ev, cudaStream_t s) {
 void Engine::capture_round(RoundPlan& p) {
   const int W = opts_.window, M = static_cast<int>(ssm_.size());
   const int64_t launches_before = launches_;
+  stamp_used_ = 0;
+  stamp_tab_.clear();
   cudaStream_t s = sv_;
   record_timing(ev_start_, s);
   check_cuda(cudaMemcpyAsync(d_in_, pin_in_, p.in_ints * 4, cudaMemcpyHostToDevice, s), "h2d lists");
@@ -590,7 +734,7 @@ void Engine::capture_round(RoundPlan& p) {
       prof_begin(kProfMeta, sj);
       launch_meta(a, st_, ln.meta, sj);
       prof_end(sj, 0);
-      forward(m, ln, FwdShape{2 * nj, nj, nj, 2}, sj, 1);
+      forward(m, ln, FwdShape{2 * nj, nj, nj, 2, 1}, sj, 1);
       int prev_t = 2 * nj, prev_q = 2;
       for (int k = 1; k <= W; ++k) {
         MetaArgs b{};
@@ -609,7 +753,7 @@ void Engine::capture_round(RoundPlan& p) {
         prof_begin(kProfMeta, sj);
         launch_meta(b, st_, ln.meta, sj);
         prof_end(sj, 0);
-        if (k < W) forward(m, ln, FwdShape{nj, nj, nj, 1}, sj, 1);
+        if (k < W) forward(m, ln, FwdShape{nj, nj, nj, 1, 1}, sj, 1);
         prev_t = nj, prev_q = 1;
       }
     }
@@ -632,7 +776,7 @@ void Engine::capture_round(RoundPlan& p) {
     prof_begin(kProfMeta, s);
     launch_meta(a, st_, tlane_.meta, s);
     prof_end(s, 0);
-    forward(target_, tlane_, FwdShape{T, n, a.padded ? n : width, W + 1}, s, opts_.debug_logits ? 2 : 1);
+    forward(target_, tlane_, FwdShape{T, n, a.padded ? n : width, W + 1, 1}, s, opts_.debug_logits ? 2 : 1);
     int32_t* o = d_out_;
     prof_begin(kProfMeta, s);
     launch_accept(tlane_.meta, n, W, d_in_ + p.off_list, d_in_ + p.off_ssm_of, tlane_.amax_val, tlane_.amax_idx,
@@ -687,6 +831,7 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, spin_roun
     capture_round(p);
   }
   check_cuda(cudaStreamSynchronize(sv_), "round");
+  dump_stamps();
   float draft_ms = 0.f, total_ms = 0.f;
   check_cuda(cudaEventElapsedTime(&draft_ms, ev_start_, ev_draft_), "event timing");
   check_cuda(cudaEventElapsedTime(&total_ms, ev_start_, ev_end_), "event timing");
@@ -950,7 +1095,7 @@ void Engine::verify_bench(int n, const int32_t* slots, const int32_t* draft_lens
   check_cuda(cudaStreamBeginCapture(sv_, cudaStreamCaptureModeRelaxed), "capture");
   capturing_ = true;
   launch_meta(a, st_, ln.meta, sv_);
-  forward(target_, ln, FwdShape{T, n, packed ? width : n, qmax}, sv_, opts_.debug_logits ? 2 : 1);
+  forward(target_, ln, FwdShape{T, n, packed ? width : n, qmax, 1}, sv_, opts_.debug_logits ? 2 : 1);
   capturing_ = false;
   check_cuda(cudaStreamEndCapture(sv_, &graph), "capture");
   check_cuda(cudaGraphInstantiate(&exec, graph, 0), "instantiate");

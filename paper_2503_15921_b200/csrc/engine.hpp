@@ -3,7 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <map>
+#include <string>
 #include <memory>
 #include <tuple>
 #include <vector>
@@ -19,6 +21,7 @@ struct ModelDev {
   spin_model_desc d{};
   int D = 0, H = 0, hd = 0, F = 0, V = 0, L = 0;
   bf16* wbuf = nullptr;
+  bf16* sbuf = nullptr;  // draft-path slab copies of the layer weights (SSMs)
   bf16* emb = nullptr;
   bf16* head = nullptr;
   std::vector<LayerW> layers;
@@ -37,6 +40,7 @@ struct Lane {
   float* h = nullptr;
   bf16 *xn = nullptr, *attn = nullptr, *act = nullptr;
   float* q = nullptr;
+  float* ssp = nullptr;  // draft path: per-unit sums of squares of h [D / 16][T]
   float* part = nullptr;
   AttnWork aw{};
   float* amax_val = nullptr;
@@ -61,6 +65,10 @@ enum ProfCat : int {
 
 struct FwdShape {
   int T, R, rows, qmax;
+  // 1: every request's new KV rows are exactly its query positions (verify, draft
+  // steps), so attention may fetch older keys before the projection completes; 0 for
+  // extends, whose virtual requests read keys written earlier in the same forward.
+  int early = 0;
 };
 
 class Engine {
@@ -87,9 +95,20 @@ class Engine {
 
  private:
   struct RoundPlan;
-  void init_model(ModelDev& m, const spin_model_desc& d);
+  void init_model(ModelDev& m, const spin_model_desc& d, bool draft);
   void init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool logits);
   void forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, int head_mode);
+  void forward_draft(ModelDev& m, Lane& ln, const FwdShape& sh, AttnGeom g, cudaStream_t s, int head_mode);
+  bool draft_fused_ = true;
+  // SPIN_STAMPS=<csv path>: per-CTA globaltimer stamps of the draft kernels, dumped after
+  // every round (launch, kind, cta, start, after-wait, after-main-loop, end) -- a
+  // profiling aid for latency-bound kernel chains.
+  unsigned long long* stamps_ = nullptr;
+  size_t stamp_cap_ = 0, stamp_used_ = 0;
+  std::vector<std::array<int, 3>> stamp_tab_;  // kind, ctas, offset
+  std::string stamp_path_;
+  unsigned long long* stamp_slot(int kind, int ctas);
+  void dump_stamps();
   void extend(int model, const std::vector<std::tuple<int, int, int>>& ranges);  // (slot, from, to)
   RoundPlan& plan_round(int n, const int32_t* slots, const int32_t* ssm_of);
   void capture_round(RoundPlan& p);

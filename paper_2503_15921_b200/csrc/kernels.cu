@@ -15,18 +15,33 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // Fixed-order sum of the stream-K partial slots of 4 consecutive features
 // (slot 0..np-1, deterministic); np comes from the plan's host-built piece table.
+// The first kUnrollPieces partial loads are predicated rather than looped so that a
+// caller summing several groups has all of their loads in flight at once.
+constexpr int kUnrollPieces = 4;
 __device__ __forceinline__ float4 sum_pieces4(const float* __restrict__ part, const PieceMap& pm, int T, int n_out,
                                               int t, int n) {
   const int np = pm.tile_pieces(t, n);
   const size_t stride = static_cast<size_t>(T) * n_out;
   const float* p = part + static_cast<size_t>(t) * n_out + n;
-  float4 acc = __ldg(reinterpret_cast<const float4*>(p));
-  for (int s = 1; s < np; ++s) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(p + s * stride));
-    acc.x = __fadd_rn(acc.x, v.x);
-    acc.y = __fadd_rn(acc.y, v.y);
-    acc.z = __fadd_rn(acc.z, v.z);
-    acc.w = __fadd_rn(acc.w, v.w);
+  float4 v[kUnrollPieces];
+#pragma unroll
+  for (int s = 0; s < kUnrollPieces; ++s)
+    if (s < np) v[s] = __ldg(reinterpret_cast<const float4*>(p + s * stride));
+  float4 acc = v[0];
+#pragma unroll
+  for (int s = 1; s < kUnrollPieces; ++s)
+    if (s < np) {
+      acc.x = __fadd_rn(acc.x, v[s].x);
+      acc.y = __fadd_rn(acc.y, v[s].y);
+      acc.z = __fadd_rn(acc.z, v[s].z);
+      acc.w = __fadd_rn(acc.w, v[s].w);
+    }
+  for (int s = kUnrollPieces; s < np; ++s) {
+    const float4 w = __ldg(reinterpret_cast<const float4*>(p + s * stride));
+    acc.x = __fadd_rn(acc.x, w.x);
+    acc.y = __fadd_rn(acc.y, w.y);
+    acc.z = __fadd_rn(acc.z, w.z);
+    acc.w = __fadd_rn(acc.w, w.w);
   }
   return acc;
 }
@@ -372,24 +387,68 @@ __global__ void __launch_bounds__(kRowThreads) embed_norm_kernel(const bf16* __r
   rmsnorm_row(s_row, D, eps, xn + static_cast<size_t>(t) * D, red);
 }
 
-// h += sum of the stream-K partials; xn = bf16(rmsnorm(h)). 4 features / thread.
+// h += sum of the stream-K partials; xn = bf16(rmsnorm(h)). Each thread owns up to
+// kNormVec float4 groups of the row (D <= 8192) and keeps them in registers: every
+// partial / residual load of a piece round is issued before any add or store, so the
+// row costs max_pieces L2 round trips instead of one per group.
+constexpr int kNormVec = 8;
 __global__ void __launch_bounds__(kRowThreads) resid_norm_kernel(const float* __restrict__ part, PieceMap pm, int T,
-                                                                 int D, float eps, float* h, bf16* xn) {
-  extern __shared__ float s_row[];
+                                                                 int D, float eps, float* __restrict__ h,
+                                                                 bf16* __restrict__ xn) {
   __shared__ float red[32];
   ptx::grid_dep_wait();
   const int t = blockIdx.x;
-  for (int i = 4 * threadIdx.x; i < D; i += 4 * kRowThreads) {
-    float4* hp = reinterpret_cast<float4*>(h + static_cast<size_t>(t) * D + i);
-    const float4 y = sum_pieces4(part, pm, T, D, t, i);
-    float4 v = *hp;
-    v.x = __fadd_rn(v.x, y.x), v.y = __fadd_rn(v.y, y.y), v.z = __fadd_rn(v.z, y.z), v.w = __fadd_rn(v.w, y.w);
-    *hp = v;
-    *reinterpret_cast<float4*>(s_row + i) = v;
+  const size_t stride = static_cast<size_t>(T) * D;
+  const float* prow = part + static_cast<size_t>(t) * D;
+  float4* hrow = reinterpret_cast<float4*>(h + static_cast<size_t>(t) * D);
+  float4 v[kNormVec], y[kNormVec];
+  int np[kNormVec];
+  int maxp = 0;
+#pragma unroll
+  for (int k = 0; k < kNormVec; ++k) {
+    const int i = 4 * (threadIdx.x + k * kRowThreads);
+    np[k] = i < D ? pm.tile_pieces(t, i) : 0;
+    maxp = max(maxp, np[k]);
+    if (i < D) {
+      v[k] = hrow[i >> 2];
+      y[k] = __ldg(reinterpret_cast<const float4*>(prow + i));
+    }
   }
-  __syncthreads();
+  for (int s = 1; s < maxp; ++s) {
+    float4 z[kNormVec];
+#pragma unroll
+    for (int k = 0; k < kNormVec; ++k)
+      if (s < np[k]) z[k] = __ldg(reinterpret_cast<const float4*>(prow + s * stride + 4 * (threadIdx.x + k * kRowThreads)));
+#pragma unroll
+    for (int k = 0; k < kNormVec; ++k)
+      if (s < np[k]) {
+        y[k].x = __fadd_rn(y[k].x, z[k].x), y[k].y = __fadd_rn(y[k].y, z[k].y);
+        y[k].z = __fadd_rn(y[k].z, z[k].z), y[k].w = __fadd_rn(y[k].w, z[k].w);
+      }
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kNormVec; ++k) {
+    if (np[k] == 0) continue;
+    v[k].x = __fadd_rn(v[k].x, y[k].x), v[k].y = __fadd_rn(v[k].y, y[k].y);
+    v[k].z = __fadd_rn(v[k].z, y[k].z), v[k].w = __fadd_rn(v[k].w, y[k].w);
+    hrow[threadIdx.x + k * kRowThreads] = v[k];
+    ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+  }
   ptx::grid_dep_launch();
-  rmsnorm_row(s_row, D, eps, xn + static_cast<size_t>(t) * D, red);
+  const float tot = block_sum(ss, red);
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(tot, static_cast<float>(D)), eps)));
+  bf16* xrow = xn + static_cast<size_t>(t) * D;
+#pragma unroll
+  for (int k = 0; k < kNormVec; ++k) {
+    if (np[k] == 0) continue;
+    __nv_bfloat162 a = __floats2bfloat162_rn(__fmul_rn(v[k].x, inv), __fmul_rn(v[k].y, inv));
+    __nv_bfloat162 b = __floats2bfloat162_rn(__fmul_rn(v[k].z, inv), __fmul_rn(v[k].w, inv));
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(xrow + 4 * (threadIdx.x + k * kRowThreads)) = u;
+  }
 }
 
 // grid (T, ceil(F / 1024)): 4 SwiGLU outputs per thread.
@@ -417,7 +476,7 @@ __global__ void __launch_bounds__(kRowThreads) swiglu_kernel(const float* __rest
 // Split-K reduction of the fused QKV projection, RoPE (rotate-half) on q and k,
 // q -> fp32 (feeds only the CUDA-core attention), k/v -> bf16 KV cache at
 // (layer, slot, head, pos). grid (T, ceil(H*hd/2 / 1024)): 4 rotary pairs / thread.
-__global__ void __launch_bounds__(kRowThreads) qkv_epilogue_kernel(const float* __restrict__ part, PieceMap pm,
+__global__ void __launch_bounds__(kRowThreads, 1) qkv_epilogue_kernel(const float* __restrict__ part, PieceMap pm,
                                                                    FwdMeta m, int T, AttnGeom g,
                                                                    const float* __restrict__ rcos,
                                                                    const float* __restrict__ rsin, float* q) {
@@ -697,7 +756,7 @@ void launch_qkv_epilogue(const float* part, const PieceMap& pm, const FwdMeta& m
 
 void launch_resid_norm(const float* part, const PieceMap& pm, int T, int D, float eps, float* h, bf16* xn,
                        cudaStream_t s) {
-  launch_pdl(resid_norm_kernel, dim3(T), dim3(kRowThreads), D * sizeof(float), s, part, pm, T, D, eps, h, xn);
+  launch_pdl(resid_norm_kernel, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, D, eps, h, xn);
 }
 
 void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* act, cudaStream_t s) {

@@ -78,6 +78,7 @@ struct MetaArgs {
 
 struct LayerW {
   const bf16 *qkv, *o, *gu, *dn;
+  const bf16 *sqkv = nullptr, *so = nullptr, *sgu = nullptr, *sdn = nullptr;  // draft slabs (SSMs)
 };
 
 // KV cache rows are stored pre-swizzled so that a contiguous range of keys, bulk-copied
@@ -103,6 +104,40 @@ void launch_resid_norm(const float* part, const PieceMap& pm, int T, int D, floa
                        cudaStream_t s);
 void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* act, cudaStream_t s);
 
+// Fused projections of the draft step (draft.cu): one CTA per 16/32 output rows over
+// the full K, epilogue in the projection, RMSNorm folded into the consumers through
+// per-unit sums of squares ssp[t][unit].
+constexpr int kDraftMaxT = 32;
+enum DraftProjMode : int { kDpQkv = 0, kDpGateUp = 1, kDpResid = 2 };
+struct DraftProj {
+  int mode;
+  const bf16* w;  // slab weights (launch_slab_weights), n_out x K
+  int n_out, K, T;
+  float* h;            // QKV / GATE_UP: fp32 residual input (normalised on load); RESID: residual, updated
+  const float* ssp;    // QKV / GATE_UP: [T][n_ssp] sums of squares of h
+  int n_ssp;
+  float eps;
+  const bf16* x;       // RESID: bf16 input [T][K]
+  float* ssp_out;      // RESID: [T][n_out / 16]
+  float* q;            // QKV: fp32 [T][D], RoPE applied; K/V appended to g's caches
+  AttnGeom g;
+  const int32_t* row_slot;
+  const int32_t* row_pos;
+  const float* rcos;
+  const float* rsin;
+  bf16* act;           // GATE_UP: SwiGLU output [T][n_out / 2]
+  unsigned long long* st;  // optional timeline stamps [CTA][4] (SPIN_STAMPS)
+  int dbg;                 // timing experiments (SPIN_DPROJ_DBG)
+};
+int draft_proj_units(const DraftProj& a);
+// Slab copy of a tiled weight matrix for the draft projections (unit-contiguous).
+size_t draft_slab_elems(int n_out, int K);
+void launch_slab_weights(const bf16* tiled, bf16* slab, int mode, int n_out, int K, int hd, cudaStream_t s);
+bool draft_fused_supported(int D, int H, int hd, int F, int T);
+cudaError_t launch_draft_proj(const DraftProj& a, cudaStream_t s);
+void launch_embed_ss(const bf16* emb, const FwdMeta& m, int T, int D, float* h, float* ssp, cudaStream_t s);
+void launch_norm_ss(const float* h, const float* ssp, int n_ssp, int T, int D, float eps, bf16* xn, cudaStream_t s);
+
 // Packed ragged causal attention over the KV cache (TMA-staged tiles) and the
 // shared-max combine of segment partials.
 struct AttnWork {
@@ -112,7 +147,10 @@ struct AttnWork {
   int32_t* counter;  // [R_cap][H] arrivals per (request, head); zero between launches
   int qmax;
   int chunks;     // chunks per pack row (must equal the MetaArgs.chunks that built the work list)
+  int early = 0;  // issue K/V tiles older than the queries before the dependency wait (FwdShape::early)
+  unsigned long long* st = nullptr;  // optional timeline stamps [CTA][4] (SPIN_STAMPS)
 };
+int attn_ctas(int n_rows, int chunks, int heads);
 // Chunks per pack row so that rows x chunks x heads warps fill the GPU.
 int attn_chunks(int rows, int heads, int num_sms);
 void launch_attention(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m, int n_rows, int n_req,
