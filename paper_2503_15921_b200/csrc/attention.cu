@@ -126,7 +126,9 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
   // projection kernel. Extends (virtual requests reading keys written earlier in the
   // same forward) wait first.
   const bool stamp = w.st != nullptr && threadIdx.x == 0;
-  if (stamp) w.st[4 * blockIdx.x] = ptx::globaltimer();
+  // stamps [CTA][8] (warp 0): start, wait release, first tile ready, q ready, tile loop end,
+  // partial stored, merge start, end
+  if (stamp) w.st[8 * blockIdx.x] = ptx::globaltimer();
   bool dep_done = false;
   if (!w.early) ptx::grid_dep_wait(), dep_done = true;
   if (item >= n_items * H) return;
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
     if (!dep_done) {
       ptx::grid_dep_wait();
       dep_done = true;
-      if (stamp) w.st[4 * blockIdx.x + 1] = ptx::globaltimer();
+      if (stamp) w.st[8 * blockIdx.x + 1] = ptx::globaltimer();
       try_issue();
     }
 
@@ -213,10 +215,12 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
 #pragma unroll
       for (int nt = 0; nt < NQT; ++nt) mrun[nt][0] = mrun[nt][1] = -INFINITY, lsum[nt][0] = lsum[nt][1] = 0.f;
       const int qbase = ph.kvlen - ph.qlen;  // absolute position of query 0
+      if (stamp && k == 0 && pb == p_lo) w.st[8 * blockIdx.x + 3] = ptx::globaltimer() + (qh[0][0][0] == 12345u);
 
       for (int t = 0; t * 16 < ph.len; ++t) {
         const int st = consumed % S;
         ptx::mbar_wait(&bar[st], static_cast<uint32_t>((consumed / S) & 1));
+        if (stamp && consumed == 0) w.st[8 * blockIdx.x + 2] = ptx::globaltimer();
         const uint32_t kb = ptx::smem_u32(ring + st * C::kStage);
         const uint32_t vb = kb + C::kHalf;
         // ---- S^T = K Q^T : 16 keys x 8 queries per n-tile. Four independent accumulator
@@ -304,6 +308,7 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
 
 #pragma unroll
       for (int i = 0; i < NR; ++i) o[i] += olo[i];
+      if (stamp) w.st[8 * blockIdx.x + 4] = ptx::globaltimer();
       // ---- piece epilogue: column sums, then the output (single piece) or a split-KV partial
 #pragma unroll
       for (int nt = 0; nt < NQT; ++nt)
@@ -345,7 +350,9 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
         }
       }
       last = __shfl_sync(kFull, last, 0);
+      if (stamp) w.st[8 * blockIdx.x + 5] = ptx::globaltimer();
       if (!last) continue;
+      if (stamp) w.st[8 * blockIdx.x + 6] = ptx::globaltimer();
       // ---- shared-max merge of the request's pieces in token order (attention.cpp:128-157)
       const int npc = ph.npieces;
       for (int qi = 0; qi < ph.qlen; ++qi) {
@@ -397,8 +404,333 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
       }
     }
   }
-  if (stamp) w.st[4 * blockIdx.x + 3] = ptx::globaltimer();
+  if (stamp) w.st[8 * blockIdx.x + 7] = ptx::globaltimer();
   ptx::grid_dep_launch();
+}
+
+// Few-query (draft step) variant: one CTA per (pack row, chunk, head) item whose four
+// warps take the item's 16-key tiles round robin, so the longest chain is a quarter of
+// a chunk (one ring's worth: a single DRAM round trip) instead of a whole chunk; the
+// warps' partials of each piece are merged in shared memory (fixed warp order), and
+// pieces of multi-piece requests go through the same global last-arriver merge as
+// attn_kernel. NQT = 1 (<= 8 queries per request).
+template <int HD>
+struct DecCfg {
+  using C = Cfg<HD, 1>;
+  static constexpr int kMergeFloats = 8 * (2 + HD);  // per warp: m[8], l[8], o[8][HD]
+  static constexpr size_t kTotal =
+      1024 + C::kRing + kMaxPieces * 64 + kNW * C::kStages * 8 + kNW * kMergeFloats * 4;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGeom g, const float* __restrict__ q,
+                                                               AttnWork w, bf16* __restrict__ out, int n_items) {
+  using C = Cfg<HD, 1>;
+  using DC = DecCfg<HD>;
+  constexpr int S = C::kStages, DT = C::kDT, NR = C::kNR, QP = C::kQP;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int gq = lane >> 2, cq = lane & 3;
+  uint8_t* ring = smem + static_cast<size_t>(warp) * S * C::kStage;
+  Piece* pcs = reinterpret_cast<Piece*>(smem + C::kRing);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::kRing + kMaxPieces * 64) + warp * S;
+  float* mrg = reinterpret_cast<float*>(smem + C::kRing + kMaxPieces * 64 + kNW * S * 8);
+  float* my_m = mrg + warp * DC::kMergeFloats;  // [8]
+  float* my_l = my_m + 8;                        // [8]
+  float* my_o = my_m + 16;                       // [8][HD]
+  const int H = g.n_heads, D = H * HD;
+  const float sl2 = g.scale * kLog2e;
+  const int item = blockIdx.x;  // (pack row, chunk) x head
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) ptx::mbar_init(&bar[s], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncwarp();
+  const bool stamp = w.st != nullptr && threadIdx.x == 0;
+  if (stamp) w.st[8 * blockIdx.x] = ptx::globaltimer();
+  bool dep_done = false;
+  if (!w.early) ptx::grid_dep_wait(), dep_done = true;
+  if (item >= n_items * H) return;  // uniform per CTA
+  const int head = item % H, rc = item / H;
+  const int p_lo = m.item_ptr[rc], p_hi = m.item_ptr[rc + 1];
+  const uint64_t pol = ptx::policy_evict_first();
+  const int kv_base = (g.layer * g.slots) * H;
+
+  int issued = 0, consumed = 0;
+  for (int pb = p_lo; pb < p_hi; pb += kMaxPieces) {
+    const int np = min(p_hi - pb, kMaxPieces);
+    __syncthreads();  // previous pass done with pcs
+    for (int k = threadIdx.x; k < np; k += kThreads) {
+      const int4* src = reinterpret_cast<const int4*>(m.pieces + 16 * (pb + k));
+      int4* dst = reinterpret_cast<int4*>(pcs + k);
+      dst[0] = src[0], dst[1] = src[1], dst[2] = src[2];
+    }
+    __syncthreads();
+    // this warp's tiles: every kNW-th tile of the pass's tile sequence (pieces in order)
+    int ik = 0, it = warp;
+    auto norm_pos = [&]() {
+      while (ik < np && it * 16 >= pcs[ik].len) it -= (pcs[ik].len + 15) / 16, ++ik;
+    };
+    norm_pos();
+    auto try_issue = [&]() {
+      while (issued - consumed < S && ik < np) {
+        const Piece& ph = pcs[ik];
+        if (!dep_done && ph.tok0 + it * 16 + 16 > ph.kvlen - ph.qlen) break;
+        if (lane == 0) {
+          const int st = issued % S;
+          uint8_t* dst = ring + st * C::kStage;
+          const size_t r0 = (static_cast<size_t>(kv_base + ph.slot * H + head) * g.ctx) + ph.tok0 + it * 16;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          ptx::mbar_arrive_expect_tx(&bar[st], C::kStage);
+          ptx::bulk_load(dst, g.k_cache + r0 * HD, C::kHalf, &bar[st], pol);
+          ptx::bulk_load(dst + C::kHalf, g.v_cache + r0 * HD, C::kHalf, &bar[st], pol);
+        }
+        ++issued;
+        it += kNW;
+        norm_pos();
+      }
+    };
+    try_issue();
+    if (!dep_done) {
+      ptx::grid_dep_wait();
+      dep_done = true;
+      if (stamp) w.st[8 * blockIdx.x + 1] = ptx::globaltimer();
+      try_issue();
+    }
+
+    int tile_base = 0;  // first tile index of piece k in the pass's sequence
+    for (int k = 0; k < np; ++k) {
+      const Piece ph = pcs[k];
+      const int n_tiles = (ph.len + 15) / 16;
+      uint32_t qh[DT][2], ql[DT][2];
+      {
+        const int qi = gq;
+        const bool ok = qi < ph.qlen;
+        const float* qr = q + static_cast<size_t>(ph.qs + (ok ? qi : 0)) * D + head * HD + 2 * cq;
+#pragma unroll
+        for (int kt = 0; kt < DT; ++kt)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const float2 v =
+                ok ? __ldg(reinterpret_cast<const float2*>(qr + 16 * kt + 8 * hh)) : make_float2(0.f, 0.f);
+            const float x = v.x * sl2, y = v.y * sl2;
+            const float hx = bf_round(x), hy = bf_round(y);
+            qh[kt][hh] = pack_bf2(hx, hy);
+            ql[kt][hh] = pack_bf2(x - hx, y - hy);
+          }
+      }
+      float o[NR], olo[NR];
+#pragma unroll
+      for (int i = 0; i < NR; ++i) o[i] = olo[i] = 0.f;
+      float mrun[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f};
+      const int qbase = ph.kvlen - ph.qlen;
+      // tiles t of this piece with (tile_base + t) % kNW == warp
+      int t = (warp - tile_base % kNW + kNW) % kNW;
+      for (; t < n_tiles; t += kNW) {
+        const int st = consumed % S;
+        ptx::mbar_wait(&bar[st], static_cast<uint32_t>((consumed / S) & 1));
+        const uint32_t kb = ptx::smem_u32(ring + st * C::kStage);
+        const uint32_t vb = kb + C::kHalf;
+        float s[4];
+        {
+          float sc[4][4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) sc[c][0] = sc[c][1] = sc[c][2] = sc[c][3] = 0.f;
+#pragma unroll
+          for (int kt = 0; kt < DT; ++kt) {
+            uint32_t a[4];
+            ldsm_x4(kb + kvoff<HD>((lane & 7) + ((lane >> 3) & 1) * 8, 2 * kt + (lane >> 4), ph.tok0), a);
+            mma16816(sc[kt & 1], a, qh[kt][0], qh[kt][1]);
+            mma16816(sc[2 + (kt & 1)], a, ql[kt][0], ql[kt][1]);
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) s[e] = (sc[0][e] + sc[1][e]) + (sc[2][e] + sc[3][e]);
+        }
+        const int key0 = ph.tok0 + t * 16 + gq;
+        const int kend = ph.tok0 + ph.len;
+        float corr[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int qpos = qbase + 2 * cq + e;
+          const bool v0 = key0 < kend && key0 <= qpos;
+          const bool v1 = key0 + 8 < kend && key0 + 8 <= qpos;
+          s[e] = v0 ? s[e] : -INFINITY;
+          s[2 + e] = v1 ? s[2 + e] : -INFINITY;
+          float mx = fmaxf(s[e], s[2 + e]);
+          mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 4));
+          mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 8));
+          mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 16));
+          const float mnew = fmaxf(mrun[e], mx);
+          corr[e] = mnew == -INFINITY ? 1.f : exp2f(mrun[e] - mnew);
+          const float p0 = mnew == -INFINITY ? 0.f : exp2f(s[e] - mnew);
+          const float p1 = mnew == -INFINITY ? 0.f : exp2f(s[2 + e] - mnew);
+          s[e] = p0;
+          s[2 + e] = p1;
+          lsum[e] = lsum[e] * corr[e] + (p0 + p1);
+          mrun[e] = mnew;
+        }
+#pragma unroll
+        for (int dt = 0; dt < DT; ++dt) {
+          float* oo = o + dt * 4;
+          oo[0] *= corr[0], oo[1] *= corr[1], oo[2] *= corr[0], oo[3] *= corr[1];
+          float* ol = olo + dt * 4;
+          ol[0] *= corr[0], ol[1] *= corr[1], ol[2] *= corr[0], ol[3] *= corr[1];
+        }
+        const float h0 = bf_round(s[0]), h1 = bf_round(s[1]), h2 = bf_round(s[2]), h3 = bf_round(s[3]);
+        const uint32_t ph0 = movm_t(pack_bf2(h0, h1)), ph1 = movm_t(pack_bf2(h2, h3));
+        const uint32_t pl0 = movm_t(pack_bf2(s[0] - h0, s[1] - h1)), pl1 = movm_t(pack_bf2(s[2] - h2, s[3] - h3));
+#pragma unroll
+        for (int dt = 0; dt < DT; ++dt) {
+          uint32_t a[4];
+          ldsm_x4_t(vb + kvoff<HD>((lane & 7) + ((lane >> 4) & 1) * 8, 2 * dt + ((lane >> 3) & 1), ph.tok0), a);
+          mma16816(o + dt * 4, a, ph0, ph1);
+          mma16816(olo + dt * 4, a, pl0, pl1);
+        }
+        ++consumed;
+        __syncwarp();
+        try_issue();
+      }
+      tile_base += n_tiles;
+#pragma unroll
+      for (int i = 0; i < NR; ++i) o[i] += olo[i];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        float l = lsum[e];
+        l += __shfl_xor_sync(kFull, l, 4);
+        l += __shfl_xor_sync(kFull, l, 8);
+        l += __shfl_xor_sync(kFull, l, 16);
+        lsum[e] = l;
+      }
+      if (stamp && k == 0) w.st[8 * blockIdx.x + 4] = ptx::globaltimer();
+      // ---- this warp's partial of the piece -> shared memory
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int e = i & 3, dt = i >> 2;
+        const int qi = 2 * cq + (e & 1);
+        const int dim = 16 * dt + gq + (e >> 1) * 8;
+        my_o[qi * HD + dim] = o[i];
+        if (dt == 0 && gq == 0 && e < 2) my_m[qi] = mrun[e], my_l[qi] = lsum[e];
+      }
+      __syncthreads();
+      // ---- fixed-order merge of the four warps' partials; output or split-KV partial
+      const bool single = ph.npieces == 1;
+      const int pidx = pb + k;
+      for (int x = threadIdx.x; x < ph.qlen * HD; x += kThreads) {
+        const int qi = x / HD, dim = x % HD;
+        float M = -INFINITY;
+#pragma unroll
+        for (int ww = 0; ww < kNW; ++ww) M = fmaxf(M, mrg[ww * DC::kMergeFloats + qi]);
+        float L = 0.f, O = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < kNW; ++ww) {
+          const float* wm = mrg + ww * DC::kMergeFloats;
+          const float f = wm[qi] == -INFINITY ? 0.f : exp2f(wm[qi] - M);
+          L += wm[8 + qi] * f;
+          O += wm[16 + qi * HD + dim] * f;
+        }
+        if (single) {
+          out[static_cast<size_t>(ph.qs + qi) * D + head * HD + dim] = __float2bfloat16_rn(O / L);
+        } else {
+          const size_t pi = (static_cast<size_t>(pidx) * H + head) * QP + qi;
+          w.part_o[pi * HD + dim] = O;
+          if (dim == 0) w.part_m[pi] = M, w.part_l[pi] = L;
+        }
+      }
+      __syncthreads();  // merge slots reused by the next piece; partial complete
+      if (stamp && k == 0) w.st[8 * blockIdx.x + 5] = ptx::globaltimer();
+      if (single || warp != 0) continue;
+      // ---- arrival: the CTA completing the last piece of (request, head) merges them
+      int last = 0;
+      if (lane == 0) {
+        int* cnt = w.counter + static_cast<size_t>(ph.req) * H + head;
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        last = atomicAdd(cnt, 1) == ph.npieces - 1;
+        if (last) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          *cnt = 0;
+        }
+      }
+      last = __shfl_sync(kFull, last, 0);
+      if (!last) continue;
+      if (stamp) w.st[8 * blockIdx.x + 6] = ptx::globaltimer();
+      const int npc = ph.npieces;
+      for (int qi = 0; qi < ph.qlen; ++qi) {
+        float M = -INFINITY;
+        for (int p0 = 0; p0 < npc; p0 += 32) {
+          const int pp = p0 + lane;
+          const int pid = pp < npc ? __ldcg(m.req_plist + ph.pptr + pp) : 0;
+          const float mp = pp < npc ? __ldcg(w.part_m + (static_cast<size_t>(pid) * H + head) * QP + qi) : -INFINITY;
+          M = fmaxf(M, mp);
+        }
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o2));
+        float L = 0.f;
+        float acc[HD / 32];
+#pragma unroll
+        for (int j = 0; j < HD / 32; ++j) acc[j] = 0.f;
+        for (int p0 = 0; p0 < npc; p0 += 32) {
+          const int pp = p0 + lane;
+          int pid = 0;
+          float f = 0.f;
+          if (pp < npc) {
+            pid = __ldcg(m.req_plist + ph.pptr + pp);
+            const size_t pi = (static_cast<size_t>(pid) * H + head) * QP + qi;
+            const float mp = __ldcg(w.part_m + pi);
+            f = mp == -INFINITY ? 0.f : exp2f(mp - M);
+            L += __ldcg(w.part_l + pi) * f;
+          }
+          const int cntp = min(32, npc - p0);
+          for (int j0 = 0; j0 < cntp; ++j0) {
+            const float fj = __shfl_sync(kFull, f, j0);
+            const int pj = __shfl_sync(kFull, pid, j0);
+            if (fj == 0.f) continue;
+            const float* src = w.part_o + ((static_cast<size_t>(pj) * H + head) * QP + qi) * HD + (HD / 32) * lane;
+            if constexpr (HD == 128) {
+              const float4 v = __ldcg(reinterpret_cast<const float4*>(src));
+              acc[0] += v.x * fj, acc[1] += v.y * fj, acc[2] += v.z * fj, acc[3] += v.w * fj;
+            } else {
+              const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
+              acc[0] += v.x * fj, acc[1] += v.y * fj;
+            }
+          }
+        }
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(kFull, L, o2);
+        const float inv = 1.0f / L;
+        bf16* dst = out + static_cast<size_t>(ph.qs + qi) * D + head * HD + (HD / 32) * lane;
+#pragma unroll
+        for (int j = 0; j < HD / 32; ++j) dst[j] = __float2bfloat16_rn(acc[j] * inv);
+      }
+    }
+  }
+  if (stamp) w.st[8 * blockIdx.x + 7] = ptx::globaltimer();
+  ptx::grid_dep_launch();
+}
+
+template <int HD>
+void launch_decode(const FwdMeta& m, int n_rows, const AttnGeom& g, const float* q, const AttnWork& w, bf16* out,
+                   cudaStream_t s) {
+  using DC = DecCfg<HD>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(attn_decode_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(DC::kTotal));
+    configured = true;
+  }
+  const int n_items = n_rows * std::max(1, w.chunks);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.stream = s;
+  cfg.gridDim = dim3(n_items * g.n_heads);  // one CTA per (row, chunk, head)
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = DC::kTotal;
+  cudaLaunchKernelEx(&cfg, attn_decode_kernel<HD>, m, g, q, w, out, n_items);
 }
 
 template <int HD, int NQT>
@@ -441,12 +773,24 @@ void launch_hd(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& 
 
 }  // namespace
 
-int attn_ctas(int n_rows, int chunks, int heads) {
+int attn_ctas(int n_rows, int chunks, int heads, int qmax) {
+  if (qmax <= kDecodeQ) return n_rows * std::max(1, chunks) * heads;
   return (n_rows * std::max(1, chunks) * heads + kNW - 1) / kNW;
 }
 
-int attn_chunks(int rows, int heads, int num_sms) {
-  // ~8 warps of work per SM (2 CTAs x 4 warps): rows x chunks x heads ~= 8 x SMs
+int attn_chunks(int rows, int heads, int num_sms, int qmax) {
+  if (qmax <= kDecodeQ) {
+    // attn_decode_kernel: one 4-warp CTA per item. Whole (request, head) pairs per CTA
+    // unless there are too few of them to fill the SMs: a split-KV merge (gpu-scope
+    // fence + arrival counter) costs more than the longer per-CTA chain.
+    static const double cps = [] {
+      const char* e = std::getenv("SPIN_ATTN_DEC_CPS");  // experiments only
+      return e ? std::atof(e) : 1.0;
+    }();
+    const double want = cps * num_sms / std::max(1, rows * heads);
+    return std::max(1, std::min(16, static_cast<int>(std::lround(want))));
+  }
+  // attn_kernel: ~8 warps of work per SM (2 CTAs x 4 warps): rows x chunks x heads ~= 8 x SMs
   static const double wps = [] {
     const char* e = std::getenv("SPIN_ATTN_WPS");  // experiments only
     return e ? std::atof(e) : 8.0;
@@ -459,6 +803,10 @@ void launch_attention(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const Fw
                       const AttnGeom& g, const float* q, const AttnWork& w, bf16* out, cudaStream_t s) {
   (void)n_req;
   if (n_rows <= 0) return;
+  if (w.qmax <= kDecodeQ) {
+    if (g.head_dim == 128) return launch_decode<128>(m, n_rows, g, q, w, out, s);
+    return launch_decode<64>(m, n_rows, g, q, w, out, s);
+  }
   if (g.head_dim == 128) return launch_hd<128>(tm_k, tm_v, m, n_rows, g, q, w, out, s);
   return launch_hd<64>(tm_k, tm_v, m, n_rows, g, q, w, out, s);
 }

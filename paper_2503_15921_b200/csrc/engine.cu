@@ -293,7 +293,7 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
   ep.part = ln.part;
   AttnWork aw = ln.aw;
   aw.qmax = sh.qmax;
-  aw.chunks = attn_chunks(sh.rows, m.H, num_sms_);
+  aw.chunks = attn_chunks(sh.rows, m.H, num_sms_, sh.qmax);
   aw.early = sh.early;
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = m.layers[l];
@@ -357,7 +357,7 @@ void Engine::forward_draft(ModelDev& m, Lane& ln, const FwdShape& sh, AttnGeom g
   int n_ssp = 1;
   AttnWork aw = ln.aw;
   aw.qmax = sh.qmax;
-  aw.chunks = attn_chunks(sh.rows, m.H, num_sms_);
+  aw.chunks = attn_chunks(sh.rows, m.H, num_sms_, sh.qmax);
   aw.early = sh.early;
   DraftProj a{};
   a.T = T;
@@ -386,7 +386,7 @@ void Engine::forward_draft(ModelDev& m, Lane& ln, const FwdShape& sh, AttnGeom g
     }
     if (!(skip & 1)) {
       prof_begin(base + 2, s);
-      aw.st = stamp_slot(1, attn_ctas(sh.rows, aw.chunks, m.H));
+      aw.st = stamp_slot(1, 2 * attn_ctas(sh.rows, aw.chunks, m.H, sh.qmax));  // 8 stamps per CTA
       launch_attention(m.tm_k, m.tm_v, ln.meta, sh.rows, sh.R, g, ln.q, aw, ln.attn, s);
       prof_end(s, 0);
     }
@@ -730,7 +730,8 @@ void Engine::capture_round(RoundPlan& p) {
       a.list = list;
       a.ssm = j;
       a.width = nj;
-      a.chunks = attn_chunks(nj, m.H, num_sms_);
+      a.chunks = attn_chunks(nj, m.H, num_sms_, 2);
+      a.padded = 1;  // few-query steps: one row per request, whole requests per CTA (no merges)
       prof_begin(kProfMeta, sj);
       launch_meta(a, st_, ln.meta, sj);
       prof_end(sj, 0);
@@ -744,7 +745,8 @@ void Engine::capture_round(RoundPlan& p) {
         b.step = k;
         b.ssm = j;
         b.width = nj;
-        b.chunks = attn_chunks(nj, m.H, num_sms_);
+        b.chunks = attn_chunks(nj, m.H, num_sms_, 1);
+        b.padded = 1;
         b.amax_val = ln.amax_val;
         b.amax_idx = ln.amax_idx;
         b.amax_tiles = tiles;

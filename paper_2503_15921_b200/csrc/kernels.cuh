@@ -150,9 +150,11 @@ struct AttnWork {
   int early = 0;  // issue K/V tiles older than the queries before the dependency wait (FwdShape::early)
   unsigned long long* st = nullptr;  // optional timeline stamps [CTA][4] (SPIN_STAMPS)
 };
-int attn_ctas(int n_rows, int chunks, int heads);
+int attn_ctas(int n_rows, int chunks, int heads, int qmax);
 // Chunks per pack row so that rows x chunks x heads warps fill the GPU.
-int attn_chunks(int rows, int heads, int num_sms);
+// Requests with at most kDecodeQ queries (draft steps) use the few-query kernel.
+constexpr int kDecodeQ = 2;
+int attn_chunks(int rows, int heads, int num_sms, int qmax = 8);
 void launch_attention(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m, int n_rows, int n_req,
                       const AttnGeom& g, const float* q, const AttnWork& w, bf16* out, cudaStream_t s);
 
