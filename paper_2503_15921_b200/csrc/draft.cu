@@ -13,9 +13,11 @@
 //     gemm.cuh as 1-KB row groups) is bulk-copied into shared memory BEFORE the
 //     programmatic-dependent-launch wait, overlapping the previous kernel;
 //   * RMSNorm is folded into the consumers: residual producers also write each
-//     unit's sum of squares per token (ssp[t][unit], a token's partials contiguous); a consumer sums those in a
-//     fixed order and scales the fp32 residual while loading it (norm-on-load),
-//     so no normalised copy of the activations is materialised;
+//     unit's sum of squares per token (ssp[t][unit], a token's partials contiguous);
+//     a consumer multiplies with bf16(h) and scales each token's outputs by
+//     1/rms(h) (a per-token factor of the product) computed from those sums in a
+//     fixed order, so no normalised copy of the activations is materialised and
+//     the matmul never waits on the sums;
 //   * the token operand is loaded straight from L2 into mma.sync B fragments:
 //     each lane reads 8 consecutive k of one token (16 B bf16 / 32 B fp32) and the
 //     A fragment takes the same 8 k of a weight row from shared memory, so the
@@ -237,13 +239,13 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
       const int t = warp + NW * j;
       if (lane == 0 && t < NT * 8)
-        inv_s[t] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(x, static_cast<float>(K)), a.eps)));
+        inv_s[t] = (a.dbg & 16) ? rsqrtf(x / K + a.eps)
+                                : __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(x, static_cast<float>(K)), a.eps)));
     }
   }
-  __syncthreads();
-  float inv[NT];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) inv[nt] = NORM ? inv_s[nt * 8 + g] : 1.f;
+  // (inv_s is published by the barrier before the cross-warp reduction: the RMSNorm
+  // scale is a per-token factor, applied to the reduced outputs, so the weight and
+  // token loads never wait on the sums of squares)
 
   float acc[MT][NT][4];
 #pragma unroll
@@ -273,11 +275,10 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
         uint32_t b0, b1, b2, b3;
         if constexpr (NORM) {
           const float4 x0 = xr[b][nt][0], x1 = xr[b][nt][1];
-          const float iv = inv[nt];
-          b0 = pack_bf16(__fmul_rn(x0.x, iv), __fmul_rn(x0.y, iv));
-          b1 = pack_bf16(__fmul_rn(x0.z, iv), __fmul_rn(x0.w, iv));
-          b2 = pack_bf16(__fmul_rn(x1.x, iv), __fmul_rn(x1.y, iv));
-          b3 = pack_bf16(__fmul_rn(x1.z, iv), __fmul_rn(x1.w, iv));
+          b0 = pack_bf16(x0.x, x0.y);
+          b1 = pack_bf16(x0.z, x0.w);
+          b2 = pack_bf16(x1.x, x1.y);
+          b3 = pack_bf16(x1.z, x1.w);
         } else {
           const uint4 x = xr[b][nt][0];
           b0 = x.x, b1 = x.y, b2 = x.z, b3 = x.w;
@@ -290,8 +291,8 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
       }
     }
   }
-  ptx::grid_dep_launch();
   if (stamp) a.st[4 * u + 2] = ptx::globaltimer();
+  if (!(a.dbg & 32)) ptx::grid_dep_launch();
 
   // ---- fixed-order cross-warp reduction; warp (m, nt) finishes tile m x n-tile nt
 #pragma unroll
@@ -310,6 +311,11 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
     c[0] += v.x, c[1] += v.y, c[2] += v.z, c[3] += v.w;
   }
   // c[0], c[1]: half-0 row (row0 + 8m + g), tokens tA, tA + 1; c[2], c[3]: half-1 row, same tokens
+  if constexpr (NORM) {
+    const float i0 = inv_s[tA], i1 = inv_s[tA + 1];
+    c[0] = __fmul_rn(c[0], i0), c[2] = __fmul_rn(c[2], i0);
+    c[1] = __fmul_rn(c[1], i1), c[3] = __fmul_rn(c[3], i1);
+  }
   if (a.mode == kDpQkv) {
     const AttnGeom& G = a.g;
     const int D = G.n_heads * G.head_dim, hd = G.head_dim, half = hd / 2;
@@ -373,7 +379,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
       if (tA + 1 < T) a.ssp_out[static_cast<size_t>(tA + 1) * (a.n_out / 16) + u] = ss[1];
     }
   }
-  if (stamp) a.st[4 * u + 3] = ptx::globaltimer();
+  if (stamp && !(a.dbg & 64)) a.st[4 * u + 3] = ptx::globaltimer();
 }
 
 // h = embedding rows (fp32), ssp[0][t] = sum of squares (one unit).

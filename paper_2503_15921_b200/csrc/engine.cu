@@ -295,6 +295,11 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
   aw.qmax = sh.qmax;
   aw.chunks = attn_chunks(sh.rows, m.H, num_sms_, sh.qmax);
   aw.early = sh.early;
+  static const int vskip = [] {  // timing experiments only: skip target kernels (results invalid)
+    const char* e = std::getenv("SPIN_VERIFY_SKIP");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int skip = &m == &target_ ? vskip : 0;
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = m.layers[l];
     g.layer = l;
@@ -302,34 +307,42 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     prof_begin(base, s);
     check_cuda(gemm_launch(pq, w.qkv, ln.xn, ep, s, pdl), "gemm qkv");
     prof_end(s, gemm_bytes(3 * D, D));
-    prof_begin(base + 3, s);
-    launch_qkv_epilogue(ln.part, pq.map, ln.meta, T, g, m.rcos, m.rsin, ln.q, s);
-    prof_end(s, 0);
+    if (!(skip & 1)) {
+      prof_begin(base + 3, s);
+      launch_qkv_epilogue(ln.part, pq.map, ln.meta, T, g, m.rcos, m.rsin, ln.q, s);
+      prof_end(s, 0);
+    }
     prof_begin(base + 2, s);
     ++launches_;  // attention + combine
-    launch_attention(m.tm_k, m.tm_v, ln.meta, sh.rows, sh.R, g, ln.q, aw, ln.attn, s);
+    if (!(skip & 8)) launch_attention(m.tm_k, m.tm_v, ln.meta, sh.rows, sh.R, g, ln.q, aw, ln.attn, s);
     prof_end(s, 0);
     const GemmPlan& po = plan(D, D, T, kGemmPartial);
     prof_begin(base, s);
     check_cuda(gemm_launch(po, w.o, ln.attn, ep, s, pdl), "gemm o");
     prof_end(s, gemm_bytes(D, D));
-    prof_begin(base + 3, s);
-    launch_resid_norm(ln.part, po.map, T, D, eps, ln.h, ln.xn, s);
-    prof_end(s, 0);
+    if (!(skip & 2)) {
+      prof_begin(base + 3, s);
+      launch_resid_norm(ln.part, po.map, T, D, eps, ln.h, ln.xn, s);
+      prof_end(s, 0);
+    }
     const GemmPlan& pg = plan(2 * F, D, T, kGemmPartial);
     prof_begin(base, s);
     check_cuda(gemm_launch(pg, w.gu, ln.xn, ep, s, pdl), "gemm gate_up");
     prof_end(s, gemm_bytes(2 * F, D));
-    prof_begin(base + 3, s);
-    launch_swiglu(ln.part, pg.map, T, F, ln.act, s);
-    prof_end(s, 0);
+    if (!(skip & 4)) {
+      prof_begin(base + 3, s);
+      launch_swiglu(ln.part, pg.map, T, F, ln.act, s);
+      prof_end(s, 0);
+    }
     const GemmPlan& pd = plan(D, F, T, kGemmPartial);
     prof_begin(base, s);
     check_cuda(gemm_launch(pd, w.dn, ln.act, ep, s, pdl), "gemm down");
     prof_end(s, gemm_bytes(D, F));
-    prof_begin(base + 3, s);
-    launch_resid_norm(ln.part, pd.map, T, D, eps, ln.h, ln.xn, s);
-    prof_end(s, 0);
+    if (!(skip & 2)) {
+      prof_begin(base + 3, s);
+      launch_resid_norm(ln.part, pd.map, T, D, eps, ln.h, ln.xn, s);
+      prof_end(s, 0);
+    }
   }
   if (head_mode > 0) {
     GemmEpilogue eh;

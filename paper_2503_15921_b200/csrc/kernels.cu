@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kRowThreads) swiglu_kernel(const float* __rest
 // Split-K reduction of the fused QKV projection, RoPE (rotate-half) on q and k,
 // q -> fp32 (feeds only the CUDA-core attention), k/v -> bf16 KV cache at
 // (layer, slot, head, pos). grid (T, ceil(H*hd/2 / 1024)): 4 rotary pairs / thread.
-__global__ void __launch_bounds__(kRowThreads, 1) qkv_epilogue_kernel(const float* __restrict__ part, PieceMap pm,
+__global__ void __launch_bounds__(kRowThreads, 2) qkv_epilogue_kernel(const float* __restrict__ part, PieceMap pm,
                                                                    FwdMeta m, int T, AttnGeom g,
                                                                    const float* __restrict__ rcos,
                                                                    const float* __restrict__ rsin, float* q) {
