@@ -428,7 +428,7 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
     return s ? std::atoi(s) : 0;
   }();
   return cudaLaunchKernelEx(&cfg, gemm_tc_kernel, static_cast<const __nv_bfloat16*>(W), tm_x, tm_part, plan.map, e,
-                            plan.n_out, plan.t, plan.stages, dbg);
+                            plan.n_out, plan.t, plan.stages, epi.mode == kGemmPartial ? dbg : 0);
 }
 
 }  // namespace spin

@@ -8,8 +8,15 @@ timeout 400 python bench.py > gpurun_out/ev_bench.json 2> gpurun_out/ev_bench.er
 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --nvtx --nvtx-include "round/" --csv --log-file gpurun_out/ev_launches.csv python tools/prof_round.py --graph 0 \
   > gpurun_out/ev_launches.log 2>&1
-timeout 300 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "round/" \
-  -k regex:gemm_tc_kernel -s 232 -c 4 -o gpurun_out/ev_gemm -f python tools/prof_round.py --graph 0 > gpurun_out/ev_ncu1.log 2>&1
-timeout 300 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "round/" \
-  -k regex:attn_kernel -s 56 -c 1 -o gpurun_out/ev_attn -f python tools/prof_round.py --graph 0 > gpurun_out/ev_ncu2.log 2>&1
+NCU="ncu --set full --import-source on --clock-control none --nvtx --nvtx-include round/"
+# target projections of layer 1 (the SSM rounds launch 8 lm_head GEMMs first)
+timeout 300 $NCU -k regex:gemm_tc_kernel -s 12 -c 4 -o gpurun_out/ev_gemm -f python tools/prof_round.py --graph 0 \
+  > gpurun_out/ev_ncu1.log 2>&1
+timeout 300 $NCU -k regex:attn_kernel -s 1 -c 1 -o gpurun_out/ev_attn -f python tools/prof_round.py --graph 0 \
+  > gpurun_out/ev_ncu2.log 2>&1
+timeout 300 $NCU -k regex:dproj_kernel -s 40 -c 4 -o gpurun_out/ev_dproj -f python tools/prof_round.py --graph 0 \
+  > gpurun_out/ev_ncu3.log 2>&1
+timeout 300 $NCU -k regex:attn_decode_kernel -s 20 -c 1 -o gpurun_out/ev_attn_dec -f python tools/prof_round.py --graph 0 \
+  > gpurun_out/ev_ncu4.log 2>&1
+SPIN_STAMPS=gpurun_out/ev_stamps.csv timeout 300 python tools/prof_round.py --graph 1 > /dev/null 2>&1
 cat gpurun_out/ev_pytest.txt; tail -c 600 gpurun_out/ev_bench.json

@@ -1,5 +1,4 @@
-# timing experiments on the draft projections (results invalid; timing only)
-for m in 0; do
-  SPIN_DPROJ_DBG=$m SPIN_STAMPS=gpurun_out/stamps_$m.csv timeout 300 python tools/prof_round.py --graph 1 > /dev/null 2>&1
-  echo "dbg $m"; python tools/stamps.py gpurun_out/stamps_$m.csv 0 0 2>/dev/null | tail -5
+# timing experiments: skip target-forward kernels (results invalid; timing only)
+for m in 0 4; do
+  SPIN_VERIFY_SKIP=$m timeout 200 python bench.py --no-cpu-baseline --steps 10 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('vskip', $m, round(d['value']), round(d['config']['draft_us_median']), round(d['config']['verify_step_us_median']))"
 done
