@@ -398,8 +398,7 @@ def main():
             out = eng.round(slots, assign)
             e2e_tokens += int(out["accepted"].sum()) + BATCH
             wall = out["round_ms"] / 1e3
-            for i in range(BATCH):
-                stats.add(i, int(assign[i]), (out["accepted"][i] + 1) / wall)
+            stats.add_many(np.arange(BATCH), assign, (out["accepted"] + 1) / wall)
             stats.gather(dist)
             verify_us.append(out["verify_ms"] * 1e3)
             draft_us.append(out["draft_ms"] * 1e3)

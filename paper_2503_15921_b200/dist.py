@@ -9,6 +9,7 @@ CPU tests.
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 
@@ -20,12 +21,18 @@ def shard(num_requests: int, world: int, rank: int) -> range:
 
 
 class AcceptanceStats:
-    """Local ArmEstimate rows [local_requests, n_ssm, (sum, count)] plus the gather."""
+    """Local ArmEstimate rows [local_requests, n_ssm, (sum, count)] plus the gather.
+
+    The rows are accumulated on the host (a numpy view of a CPU tensor: per-request
+    updates are host arithmetic, not device launches); `device` holds the gather
+    buffers (CUDA for NCCL), filled by one host->device copy per gather."""
 
     def __init__(self, num_requests: int, n_ssm: int, world: int, rank: int, device="cpu"):
         self.world, self.rank = world, rank
         self.owned = shard(num_requests, world, rank)
         self.rows = max(len(shard(num_requests, world, r)) for r in range(world))  # padded for the gather
+        self.host = torch.zeros((self.rows, n_ssm, 2), dtype=torch.float64)
+        self._np = self.host.numpy()
         self.local = torch.zeros((self.rows, n_ssm, 2), dtype=torch.float64, device=device)
         # flat [world * rows, ...]: the layout all_gather_into_tensor fills (gloo and NCCL)
         self.gathered = torch.zeros((world * self.rows, n_ssm, 2), dtype=torch.float64, device=device)
@@ -33,18 +40,23 @@ class AcceptanceStats:
 
     def add(self, local_index: int, ssm: int, goodput: float) -> None:
         """ArmEstimate::add (bandit.hpp:28-31)."""
-        self.local[local_index, ssm, 0] += goodput
-        self.local[local_index, ssm, 1] += 1
+        self._np[local_index, ssm, 0] += goodput
+        self._np[local_index, ssm, 1] += 1
+
+    def add_many(self, local_indices, ssms, goodputs) -> None:
+        """ArmEstimate::add for a batch of (request, SSM, goodput) observations, in order."""
+        np.add.at(self._np[..., 0], (np.asarray(local_indices), np.asarray(ssms)), np.asarray(goodputs, np.float64))
+        np.add.at(self._np[..., 1], (np.asarray(local_indices), np.asarray(ssms)), 1.0)
 
     def gather(self, dist=None) -> torch.Tensor:
         """All-gather; returns global [num_requests, n_ssm, 2] in request-id order."""
         if dist is not None and self.world > 1:
+            self.local.copy_(self.host)
             dist.all_gather_into_tensor(self.gathered, self.local)
-        else:
-            self.gathered[: self.rows].copy_(self.local)
-        parts = [self.gathered[r * self.rows: r * self.rows + len(shard(self.num_requests, self.world, r))]
-                 for r in range(self.world)]
-        return torch.cat(parts, 0)
+            parts = [self.gathered[r * self.rows: r * self.rows + len(shard(self.num_requests, self.world, r))]
+                     for r in range(self.world)]
+            return torch.cat(parts, 0)
+        return self.host[: len(self.owned)].clone()
 
     @staticmethod
     def means(global_rows: torch.Tensor) -> torch.Tensor:

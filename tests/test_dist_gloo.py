@@ -3,6 +3,7 @@ per-(request, SSM) acceptance statistics exactly as bench.py does over NCCL."""
 import os
 import socket
 
+import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
@@ -64,3 +65,14 @@ def test_gloo_allgather_of_acceptance_stats(n_req):
     assert torch.equal(torch.tensor(res[0], dtype=torch.float64), ref)
     means = AcceptanceStats.means(ref)
     assert torch.isinf(means[0, 1]) and means[1, 1] == 10 + 1
+
+
+def test_add_many_matches_add():
+    a = AcceptanceStats(10, 3, 1, 0)
+    b = AcceptanceStats(10, 3, 1, 0)
+    rng = np.random.default_rng(7)
+    idx, ssm, gp = rng.integers(0, 10, 50), rng.integers(0, 3, 50), rng.random(50)
+    for i, j, g in zip(idx, ssm, gp):
+        a.add(int(i), int(j), float(g))
+    b.add_many(idx, ssm, gp)
+    assert torch.allclose(a.gather(), b.gather())
