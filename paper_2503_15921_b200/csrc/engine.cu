@@ -305,6 +305,8 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     g.layer = l;
     const GemmPlan& pq = plan(3 * D, D, T, kGemmPartial);
     prof_begin(base, s);
+    const bool stamp_layer = &m == &target_ && l == 1;
+    ep.st = stamp_layer ? stamp_slot(10, 2 * pq.grid) : nullptr;
     check_cuda(gemm_launch(pq, w.qkv, ln.xn, ep, s, pdl), "gemm qkv");
     prof_end(s, gemm_bytes(3 * D, D));
     if (!(skip & 1)) {
@@ -318,6 +320,7 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     prof_end(s, 0);
     const GemmPlan& po = plan(D, D, T, kGemmPartial);
     prof_begin(base, s);
+    ep.st = stamp_layer ? stamp_slot(11, 2 * po.grid) : nullptr;
     check_cuda(gemm_launch(po, w.o, ln.attn, ep, s, pdl), "gemm o");
     prof_end(s, gemm_bytes(D, D));
     if (!(skip & 2)) {
@@ -327,6 +330,7 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     }
     const GemmPlan& pg = plan(2 * F, D, T, kGemmPartial);
     prof_begin(base, s);
+    ep.st = stamp_layer ? stamp_slot(12, 2 * pg.grid) : nullptr;
     check_cuda(gemm_launch(pg, w.gu, ln.xn, ep, s, pdl), "gemm gate_up");
     prof_end(s, gemm_bytes(2 * F, D));
     if (!(skip & 4)) {
@@ -336,7 +340,9 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     }
     const GemmPlan& pd = plan(D, F, T, kGemmPartial);
     prof_begin(base, s);
+    ep.st = stamp_layer ? stamp_slot(13, 2 * pd.grid) : nullptr;
     check_cuda(gemm_launch(pd, w.dn, ln.act, ep, s, pdl), "gemm down");
+    ep.st = nullptr;
     prof_end(s, gemm_bytes(D, F));
     if (!(skip & 2)) {
       prof_begin(base + 3, s);

@@ -26,6 +26,11 @@ constexpr int kMaxStages = 8;
 constexpr int kThreads = 256;
 constexpr uint32_t kTileABytes = kBlockM * kBlockK * 2;  // 16 KiB
 constexpr size_t kRedBytes = 4 * 256 * 8;                // argmax cross-warp scratch
+// PARTIAL epilogue: fp32 tiles leave through kStgSlots staging slots of 16 tokens x 128
+// features (8 KB), one TMA tensor store per slot, so storing a piece neither waits for the
+// ring to drain nor competes with the weight stream for LSU bandwidth.
+constexpr int kStgSlots = 8;
+constexpr size_t kStgBytes = static_cast<size_t>(kStgSlots) * 16 * kBlockM * 4;
 constexpr size_t kBarBytes = 256;
 
 struct Piece {
@@ -84,8 +89,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tile_b_bytes = static_cast<uint32_t>(bn) * kBlockK * 2;
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + static_cast<size_t>(stages) * kTileABytes;
-  uint8_t* smem_red = smem_b + static_cast<size_t>(stages) * tile_b_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_red + kRedBytes);
+  uint8_t* smem_red = smem_b + static_cast<size_t>(stages) * tile_b_bytes;  // ARGMAX scratch | PARTIAL staging
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smem_red + (pm.mode == kGemmPartial ? kStgBytes : kRedBytes));
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + kMaxStages;
   uint64_t* tfull_bar = bars + 2 * kMaxStages;
@@ -94,6 +100,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  // stamps [CTA][8]: start, producer wait release, first stage ready (MMA), last MMA issued,
+  // first epilogue start, last epilogue done, end
+  unsigned long long* st = epi.st ? epi.st + 8 * blockIdx.x : nullptr;
+  if (st && threadIdx.x == 0) st[0] = ptx::globaltimer();
   const int n_tiles = pm.n_mtiles * ((t_total + bn - 1) / bn);
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(2 * bn)) tmem_cols <<= 1;
@@ -147,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::grid_dep_wait();
       waited = true;
+      if (st) st[1] = ptx::globaltimer();
       int issued = 0;
       while (it.next(pm, n_tiles, p)) {
         const int mt = p.tile % pm.n_mtiles;
@@ -188,6 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = p.kb0; kb < p.kb1; ++kb) {
         ptx::mbar_wait(&full_bar[stage], phase);
         ptx::tc_fence_after();
+        if (st && lane == 0 && iter == 0 && kb == p.kb0) st[2] = ptx::globaltimer();
         if (lane == 0) {
           const uint64_t da = ptx::smem_desc_sw128(smem_a + static_cast<size_t>(stage) * kTileABytes);
           const uint64_t db = ptx::smem_desc_sw128(smem_b + static_cast<size_t>(stage) * tile_b_bytes);
@@ -209,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ++iter;
     }
+    if (st && lane == 0) st[3] = ptx::globaltimer();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;  // TMEM lane quadrant (warp % 4)
@@ -218,13 +231,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     PieceIter it;
     it.init(pm, n_tiles);
     Piece p;
-    int iter = 0;
+    int iter = 0, chunk = 0;
     while (it.next(pm, n_tiles, p)) {
       const int acc = iter & 1;
       const int mt = p.tile % pm.n_mtiles;
       const int nt = p.tile / pm.n_mtiles;
       ptx::mbar_wait(&tfull_bar[acc], (iter >> 1) & 1);
       ptx::tc_fence_after();
+      if (st && ew == 0 && lane == 0 && iter == 0) st[4] = ptx::globaltimer();
       const int row = ew * 32 + lane;
       const int n = mt * kBlockM + row;
       const bool n_ok = n < n_out;
@@ -232,41 +246,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       PieceIter ahead = it;
       Piece pn;
       const bool last_piece = !ahead.next(pm, n_tiles, pn);
-      if (epi.mode == kGemmPartial && last_piece && !(dbg & 8)) {
-        // The CTA's last piece: every MMA is done, so the stage ring is free. Stage the
-        // fp32 tile as [t][128 features] and write it with one TMA tensor store.
-        float* stg = reinterpret_cast<float*>(smem);
-        for (int c0 = 0; c0 < bn; c0 += 16) {
+      if (epi.mode == kGemmPartial) {
+        // 16-token chunks through the staging slots; a slot is rewritten only after the
+        // store issued kStgSlots chunks earlier has finished reading it
+        float* stg_base = reinterpret_cast<float*>(smem_red);
+        for (int c0 = 0; c0 < bn; c0 += 16, ++chunk) {
+          float* stg = stg_base + (chunk % kStgSlots) * (16 * kBlockM);
+          if (chunk >= kStgSlots) {
+            if (ew == 0 && lane == 0) ptx::bulk_wait_read<kStgSlots - 1>();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+          }
           float v[16];
           ptx::tmem_ld16(t_addr + c0, v);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) stg[(c0 + j) * kBlockM + row] = v[j];
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
-        ptx::fence_proxy_async_smem();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (ew == 0 && lane == 0) {
-          ptx::tma_store_3d(&tm_part, stg, mt * kBlockM, nt * bn, p.slot);
-          ptx::bulk_commit();
-          ptx::bulk_wait0();  // the consumer kernel reads the partial after this grid completes
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-      } else if (epi.mode == kGemmPartial) {
-        float* dst = epi.part + static_cast<size_t>(p.slot) * t_total * n_out;
-        for (int c0 = 0; c0 < bn; c0 += 16) {
-          float v[16];
-          ptx::tmem_ld16(t_addr + c0, v);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int t = nt * bn + c0 + j;
-            if (n_ok && t < t_total && !(dbg & 4)) dst[static_cast<size_t>(t) * n_out + n] = v[j];
+          for (int j = 0; j < 16; ++j) stg[j * kBlockM + row] = v[j];
+          ptx::fence_proxy_async_smem();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (ew == 0 && lane == 0 && !(dbg & 4)) {
+            ptx::tma_store_3d(&tm_part, stg, mt * kBlockM, nt * bn + c0, p.slot);
+            ptx::bulk_commit();
           }
         }
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+        (void)last_piece;
+        (void)n_ok;
       } else {
         for (int c0 = 0; c0 < bn; c0 += 16) {
           float v[16];
@@ -304,8 +309,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
+      if (st && ew == 0 && lane == 0 && iter == 0) st[7] = ptx::globaltimer();
       ++iter;
     }
+    // partials must be in global memory before the grid completes (the consumer reads them)
+    if (epi.mode == kGemmPartial && ew == 0 && lane == 0) ptx::bulk_wait0();
+    if (st && ew == 0 && lane == 0) st[5] = ptx::globaltimer();
   }
 
   ptx::grid_dep_launch();
@@ -313,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc(tmem_base, tmem_cols);
+  if (st && threadIdx.x == 0) st[6] = ptx::globaltimer();
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
@@ -357,9 +367,13 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
   p.kb = (k + kBlockK - 1) / kBlockK;
   const long long n_tiles = static_cast<long long>(p.n_mtiles) * p.n_ntiles;
   const size_t stage_bytes = kTileABytes + static_cast<size_t>(p.bn) * kBlockK * 2;
-  const size_t budget = 227 * 1024 - 1024 - kRedBytes - kBarBytes;
-  p.stages = static_cast<int>(std::min<size_t>(kMaxStages, budget / stage_bytes));
-  p.smem_bytes = 1024 + p.stages * stage_bytes + kRedBytes + kBarBytes;
+  const size_t budget = 227 * 1024 - 1024 - (mode == kGemmPartial ? kStgBytes : kRedBytes) - kBarBytes;
+  static const int cap = [] {
+    const char* e = std::getenv("SPIN_GEMM_STAGES");  // experiments only
+    return e ? std::atoi(e) : kMaxStages;
+  }();
+  p.stages = static_cast<int>(std::min<size_t>(std::min(kMaxStages, cap), budget / stage_bytes));
+  p.smem_bytes = 1024 + p.stages * stage_bytes + (mode == kGemmPartial ? kStgBytes : kRedBytes) + kBarBytes;
   PieceMap& m = p.map;
   m.mode = mode;
   m.kb = p.kb;
@@ -400,7 +414,7 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(plan.n_out), static_cast<cuuint64_t>(plan.t),
                           static_cast<cuuint64_t>(plan.max_pieces)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(plan.n_out) * 4, static_cast<cuuint64_t>(plan.n_out) * plan.t * 4};
-    cuuint32_t box[3] = {static_cast<cuuint32_t>(kBlockM), static_cast<cuuint32_t>(plan.bn), 1};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(kBlockM), 16, 1};  // one staging slot
     cuuint32_t estr[3] = {1, 1, 1};
     if (fn == nullptr || (plan.n_out * 4) % 16 != 0 ||
         fn(&tm_part, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, epi.part, dims, strides, box, estr,
