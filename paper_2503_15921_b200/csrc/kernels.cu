@@ -375,6 +375,7 @@ __global__ void __launch_bounds__(kRowThreads) embed_norm_kernel(const bf16* __r
   extern __shared__ float s_row[];
   __shared__ float red[32];
   ptx::grid_dep_wait();
+  ptx::grid_dep_launch();  // dependents (the next GEMM) may start their weight prefetch now
   const int t = blockIdx.x;
   const bf16* e = emb + static_cast<size_t>(tok[t]) * D;
   for (int i = threadIdx.x; i < D; i += kRowThreads) {
@@ -383,7 +384,6 @@ __global__ void __launch_bounds__(kRowThreads) embed_norm_kernel(const bf16* __r
     h[static_cast<size_t>(t) * D + i] = v;
   }
   __syncthreads();
-  ptx::grid_dep_launch();
   rmsnorm_row(s_row, D, eps, xn + static_cast<size_t>(t) * D, red);
 }
 
@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(kRowThreads) resid_norm_kernel(const float* __
                                                                  bf16* __restrict__ xn) {
   __shared__ float red[32];
   ptx::grid_dep_wait();
+  ptx::grid_dep_launch();  // dependents (the next GEMM) may start their weight prefetch now
   const int t = blockIdx.x;
   const size_t stride = static_cast<size_t>(T) * D;
   const float* prow = part + static_cast<size_t>(t) * D;
@@ -435,7 +436,6 @@ __global__ void __launch_bounds__(kRowThreads) resid_norm_kernel(const float* __
     hrow[threadIdx.x + k * kRowThreads] = v[k];
     ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
   }
-  ptx::grid_dep_launch();
   const float tot = block_sum(ss, red);
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(tot, static_cast<float>(D)), eps)));
   bf16* xrow = xn + static_cast<size_t>(t) * D;
@@ -459,6 +459,7 @@ constexpr int kSwiVec = 1;
 __global__ void __launch_bounds__(kRowThreads) swiglu_kernel(const float* __restrict__ part, PieceMap pm, int T, int F,
                                                              bf16* act) {
   ptx::grid_dep_wait();
+  ptx::grid_dep_launch();  // dependents (the next GEMM) may start their weight prefetch now
   const int t = blockIdx.x;
   float4 g[kSwiVec], u[kSwiVec];
 #pragma unroll
@@ -483,7 +484,6 @@ __global__ void __launch_bounds__(kRowThreads) swiglu_kernel(const float* __rest
     o.y = *reinterpret_cast<uint32_t*>(&b);
     *reinterpret_cast<uint2*>(act + static_cast<size_t>(t) * F + f) = o;
   }
-  ptx::grid_dep_launch();
 }
 
 __global__ void __launch_bounds__(kRowThreads, 2) qkv_epilogue_kernel(const float* __restrict__ part, PieceMap pm,
@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) qkv_epilogue_kernel(const floa
                                                                    const float* __restrict__ rcos,
                                                                    const float* __restrict__ rsin, float* q) {
   ptx::grid_dep_wait();
+  ptx::grid_dep_launch();  // dependents (the next GEMM) may start their weight prefetch now
   const int t = blockIdx.x;
   const int H = g.n_heads, hd = g.head_dim, half = hd / 2, D = H * hd, N = 3 * D;
   const int p4 = 4 * (blockIdx.y * kRowThreads + threadIdx.x);  // first of 4 rotary pairs
@@ -533,7 +534,6 @@ __global__ void __launch_bounds__(kRowThreads, 2) qkv_epilogue_kernel(const floa
       put4(g.v_cache + kv + kv_swz(pos, i + half), v1.x, v1.y, v1.z, v1.w);
     }
   }
-  ptx::grid_dep_launch();
 }
 
 // ------------------------------------------------------------------ accept
