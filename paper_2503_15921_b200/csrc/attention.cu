@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
       if (stamp) w.st[8 * blockIdx.x + 1] = ptx::globaltimer();
       try_issue();
     }
+    if (pb == p_lo) ptx::grid_dep_launch();  // the next GEMM takes SMs as this grid drains
 
     for (int k = 0; k < np; ++k) {
       const Piece ph = pcs[k];
