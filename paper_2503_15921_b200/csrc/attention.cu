@@ -94,6 +94,99 @@ struct Piece {
   int req, slot, tok0, len, qs, qlen, kvlen, npieces, pptr, pad[7];
 };
 
+// Shared-max merge of a request's split-KV partials (attention.cpp:128-157), by one warp,
+// pieces in token order. Lanes own pieces for the max / sum and head dims for the
+// output; every query's (max, sum) loads of all pieces are issued together, then one
+// pass over the pieces accumulates up to 8 queries' outputs (independent loads).
+template <int HD, int QP>
+__device__ __forceinline__ void merge_pieces(const FwdMeta& m, const AttnWork& w, const Piece& ph, int head, int H,
+                                             int D, bf16* __restrict__ out, int lane) {
+  constexpr int DV = HD / 32;  // head dims per lane
+  const int npc = ph.npieces;
+  if (npc > 32) {  // rare (long requests split over many chunks): query-serial merge
+    for (int qi = 0; qi < ph.qlen; ++qi) {
+      float M = -INFINITY;
+      for (int p0 = lane; p0 < npc; p0 += 32) {
+        const int id = __ldcg(m.req_plist + ph.pptr + p0);
+        M = fmaxf(M, __ldcg(w.part_m + (static_cast<size_t>(id) * H + head) * QP + qi));
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o2));
+      float L = 0.f, acc[DV];
+#pragma unroll
+      for (int j = 0; j < DV; ++j) acc[j] = 0.f;
+      for (int pj = 0; pj < npc; ++pj) {
+        const int id = __ldcg(m.req_plist + ph.pptr + pj);
+        const size_t pi = (static_cast<size_t>(id) * H + head) * QP + qi;
+        const float mp = __ldcg(w.part_m + pi);
+        const float f = mp == -INFINITY ? 0.f : exp2f(mp - M);
+        if (f == 0.f) continue;
+        L += __ldcg(w.part_l + pi) * f;
+        const float* src = w.part_o + pi * HD + DV * lane;
+#pragma unroll
+        for (int j = 0; j < DV; ++j) acc[j] += __ldcg(src + j) * f;
+      }
+      bf16* dst = out + static_cast<size_t>(ph.qs + qi) * D + head * HD + DV * lane;
+#pragma unroll
+      for (int j = 0; j < DV; ++j) dst[j] = __float2bfloat16_rn(acc[j] / L);
+    }
+    return;
+  }
+  const int pid = lane < npc ? __ldcg(m.req_plist + ph.pptr + lane) : 0;
+  for (int q0 = 0; q0 < ph.qlen; q0 += 8) {
+    float mq[8], lq[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool ok = lane < npc && q0 + i < ph.qlen;
+      const size_t pi = (static_cast<size_t>(pid) * H + head) * QP + q0 + i;
+      mq[i] = ok ? __ldcg(w.part_m + pi) : -INFINITY;
+      lq[i] = ok ? __ldcg(w.part_l + pi) : 0.f;
+    }
+    float f[8], L[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float M = mq[i];
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o2));
+      f[i] = mq[i] == -INFINITY ? 0.f : exp2f(mq[i] - M);
+      float l = lq[i] * f[i];
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) l += __shfl_xor_sync(kFull, l, o2);
+      L[i] = l;
+    }
+    float acc[8][DV];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < DV; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
+    for (int pj = 0; pj < npc; ++pj) {
+      const int id = __shfl_sync(kFull, pid, pj);
+      const float* src = w.part_o + ((static_cast<size_t>(id) * H + head) * QP + q0) * HD + DV * lane;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float fi = __shfl_sync(kFull, f[i], pj);
+        if (q0 + i >= ph.qlen || fi == 0.f) continue;
+        if constexpr (HD == 128) {
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(src + i * HD));
+          acc[i][0] += v.x * fi, acc[i][1] += v.y * fi, acc[i][2] += v.z * fi, acc[i][3] += v.w * fi;
+        } else {
+          const float2 v = __ldcg(reinterpret_cast<const float2*>(src + i * HD));
+          acc[i][0] += v.x * fi, acc[i][1] += v.y * fi;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (q0 + i >= ph.qlen) continue;
+      const float inv = 1.0f / L[i];
+      bf16* dst = out + static_cast<size_t>(ph.qs + q0 + i) * D + head * HD + DV * lane;
+#pragma unroll
+      for (int j = 0; j < DV; ++j) dst[j] = __float2bfloat16_rn(acc[i][j] * inv);
+    }
+  }
+}
+
 template <int HD, int NQT>
 __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ CUtensorMap tm_k,
                                                         const __grid_constant__ CUtensorMap tm_v, FwdMeta m,
@@ -355,54 +448,7 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
       if (!last) continue;
       if (stamp) w.st[8 * blockIdx.x + 6] = ptx::globaltimer();
       // ---- shared-max merge of the request's pieces in token order (attention.cpp:128-157)
-      const int npc = ph.npieces;
-      for (int qi = 0; qi < ph.qlen; ++qi) {
-        float M = -INFINITY;
-        for (int p0 = 0; p0 < npc; p0 += 32) {
-          const int pp = p0 + lane;
-          const int pid = pp < npc ? __ldcg(m.req_plist + ph.pptr + pp) : 0;
-          const float mp = pp < npc ? __ldcg(w.part_m + (static_cast<size_t>(pid) * H + head) * QP + qi) : -INFINITY;
-          M = fmaxf(M, mp);
-        }
-#pragma unroll
-        for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o2));
-        float L = 0.f;
-        float acc[HD / 32];
-#pragma unroll
-        for (int j = 0; j < HD / 32; ++j) acc[j] = 0.f;
-        for (int p0 = 0; p0 < npc; p0 += 32) {
-          const int pp = p0 + lane;
-          int pid = 0;
-          float f = 0.f;
-          if (pp < npc) {
-            pid = __ldcg(m.req_plist + ph.pptr + pp);
-            const size_t pi = (static_cast<size_t>(pid) * H + head) * QP + qi;
-            const float mp = __ldcg(w.part_m + pi);
-            f = mp == -INFINITY ? 0.f : exp2f(mp - M);
-            L += __ldcg(w.part_l + pi) * f;
-          }
-          const int cntp = min(32, npc - p0);
-          for (int j0 = 0; j0 < cntp; ++j0) {
-            const float fj = __shfl_sync(kFull, f, j0);
-            const int pj = __shfl_sync(kFull, pid, j0);
-            if (fj == 0.f) continue;
-            const float* src = w.part_o + ((static_cast<size_t>(pj) * H + head) * QP + qi) * HD + (HD / 32) * lane;
-            if constexpr (HD == 128) {
-              const float4 v = __ldcg(reinterpret_cast<const float4*>(src));
-              acc[0] += v.x * fj, acc[1] += v.y * fj, acc[2] += v.z * fj, acc[3] += v.w * fj;
-            } else {
-              const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
-              acc[0] += v.x * fj, acc[1] += v.y * fj;
-            }
-          }
-        }
-#pragma unroll
-        for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(kFull, L, o2);
-        const float inv = 1.0f / L;
-        bf16* dst = out + static_cast<size_t>(ph.qs + qi) * D + head * HD + (HD / 32) * lane;
-#pragma unroll
-        for (int j = 0; j < HD / 32; ++j) dst[j] = __float2bfloat16_rn(acc[j] * inv);
-      }
+      merge_pieces<HD, QP>(m, w, ph, head, H, D, out, lane);
     }
   }
   if (stamp) w.st[8 * blockIdx.x + 7] = ptx::globaltimer();
@@ -656,54 +702,7 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
       last = __shfl_sync(kFull, last, 0);
       if (!last) continue;
       if (stamp) w.st[8 * blockIdx.x + 6] = ptx::globaltimer();
-      const int npc = ph.npieces;
-      for (int qi = 0; qi < ph.qlen; ++qi) {
-        float M = -INFINITY;
-        for (int p0 = 0; p0 < npc; p0 += 32) {
-          const int pp = p0 + lane;
-          const int pid = pp < npc ? __ldcg(m.req_plist + ph.pptr + pp) : 0;
-          const float mp = pp < npc ? __ldcg(w.part_m + (static_cast<size_t>(pid) * H + head) * QP + qi) : -INFINITY;
-          M = fmaxf(M, mp);
-        }
-#pragma unroll
-        for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o2));
-        float L = 0.f;
-        float acc[HD / 32];
-#pragma unroll
-        for (int j = 0; j < HD / 32; ++j) acc[j] = 0.f;
-        for (int p0 = 0; p0 < npc; p0 += 32) {
-          const int pp = p0 + lane;
-          int pid = 0;
-          float f = 0.f;
-          if (pp < npc) {
-            pid = __ldcg(m.req_plist + ph.pptr + pp);
-            const size_t pi = (static_cast<size_t>(pid) * H + head) * QP + qi;
-            const float mp = __ldcg(w.part_m + pi);
-            f = mp == -INFINITY ? 0.f : exp2f(mp - M);
-            L += __ldcg(w.part_l + pi) * f;
-          }
-          const int cntp = min(32, npc - p0);
-          for (int j0 = 0; j0 < cntp; ++j0) {
-            const float fj = __shfl_sync(kFull, f, j0);
-            const int pj = __shfl_sync(kFull, pid, j0);
-            if (fj == 0.f) continue;
-            const float* src = w.part_o + ((static_cast<size_t>(pj) * H + head) * QP + qi) * HD + (HD / 32) * lane;
-            if constexpr (HD == 128) {
-              const float4 v = __ldcg(reinterpret_cast<const float4*>(src));
-              acc[0] += v.x * fj, acc[1] += v.y * fj, acc[2] += v.z * fj, acc[3] += v.w * fj;
-            } else {
-              const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
-              acc[0] += v.x * fj, acc[1] += v.y * fj;
-            }
-          }
-        }
-#pragma unroll
-        for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(kFull, L, o2);
-        const float inv = 1.0f / L;
-        bf16* dst = out + static_cast<size_t>(ph.qs + qi) * D + head * HD + (HD / 32) * lane;
-#pragma unroll
-        for (int j = 0; j < HD / 32; ++j) dst[j] = __float2bfloat16_rn(acc[j] * inv);
-      }
+      merge_pieces<HD, QP>(m, w, ph, head, H, D, out, lane);
     }
   }
   if (stamp) w.st[8 * blockIdx.x + 7] = ptx::globaltimer();

@@ -16,9 +16,10 @@ with open(sys.argv[1]) as f:
         rows[l].append(t)
         kinds[l] = k
 first = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+KIND = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 res = defaultdict(list)
 for l in sorted(rows):
-    if kinds[l] != 1 or l < first:
+    if kinds[l] != KIND or l < first:
         continue
     t = np.array(rows[l], dtype=float).reshape(-1, 8)
     t = t[t[:, 0] > 0]
