@@ -464,9 +464,11 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
 template <int HD>
 struct DecCfg {
   using C = Cfg<HD, 1>;
-  static constexpr int kMergeFloats = 8 * (2 + HD);  // per warp: m[8], l[8], o[8][HD]
-  static constexpr size_t kTotal =
-      1024 + C::kRing + kMaxPieces * 64 + kNW * C::kStages * 8 + kNW * kMergeFloats * 4;
+  static constexpr int kQ = kDecodeQ;                // queries per request (<= 2)
+  static constexpr int kMergeFloats = kQ * (2 + HD);  // per slot: m[kQ], l[kQ], o[kQ][HD]
+  static constexpr int kCluster = 2;                 // CTAs per item (tiles round robin over 2 x 4 warps)
+  static constexpr size_t kTotal = 1024 + C::kRing + kMaxPieces * 64 + kNW * C::kStages * 8 +
+                                   (kNW + kCluster) * kMergeFloats * 4;  // warp slots + cluster receive slots
 };
 
 template <int HD>
@@ -474,6 +476,7 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
                                                                AttnWork w, bf16* __restrict__ out, int n_items) {
   using C = Cfg<HD, 1>;
   using DC = DecCfg<HD>;
+  constexpr int CS = DC::kCluster;
   constexpr int S = C::kStages, DT = C::kDT, NR = C::kNR, QP = C::kQP;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
@@ -484,12 +487,17 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
   Piece* pcs = reinterpret_cast<Piece*>(smem + C::kRing);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::kRing + kMaxPieces * 64) + warp * S;
   float* mrg = reinterpret_cast<float*>(smem + C::kRing + kMaxPieces * 64 + kNW * S * 8);
-  float* my_m = mrg + warp * DC::kMergeFloats;  // [8]
-  float* my_l = my_m + 8;                        // [8]
-  float* my_o = my_m + 16;                       // [8][HD]
+  constexpr int kQ = DC::kQ;
+  float* my_m = mrg + warp * DC::kMergeFloats;  // [kQ]
+  float* my_l = my_m + kQ;                       // [kQ]
+  float* my_o = my_m + 2 * kQ;                   // [kQ][HD]
+  float* rcv = mrg + kNW * DC::kMergeFloats;     // [CS] CTA partials, filled over DSMEM (rank 0 reads)
   const int H = g.n_heads, D = H * HD;
   const float sl2 = g.scale * kLog2e;
-  const int item = blockIdx.x;  // (pack row, chunk) x head
+  const int item = blockIdx.x / CS;  // (pack row, chunk) x head; a cluster of CS CTAs per item
+  const int crank = static_cast<int>(ptx::cluster_ctarank());
+  const int vwarp = crank * kNW + warp, vwarps = CS * kNW;  // tiles round robin over the cluster's warps
+  ptx::cluster_arrive_relaxed();  // (waited before the first remote store: every CTA has started)
   if (lane == 0) {
     for (int s = 0; s < S; ++s) ptx::mbar_init(&bar[s], 1);
     ptx::fence_mbar_init();
@@ -499,7 +507,6 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
   if (stamp) w.st[8 * blockIdx.x] = ptx::globaltimer();
   bool dep_done = false;
   if (!w.early) ptx::grid_dep_wait(), dep_done = true;
-  if (item >= n_items * H) return;  // uniform per CTA
   const int head = item % H, rc = item / H;
   const int p_lo = m.item_ptr[rc], p_hi = m.item_ptr[rc + 1];
   const uint64_t pol = ptx::policy_evict_first();
@@ -515,8 +522,8 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
       dst[0] = src[0], dst[1] = src[1], dst[2] = src[2];
     }
     __syncthreads();
-    // this warp's tiles: every kNW-th tile of the pass's tile sequence (pieces in order)
-    int ik = 0, it = warp;
+    // this warp's tiles: every vwarps-th tile of the pass's tile sequence (pieces in order)
+    int ik = 0, it = vwarp;
     auto norm_pos = [&]() {
       while (ik < np && it * 16 >= pcs[ik].len) it -= (pcs[ik].len + 15) / 16, ++ik;
     };
@@ -535,7 +542,7 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
           ptx::bulk_load(dst + C::kHalf, g.v_cache + r0 * HD, C::kHalf, &bar[st], pol);
         }
         ++issued;
-        it += kNW;
+        it += vwarps;
         norm_pos();
       }
     };
@@ -573,9 +580,9 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
       for (int i = 0; i < NR; ++i) o[i] = olo[i] = 0.f;
       float mrun[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f};
       const int qbase = ph.kvlen - ph.qlen;
-      // tiles t of this piece with (tile_base + t) % kNW == warp
-      int t = (warp - tile_base % kNW + kNW) % kNW;
-      for (; t < n_tiles; t += kNW) {
+      // tiles t of this piece with (tile_base + t) % vwarps == vwarp
+      int t = (vwarp - tile_base % vwarps + vwarps) % vwarps;
+      for (; t < n_tiles; t += vwarps) {
         const int st = consumed % S;
         ptx::mbar_wait(&bar[st], static_cast<uint32_t>((consumed / S) & 1));
         const uint32_t kb = ptx::smem_u32(ring + st * C::kStage);
@@ -657,13 +664,15 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
         const int e = i & 3, dt = i >> 2;
         const int qi = 2 * cq + (e & 1);
         const int dim = 16 * dt + gq + (e >> 1) * 8;
+        if (qi >= kQ) continue;
         my_o[qi * HD + dim] = o[i];
         if (dt == 0 && gq == 0 && e < 2) my_m[qi] = mrun[e], my_l[qi] = lsum[e];
       }
       __syncthreads();
-      // ---- fixed-order merge of the four warps' partials; output or split-KV partial
-      const bool single = ph.npieces == 1;
-      const int pidx = pb + k;
+      // ---- fixed-order merge of the four warps' partials into this CTA's partial, stored
+      // into receive slot `crank` of the cluster's rank-0 CTA (shared memory over DSMEM)
+      if (k == 0 && pb == p_lo) ptx::cluster_wait();  // every CTA of the cluster has started
+      const uint32_t slot0 = ptx::mapa(ptx::smem_u32(rcv + crank * DC::kMergeFloats), 0);
       for (int x = threadIdx.x; x < ph.qlen * HD; x += kThreads) {
         const int qi = x / HD, dim = x % HD;
         float M = -INFINITY;
@@ -674,20 +683,47 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
         for (int ww = 0; ww < kNW; ++ww) {
           const float* wm = mrg + ww * DC::kMergeFloats;
           const float f = wm[qi] == -INFINITY ? 0.f : exp2f(wm[qi] - M);
-          L += wm[8 + qi] * f;
-          O += wm[16 + qi * HD + dim] * f;
+          L += wm[kQ + qi] * f;
+          O += wm[2 * kQ + qi * HD + dim] * f;
         }
-        if (single) {
-          out[static_cast<size_t>(ph.qs + qi) * D + head * HD + dim] = __float2bfloat16_rn(O / L);
-        } else {
-          const size_t pi = (static_cast<size_t>(pidx) * H + head) * QP + qi;
-          w.part_o[pi * HD + dim] = O;
-          if (dim == 0) w.part_m[pi] = M, w.part_l[pi] = L;
+        ptx::st_cluster_f32(slot0 + 4u * (2 * kQ + qi * HD + dim), O);
+        if (dim == 0) ptx::st_cluster_f32(slot0 + 4u * qi, M), ptx::st_cluster_f32(slot0 + 4u * (kQ + qi), L);
+      }
+      ptx::cluster_arrive();
+      ptx::cluster_wait();  // rank 0 holds every CTA partial of the piece
+      const bool single = ph.npieces == 1;
+      const int pidx = pb + k;
+      if (crank == 0) {
+        for (int x = threadIdx.x; x < ph.qlen * HD; x += kThreads) {
+          const int qi = x / HD, dim = x % HD;
+          float M = -INFINITY;
+#pragma unroll
+          for (int r = 0; r < CS; ++r) M = fmaxf(M, rcv[r * DC::kMergeFloats + qi]);
+          float L = 0.f, O = 0.f;
+#pragma unroll
+          for (int r = 0; r < CS; ++r) {
+            const float* rm = rcv + r * DC::kMergeFloats;
+            const float f = rm[qi] == -INFINITY ? 0.f : exp2f(rm[qi] - M);
+            L += rm[kQ + qi] * f;
+            O += rm[2 * kQ + qi * HD + dim] * f;
+          }
+          if (single) {
+            out[static_cast<size_t>(ph.qs + qi) * D + head * HD + dim] = __float2bfloat16_rn(O / L);
+          } else {
+            const size_t pi = (static_cast<size_t>(pidx) * H + head) * QP + qi;
+            w.part_o[pi * HD + dim] = O;
+            if (dim == 0) w.part_m[pi] = M, w.part_l[pi] = L;
+          }
         }
       }
-      __syncthreads();  // merge slots reused by the next piece; partial complete
+      if (pb + k + 1 < p_hi) {  // another piece follows: slots are reused
+        ptx::cluster_arrive();
+        ptx::cluster_wait();
+      } else {
+        __syncthreads();  // partial complete before the arrival below
+      }
       if (stamp && k == 0) w.st[8 * blockIdx.x + 5] = ptx::globaltimer();
-      if (single || warp != 0) continue;
+      if (single || crank != 0 || warp != 0) continue;
       // ---- arrival: the CTA completing the last piece of (request, head) merges them
       int last = 0;
       if (lane == 0) {
@@ -727,7 +763,15 @@ void launch_decode(const FwdMeta& m, int n_rows, const AttnGeom& g, const float*
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cfg.stream = s;
-  cfg.gridDim = dim3(n_items * g.n_heads);  // one CTA per (row, chunk, head)
+  cudaLaunchAttribute attr2[2];
+  attr2[0] = attr[0];
+  attr2[1].id = cudaLaunchAttributeClusterDimension;
+  attr2[1].val.clusterDim.x = DC::kCluster;
+  attr2[1].val.clusterDim.y = 1;
+  attr2[1].val.clusterDim.z = 1;
+  cfg.attrs = attr2;
+  cfg.numAttrs = 2;
+  cfg.gridDim = dim3(n_items * g.n_heads * DC::kCluster);  // one cluster per (row, chunk, head)
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = DC::kTotal;
   cudaLaunchKernelEx(&cfg, attn_decode_kernel<HD>, m, g, q, w, out, n_items);
@@ -774,7 +818,7 @@ void launch_hd(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& 
 }  // namespace
 
 int attn_ctas(int n_rows, int chunks, int heads, int qmax) {
-  if (qmax <= kDecodeQ) return n_rows * std::max(1, chunks) * heads;
+  if (qmax <= kDecodeQ) return n_rows * std::max(1, chunks) * heads * 2;  // DecCfg::kCluster
   return (n_rows * std::max(1, chunks) * heads + kNW - 1) / kNW;
 }
 
