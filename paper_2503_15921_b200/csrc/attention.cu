@@ -549,6 +549,7 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
     try_issue();
     if (!dep_done) {
       ptx::grid_dep_wait();
+      ptx::grid_dep_launch();
       dep_done = true;
       if (stamp) w.st[8 * blockIdx.x + 1] = ptx::globaltimer();
       try_issue();
@@ -742,7 +743,7 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
     }
   }
   if (stamp) w.st[8 * blockIdx.x + 7] = ptx::globaltimer();
-  ptx::grid_dep_launch();
+
 }
 
 template <int HD>

@@ -189,6 +189,9 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
   }
   __syncthreads();
   ptx::grid_dep_wait();
+  // dependents may launch now: their prologues only read weights and data that is final
+  // once this grid's own dependency wait has returned
+  ptx::grid_dep_launch();
   if (stamp) a.st[4 * u + 1] = ptx::globaltimer();
 
   // ---- this warp's 32-k steps: atoms warp, warp + NW, ...; two steps per atom
@@ -292,7 +295,6 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
     }
   }
   if (stamp) a.st[4 * u + 2] = ptx::globaltimer();
-  if (!(a.dbg & 32)) ptx::grid_dep_launch();
 
   // ---- fixed-order cross-warp reduction; warp (m, nt) finishes tile m x n-tile nt
 #pragma unroll
