@@ -389,6 +389,7 @@ __global__ void __launch_bounds__(256) embed_ss_kernel(const bf16* __restrict__ 
                                                        int T, int D, float* __restrict__ h, float* __restrict__ ssp) {
   __shared__ float red[32];
   ptx::grid_dep_wait();
+  ptx::grid_dep_launch();
   const int t = blockIdx.x;
   const bf16* e = emb + static_cast<size_t>(tok[t]) * D;
   float ss = 0.f;
@@ -401,7 +402,6 @@ __global__ void __launch_bounds__(256) embed_ss_kernel(const bf16* __restrict__ 
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
   if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
   __syncthreads();
-  ptx::grid_dep_launch();
   if (threadIdx.x == 0) {
     float tot = 0.f;
     for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) tot += red[w];
@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(256) norm_ss_kernel(const float* __restrict__ 
                                                       int n_ssp, int T, int D, float eps, bf16* __restrict__ xn) {
   __shared__ float inv_s;
   ptx::grid_dep_wait();
+  ptx::grid_dep_launch();
   const int t = blockIdx.x;
   if (threadIdx.x < 32) {
     float ss = 0.f;
@@ -424,7 +425,6 @@ __global__ void __launch_bounds__(256) norm_ss_kernel(const float* __restrict__ 
       inv_s = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, static_cast<float>(D)), eps)));
   }
   __syncthreads();
-  ptx::grid_dep_launch();
   const float inv = inv_s;
   for (int i = 4 * threadIdx.x; i < D; i += 4 * blockDim.x) {
     const float4 v = *reinterpret_cast<const float4*>(h + static_cast<size_t>(t) * D + i);

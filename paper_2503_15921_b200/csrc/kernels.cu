@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
   const int W = st.window;
 
   ptx::grid_dep_wait();
+  ptx::grid_dep_launch();  // the next kernel's prologue reads nothing of ours before its wait
   // ---- collect the previous draft step's argmax (one warp per request)
   if (a.mode == kMetaDraftK || a.mode == kMetaCollect) {
     for (int r = warp; r < n; r += kMetaThreads / 32) {
@@ -121,7 +122,6 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
       const int slot = a.list[r];
       st.ssm_len[static_cast<size_t>(a.ssm) * st.slots + slot] = st.committed[slot] + W - 1;
     }
-    ptx::grid_dep_launch();
     return;
   }
   // ---- rows and requests
@@ -347,7 +347,6 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
       }
     }
   }
-  ptx::grid_dep_launch();
 }
 
 // ------------------------------------------------------------------ norms
