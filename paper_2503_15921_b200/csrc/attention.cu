@@ -98,34 +98,48 @@ struct Piece {
 // pieces in token order. Lanes own pieces for the max / sum and head dims for the
 // output; every query's (max, sum) loads of all pieces are issued together, then one
 // pass over the pieces accumulates up to 8 queries' outputs (independent loads).
-template <int HD, int QP>
+template <int HD, int QP, bool kBatched>
 __device__ __forceinline__ void merge_pieces(const FwdMeta& m, const AttnWork& w, const Piece& ph, int head, int H,
                                              int D, bf16* __restrict__ out, int lane) {
   constexpr int DV = HD / 32;  // head dims per lane
   const int npc = ph.npieces;
-  if (npc > 32) {  // rare (long requests split over many chunks): query-serial merge
+  if (npc > 32 || !kBatched) {  // query-serial merge: many pieces, or register-tight kernels
     for (int qi = 0; qi < ph.qlen; ++qi) {
       float M = -INFINITY;
-      for (int p0 = lane; p0 < npc; p0 += 32) {
-        const int id = __ldcg(m.req_plist + ph.pptr + p0);
-        M = fmaxf(M, __ldcg(w.part_m + (static_cast<size_t>(id) * H + head) * QP + qi));
+      for (int p0 = 0; p0 < npc; p0 += 32) {
+        const int pp = p0 + lane;
+        const int id = pp < npc ? __ldcg(m.req_plist + ph.pptr + pp) : 0;
+        const float mp = pp < npc ? __ldcg(w.part_m + (static_cast<size_t>(id) * H + head) * QP + qi) : -INFINITY;
+        M = fmaxf(M, mp);
       }
 #pragma unroll
       for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o2));
       float L = 0.f, acc[DV];
 #pragma unroll
       for (int j = 0; j < DV; ++j) acc[j] = 0.f;
-      for (int pj = 0; pj < npc; ++pj) {
-        const int id = __ldcg(m.req_plist + ph.pptr + pj);
-        const size_t pi = (static_cast<size_t>(id) * H + head) * QP + qi;
-        const float mp = __ldcg(w.part_m + pi);
-        const float f = mp == -INFINITY ? 0.f : exp2f(mp - M);
-        if (f == 0.f) continue;
-        L += __ldcg(w.part_l + pi) * f;
-        const float* src = w.part_o + pi * HD + DV * lane;
+      for (int p0 = 0; p0 < npc; p0 += 32) {
+        const int pp = p0 + lane;
+        int id = 0;
+        float f = 0.f;
+        if (pp < npc) {
+          id = __ldcg(m.req_plist + ph.pptr + pp);
+          const size_t pi = (static_cast<size_t>(id) * H + head) * QP + qi;
+          const float mp = __ldcg(w.part_m + pi);
+          f = mp == -INFINITY ? 0.f : exp2f(mp - M);
+          L += __ldcg(w.part_l + pi) * f;
+        }
+        const int cntp = min(32, npc - p0);
+        for (int j0 = 0; j0 < cntp; ++j0) {
+          const float fj = __shfl_sync(kFull, f, j0);
+          const int pj = __shfl_sync(kFull, id, j0);
+          if (fj == 0.f) continue;
+          const float* src = w.part_o + ((static_cast<size_t>(pj) * H + head) * QP + qi) * HD + DV * lane;
 #pragma unroll
-        for (int j = 0; j < DV; ++j) acc[j] += __ldcg(src + j) * f;
+          for (int j = 0; j < DV; ++j) acc[j] += __ldcg(src + j) * fj;
+        }
       }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(kFull, L, o2);
       bf16* dst = out + static_cast<size_t>(ph.qs + qi) * D + head * HD + DV * lane;
 #pragma unroll
       for (int j = 0; j < DV; ++j) dst[j] = __float2bfloat16_rn(acc[j] / L);
@@ -448,7 +462,7 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
       if (!last) continue;
       if (stamp) w.st[8 * blockIdx.x + 6] = ptx::globaltimer();
       // ---- shared-max merge of the request's pieces in token order (attention.cpp:128-157)
-      merge_pieces<HD, QP>(m, w, ph, head, H, D, out, lane);
+      merge_pieces<HD, QP, QP == 8>(m, w, ph, head, H, D, out, lane);
     }
   }
   if (stamp) w.st[8 * blockIdx.x + 7] = ptx::globaltimer();
@@ -739,7 +753,7 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
       last = __shfl_sync(kFull, last, 0);
       if (!last) continue;
       if (stamp) w.st[8 * blockIdx.x + 6] = ptx::globaltimer();
-      merge_pieces<HD, QP>(m, w, ph, head, H, D, out, lane);
+      merge_pieces<HD, QP, QP == 8>(m, w, ph, head, H, D, out, lane);
     }
   }
   if (stamp) w.st[8 * blockIdx.x + 7] = ptx::globaltimer();

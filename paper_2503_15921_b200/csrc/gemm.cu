@@ -29,7 +29,7 @@ constexpr size_t kRedBytes = 4 * 256 * 8;                // argmax cross-warp sc
 // PARTIAL epilogue: fp32 tiles leave through kStgSlots staging slots of 16 tokens x 128
 // features (8 KB), one TMA tensor store per slot, so storing a piece neither waits for the
 // ring to drain nor competes with the weight stream for LSU bandwidth.
-constexpr int kStgSlots = 8;
+constexpr int kStgSlots = 4;
 constexpr size_t kStgBytes = static_cast<size_t>(kStgSlots) * 16 * kBlockM * 4;
 constexpr size_t kBarBytes = 256;
 
