@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         Piece q;
         int s = 0;
         while (s < stages && pre.next(pm, n_tiles, q)) {
-          const int mt = q.tile % pm.n_mtiles;
+          const int mt = q.tile / pm.n_ntiles;
           for (int kb = q.kb0; kb < q.kb1 && s < stages; ++kb, ++s) {
             ptx::mbar_arrive_expect_tx(&full_bar[s], kTileABytes + ((dbg & 1) ? 0u : tile_b_bytes));
             ptx::bulk_load(smem_a + static_cast<size_t>(s) * kTileABytes,
@@ -160,8 +160,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (st) st[1] = ptx::globaltimer();
       int issued = 0;
       while (it.next(pm, n_tiles, p)) {
-        const int mt = p.tile % pm.n_mtiles;
-        const int nt = p.tile / pm.n_mtiles;
+        const int mt = p.tile / pm.n_ntiles;
+        const int nt = p.tile % pm.n_ntiles;
         for (int kb = p.kb0; kb < p.kb1; ++kb) {
           if (issued >= prefetched) {
             ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int iter = 0, chunk = 0;
     while (it.next(pm, n_tiles, p)) {
       const int acc = iter & 1;
-      const int mt = p.tile % pm.n_mtiles;
-      const int nt = p.tile / pm.n_mtiles;
+      const int mt = p.tile / pm.n_ntiles;
+      const int nt = p.tile % pm.n_ntiles;
       ptx::mbar_wait(&tfull_bar[acc], (iter >> 1) & 1);
       ptx::tc_fence_after();
       if (st && ew == 0 && lane == 0 && iter == 0) st[4] = ptx::globaltimer();
@@ -378,6 +378,7 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
   m.mode = mode;
   m.kb = p.kb;
   m.n_mtiles = p.n_mtiles;
+  m.n_ntiles = p.n_ntiles;
   m.bn = p.bn;
   m.units = n_tiles * p.kb;
   if (mode == kGemmPartial) {
@@ -391,7 +392,7 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
     int mp = 1;
     p.tile_pieces.resize(n_tiles);
     for (long long tile = 0; tile < n_tiles; ++tile) {
-      const int np = m.pieces(static_cast<int>((tile / p.n_mtiles) * p.bn), static_cast<int>((tile % p.n_mtiles) * kBlockM));
+      const int np = m.pieces(static_cast<int>((tile % p.n_ntiles) * p.bn), static_cast<int>((tile / p.n_ntiles) * kBlockM));
       p.tile_pieces[tile] = static_cast<uint8_t>(np);
       mp = std::max(mp, np);
     }

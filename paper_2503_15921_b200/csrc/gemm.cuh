@@ -33,6 +33,8 @@ struct PieceMap {
   int grid;         // CTAs
   int kb;           // 64-wide k blocks per tile
   int n_mtiles;     // 128-row tiles over N_out
+  int n_ntiles;     // token tiles; tile = mt * n_ntiles + nt (token tiles of one weight tile adjacent,
+                    // so the CTAs streaming them run concurrently and share each weight atom in L2)
   int bn;           // token tile
   int mode;         // GemmMode
   const uint8_t* tbl = nullptr;  // device: pieces per tile (filled by the host at plan time)
@@ -44,10 +46,10 @@ struct PieceMap {
   // Number of partial slots written for (token t, feature n).
   __host__ __device__ __forceinline__ int pieces(int t, int n) const {
     if (mode != kGemmPartial) return 1;
-    const long long tile = static_cast<long long>(t / bn) * n_mtiles + n / 128;
+    const long long tile = static_cast<long long>(n / 128) * n_ntiles + t / bn;
     return cta_of(tile * kb + kb - 1) - cta_of(tile * kb) + 1;
   }
-  __device__ __forceinline__ int tile_pieces(int t, int n) const { return tbl[(t / bn) * n_mtiles + n / 128]; }
+  __device__ __forceinline__ int tile_pieces(int t, int n) const { return tbl[(n / 128) * n_ntiles + t / bn]; }
 };
 
 struct GemmPlan {
