@@ -316,9 +316,13 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
           ql[nt][kt][hh] = pack_bf2(x - hx, y - hy);
         }
       }
-      float o[NR], olo[NR];
+      // NQT > 1: the lo plane accumulates into o (register budget); NQT = 1: separate chain
+      constexpr int NRL = NQT == 1 ? NR : 1;
+      float o[NR], olo[NRL];
 #pragma unroll
-      for (int i = 0; i < NR; ++i) o[i] = olo[i] = 0.f;
+      for (int i = 0; i < NR; ++i) o[i] = 0.f;
+#pragma unroll
+      for (int i = 0; i < NRL; ++i) olo[i] = 0.f;
       float mrun[NQT][2], lsum[NQT][2];
 #pragma unroll
       for (int nt = 0; nt < NQT; ++nt) mrun[nt][0] = mrun[nt][1] = -INFINITY, lsum[nt][0] = lsum[nt][1] = 0.f;
@@ -386,8 +390,10 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
           for (int dt = 0; dt < DT; ++dt) {
             float* oo = o + (nt * DT + dt) * 4;
             oo[0] *= corr[0], oo[1] *= corr[1], oo[2] *= corr[0], oo[3] *= corr[1];
-            float* ol = olo + (nt * DT + dt) * 4;
-            ol[0] *= corr[0], ol[1] *= corr[1], ol[2] *= corr[0], ol[3] *= corr[1];
+            if constexpr (NQT == 1) {
+              float* ol = olo + (nt * DT + dt) * 4;
+              ol[0] *= corr[0], ol[1] *= corr[1], ol[2] *= corr[0], ol[3] *= corr[1];
+            }
           }
           // P^T as the B operand: movmatrix turns the (key g, queries 2c..2c+1)
           // accumulator pairs into (query g, keys 2c..2c+1) fragments
@@ -406,7 +412,10 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
 #pragma unroll
           for (int nt = 0; nt < NQT; ++nt) {
             mma16816(o + (nt * DT + dt) * 4, a, ph_[nt][0], ph_[nt][1]);
-            mma16816(olo + (nt * DT + dt) * 4, a, pl_[nt][0], pl_[nt][1]);
+            if constexpr (NQT == 1)
+              mma16816(olo + (nt * DT + dt) * 4, a, pl_[nt][0], pl_[nt][1]);
+            else
+              mma16816(o + (nt * DT + dt) * 4, a, pl_[nt][0], pl_[nt][1]);
           }
         }
         ++consumed;
@@ -414,8 +423,10 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
         try_issue();
       }
 
+      if constexpr (NQT == 1) {
 #pragma unroll
-      for (int i = 0; i < NR; ++i) o[i] += olo[i];
+        for (int i = 0; i < NR; ++i) o[i] += olo[i];
+      }
       if (stamp) w.st[8 * blockIdx.x + 4] = ptx::globaltimer();
       // ---- piece epilogue: column sums, then the output (single piece) or a split-KV partial
 #pragma unroll
