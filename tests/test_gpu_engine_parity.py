@@ -97,3 +97,25 @@ def test_device_resident_rounds_match_host_rounds():
     assert ms > 0
     for s in range(B):
         assert np.array_equal(dev.tokens(s), host.tokens(s))
+
+
+def test_wide_batch_mixed_draft_paths_vs_oracle():
+    """64 requests over 2 SSMs: draft step 0 runs 64 rows per SSM through the generic
+    path (> 32 rows), steps 1-3 run 32 rows through the fused draft projections with
+    four token tiles and the 2-CTA few-query attention. Same tie-aware oracle contract."""
+    b = 64
+    prompts = synthetic_prompts(b, 16, 64, TINY_TARGET.vocab, 2604)
+    gpu = Engine(TINY_TARGET, TINY_SSMS, max_requests=b, max_ctx=CTX, window=W)
+    cpu = OracleEngine(TINY_TARGET, TINY_SSMS, max_requests=b, max_ctx=CTX, window=W)
+    gpu.prefill(range(b), prompts)
+    cpu.prefill(range(b), prompts)
+    slots = np.arange(b, dtype=np.int32)
+    assign = np.array([0, 1] * (b // 2), np.int32)
+    for r in range(4):
+        g = gpu.round(slots, assign)
+        c = cpu.round(slots, assign, hints=g, tau=TAU)
+        for k in ("drafts", "target", "accepted", "bonus", "committed"):
+            assert np.array_equal(g[k], c[k]), (r, k)
+    assert cpu.forced() <= MAX_FORCED * 4 * b * (2 * W + 1), cpu.forced()
+    for s in range(b):
+        assert np.array_equal(gpu.tokens(s), cpu.tokens(s))
