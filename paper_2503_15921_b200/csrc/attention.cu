@@ -33,8 +33,15 @@ namespace spin {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kNW = 4;                   // warps per CTA
+constexpr int kNW = 4;                   // warps per CTA (few-query kernel)
 constexpr int kThreads = 32 * kNW;
+// attn_kernel: independent warps, so CTAs of one warp let the block scheduler spread the
+// (row, chunk, head) items evenly over the SMs (4-warp CTAs left 108 SMs with 8 items and
+// 40 with 4 at config 2)
+#ifndef SPIN_ATTN_VW
+#define SPIN_ATTN_VW 1
+#endif
+constexpr int kVW = SPIN_ATTN_VW;
 constexpr int kMaxPieces = 16;           // piece records staged per warp per pass
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -76,17 +83,18 @@ __device__ __forceinline__ uint32_t kvoff(int row, int chunk, int base) {
   return static_cast<uint32_t>(row * (HD * 2) + (chunk >> 3) * 128 + (((chunk & 7) ^ ((row + base) & 7)) << 4));
 }
 
-template <int HD, int NQT>
+template <int HD, int NQT, int NW = kNW>
 struct Cfg {
+  static constexpr int kWarps = NW;
   static constexpr int kStages = HD == 128 ? 3 : 4;     // per-warp ring depth
   static constexpr uint32_t kHalf = 16 * HD * 2;        // K or V of one 16-key tile
   static constexpr uint32_t kStage = 2 * kHalf;
-  static constexpr uint32_t kRing = kNW * kStages * kStage;
+  static constexpr uint32_t kRing = NW * kStages * kStage;
   static constexpr int kDT = HD / 16;                   // 16-dim tiles
   static constexpr int kNR = kDT * NQT * 4;             // O^T fragment registers per thread
   static constexpr int kQP = 8 * NQT;                   // padded queries
   static constexpr int kQF = kDT * NQT * 4;             // raw Q floats per thread
-  static constexpr size_t kTotal = 1024 + kRing + kNW * kMaxPieces * 64 + kNW * kStages * 8;
+  static constexpr size_t kTotal = 1024 + kRing + NW * kMaxPieces * 64 + NW * kStages * 8;
 };
 
 // Piece record written by meta_kernel (FwdMeta::pieces).
@@ -202,11 +210,11 @@ __device__ __forceinline__ void merge_pieces(const FwdMeta& m, const AttnWork& w
 }
 
 template <int HD, int NQT>
-__global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ CUtensorMap tm_k,
+__global__ void __launch_bounds__(32 * kVW) attn_kernel(const __grid_constant__ CUtensorMap tm_k,
                                                         const __grid_constant__ CUtensorMap tm_v, FwdMeta m,
                                                         AttnGeom g, const float* __restrict__ q, AttnWork w,
                                                         bf16* __restrict__ out, int n_items) {
-  using C = Cfg<HD, NQT>;
+  using C = Cfg<HD, NQT, kVW>;
   constexpr int S = C::kStages, DT = C::kDT, NR = C::kNR, QP = C::kQP, QF = C::kQF;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
@@ -215,11 +223,11 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __grid_constant__ 
   const int gq = lane >> 2, cq = lane & 3;
   uint8_t* ring = smem + static_cast<size_t>(warp) * S * C::kStage;
   Piece* pcs = reinterpret_cast<Piece*>(smem + C::kRing) + warp * kMaxPieces;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::kRing + kNW * kMaxPieces * 64) + warp * S;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::kRing + kVW * kMaxPieces * 64) + warp * S;
   const int H = g.n_heads, D = H * HD;
   const float sl2 = g.scale * kLog2e;
 
-  const int item = blockIdx.x * kNW + warp;  // (pack row, chunk) x head, one per warp
+  const int item = blockIdx.x * kVW + warp;  // (pack row, chunk) x head, one per warp
   if (lane == 0) {
     for (int s = 0; s < S; ++s) ptx::mbar_init(&bar[s], 1);
     ptx::fence_mbar_init();
@@ -806,7 +814,7 @@ void launch_decode(const FwdMeta& m, int n_rows, const AttnGeom& g, const float*
 template <int HD, int NQT>
 void launch_t(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m, int n_rows, const AttnGeom& g,
               const float* q, const AttnWork& w, bf16* out, cudaStream_t s) {
-  using C = Cfg<HD, NQT>;
+  using C = Cfg<HD, NQT, kVW>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(attn_kernel<HD, NQT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -827,8 +835,8 @@ void launch_t(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cfg.stream = s;
-  cfg.gridDim = dim3((n_items * g.n_heads + kNW - 1) / kNW);  // one warp per (row, chunk, head)
-  cfg.blockDim = dim3(kThreads);
+  cfg.gridDim = dim3((n_items * g.n_heads + kVW - 1) / kVW);  // one warp per (row, chunk, head)
+  cfg.blockDim = dim3(32 * kVW);
   cfg.dynamicSmemBytes = C::kTotal;
   cudaLaunchKernelEx(&cfg, attn_kernel<HD, NQT>, tm_k, tm_v, m, g, q, wk, out, n_items);
 }
@@ -845,7 +853,7 @@ void launch_hd(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& 
 
 int attn_ctas(int n_rows, int chunks, int heads, int qmax) {
   if (qmax <= kDecodeQ) return n_rows * std::max(1, chunks) * heads * 2;  // DecCfg::kCluster
-  return (n_rows * std::max(1, chunks) * heads + kNW - 1) / kNW;
+  return (n_rows * std::max(1, chunks) * heads + kVW - 1) / kVW;
 }
 
 int attn_chunks(int rows, int heads, int num_sms, int qmax) {
