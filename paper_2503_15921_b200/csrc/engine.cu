@@ -315,7 +315,6 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
       prof_end(s, 0);
     }
     prof_begin(base + 2, s);
-    ++launches_;  // attention + combine
     aw.st = stamp_layer ? stamp_slot(14, 2 * attn_ctas(sh.rows, aw.chunks, m.H, sh.qmax)) : nullptr;
     if (!(skip & 8)) launch_attention(m.tm_k, m.tm_v, ln.meta, sh.rows, sh.R, g, ln.q, aw, ln.attn, s);
     aw.st = nullptr;
