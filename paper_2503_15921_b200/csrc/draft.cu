@@ -19,7 +19,7 @@
 //     fixed order, so no normalised copy of the activations is materialised and
 //     the matmul never waits on the sums;
 //   * the token operand is loaded straight from L2 into mma.sync B fragments:
-//     each lane reads 8 consecutive k of one token (16 B bf16 / 32 B fp32) and the
+//     each lane reads 8 consecutive k of one token (16 B of bf16) and the
 //     A fragment takes the same 8 k of a weight row from shared memory, so the
 //     k order inside a 32-k step is a permutation shared by A and B (the dot
 //     product is unchanged).
@@ -110,7 +110,7 @@ __global__ void slab_weights_kernel(const bf16* __restrict__ tiled, bf16* __rest
 template <int NW, int NT, int MT, bool NORM>
 struct DpCfg {
   static constexpr int kSlab = MT * 16 * 128;                  // bytes of one 64-k atom of the unit
-  static constexpr int kXRegs = NT * (NORM ? 8 : 4);           // registers per 32-k step of the token operand
+  static constexpr int kXRegs = NT * 4;                        // registers per 32-k step of the token operand
   static constexpr int kBatch = kXRegs >= 48 ? 1 : 48 / kXRegs;  // 32-k steps loaded per round trip
   static constexpr int kRed = NW * MT * NT * 32 * 4;           // cross-warp reduction floats
   static constexpr int kAtomsPerCopy = 8 / MT;                 // 16-KB bulk copies
@@ -196,9 +196,9 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
 
   // ---- this warp's 32-k steps: atoms warp, warp + NW, ...; two steps per atom
   const int n_steps = warp < KB ? 2 * ((KB - warp + NW - 1) / NW) : 0;
-  using XR = typename std::conditional<NORM, float4, uint4>::type;
-  constexpr int XPer = NORM ? 2 : 1;  // vector loads per (step, n-tile)
-  XR xr[C::kBatch][NT][XPer];
+  // token operand: bf16 rows (the residual producers keep a bf16 copy of h beside the
+  // fp32 stream, so the norm consumers load 16 B per 8 k like the others)
+  uint4 xr[C::kBatch][NT];
   auto load_batch = [&](int s0) {
 #pragma unroll
     for (int b = 0; b < C::kBatch; ++b) {
@@ -209,14 +209,8 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
       for (int nt = 0; nt < NT; ++nt) {
         const int tok = nt * 8 + g;
         const bool ok = s < n_steps && tok < T && kk < K && !(a.dbg & 2);
-        if constexpr (NORM) {
-          const float4* p = reinterpret_cast<const float4*>(a.h + static_cast<size_t>(tok) * K + kk);
-          xr[b][nt][0] = ok ? __ldcg(p) : make_float4(0.f, 0.f, 0.f, 0.f);
-          xr[b][nt][1] = ok ? __ldcg(p + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-        } else {
-          xr[b][nt][0] = ok ? __ldcg(reinterpret_cast<const uint4*>(a.x + static_cast<size_t>(tok) * K + kk))
-                            : make_uint4(0u, 0u, 0u, 0u);
-        }
+        xr[b][nt] = ok ? __ldcg(reinterpret_cast<const uint4*>(a.x + static_cast<size_t>(tok) * K + kk))
+                       : make_uint4(0u, 0u, 0u, 0u);
       }
     }
   };
@@ -275,17 +269,8 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        uint32_t b0, b1, b2, b3;
-        if constexpr (NORM) {
-          const float4 x0 = xr[b][nt][0], x1 = xr[b][nt][1];
-          b0 = pack_bf16(x0.x, x0.y);
-          b1 = pack_bf16(x0.z, x0.w);
-          b2 = pack_bf16(x1.x, x1.y);
-          b3 = pack_bf16(x1.z, x1.w);
-        } else {
-          const uint4 x = xr[b][nt][0];
-          b0 = x.x, b1 = x.y, b2 = x.z, b3 = x.w;
-        }
+        const uint4 x = xr[b][nt];
+        const uint32_t b0 = x.x, b1 = x.y, b2 = x.z, b3 = x.w;
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
           mma16816(acc[m][nt], wa[m].x, wb[m].x, wa[m].y, wb[m].y, b0, b1);
@@ -369,6 +354,8 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
       const float h0 = __fadd_rn(pre[e][0], c[e]), h1 = __fadd_rn(pre[e][1], c[2 + e]);
       hr[n0] = h0;
       hr[n1] = h1;
+      a.hb[static_cast<size_t>(tt) * D + n0] = __float2bfloat16_rn(h0);
+      a.hb[static_cast<size_t>(tt) * D + n1] = __float2bfloat16_rn(h1);
       ss[e] = __fadd_rn(__fmul_rn(h0, h0), __fmul_rn(h1, h1));
     }
 #pragma unroll
@@ -386,7 +373,8 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
 
 // h = embedding rows (fp32), ssp[0][t] = sum of squares (one unit).
 __global__ void __launch_bounds__(256) embed_ss_kernel(const bf16* __restrict__ emb, const int32_t* __restrict__ tok,
-                                                       int T, int D, float* __restrict__ h, float* __restrict__ ssp) {
+                                                       int T, int D, float* __restrict__ h, bf16* __restrict__ hb,
+                                                       float* __restrict__ ssp) {
   __shared__ float red[32];
   ptx::grid_dep_wait();
   ptx::grid_dep_launch();
@@ -394,8 +382,10 @@ __global__ void __launch_bounds__(256) embed_ss_kernel(const bf16* __restrict__ 
   const bf16* e = emb + static_cast<size_t>(tok[t]) * D;
   float ss = 0.f;
   for (int i = 2 * threadIdx.x; i < D; i += 2 * blockDim.x) {
-    const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(e + i));
+    const __nv_bfloat162 raw = *reinterpret_cast<const __nv_bfloat162*>(e + i);
+    const float2 v = __bfloat1622float2(raw);
     *reinterpret_cast<float2*>(h + static_cast<size_t>(t) * D + i) = v;
+    *reinterpret_cast<__nv_bfloat162*>(hb + static_cast<size_t>(t) * D + i) = raw;
     ss += v.x * v.x + v.y * v.y;
   }
 #pragma unroll
@@ -513,8 +503,9 @@ cudaError_t launch_draft_proj(const DraftProj& a_in, cudaStream_t s) {
   }
 }
 
-void launch_embed_ss(const bf16* emb, const FwdMeta& m, int T, int D, float* h, float* ssp, cudaStream_t s) {
-  launch_pdl(embed_ss_kernel, dim3(T), dim3(256), 0, s, emb, static_cast<const int32_t*>(m.row_tok), T, D, h, ssp);
+void launch_embed_ss(const bf16* emb, const FwdMeta& m, int T, int D, float* h, bf16* hb, float* ssp,
+                     cudaStream_t s) {
+  launch_pdl(embed_ss_kernel, dim3(T), dim3(256), 0, s, emb, static_cast<const int32_t*>(m.row_tok), T, D, h, hb, ssp);
 }
 
 void launch_norm_ss(const float* h, const float* ssp, int n_ssp, int T, int D, float eps, bf16* xn, cudaStream_t s) {

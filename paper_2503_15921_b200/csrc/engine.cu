@@ -221,6 +221,7 @@ void Engine::init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool l
   ln.attn = dalloc<bf16>(A, static_cast<size_t>(T_cap) * m.D);
   ln.act = dalloc<bf16>(A, static_cast<size_t>(T_cap) * m.F);
   ln.ssp = dalloc<float>(A, static_cast<size_t>(m.D / 16 + 1) * std::min(T_cap, kDraftMaxT));
+  ln.hb = dalloc<bf16>(A, static_cast<size_t>(std::min(T_cap, kDraftMaxT)) * m.D);
   size_t part = 0;
   const int shapes[4][2] = {{3 * m.D, m.D}, {m.D, m.D}, {2 * m.F, m.D}, {m.D, m.F}};
   for (auto& sh : shapes) {
@@ -372,7 +373,7 @@ void Engine::forward_draft(ModelDev& m, Lane& ln, const FwdShape& sh, AttnGeom g
   const int base = kProfSsmGemm;
   auto wbytes = [&](int n_out, int k) { return 2.0 * n_out * k + 2.0 * T * k + 2.0 * T * n_out; };
   prof_begin(base + 3, s);
-  launch_embed_ss(m.emb, ln.meta, T, D, ln.h, ln.ssp, s);
+  launch_embed_ss(m.emb, ln.meta, T, D, ln.h, ln.hb, ln.ssp, s);
   prof_end(s, 0);
   int n_ssp = 1;
   AttnWork aw = ln.aw;
@@ -387,6 +388,7 @@ void Engine::forward_draft(ModelDev& m, Lane& ln, const FwdShape& sh, AttnGeom g
   a.rcos = m.rcos;
   a.rsin = m.rsin;
   a.h = ln.h;
+  a.hb = ln.hb;
   a.q = ln.q;
   a.act = ln.act;
   static const int skip = [] {  // timing experiments only: skip kernels (results invalid)
@@ -397,7 +399,7 @@ void Engine::forward_draft(ModelDev& m, Lane& ln, const FwdShape& sh, AttnGeom g
     const LayerW& w = m.layers[l];
     g.layer = l;
     a.g = g;
-    a.mode = kDpQkv, a.w = w.sqkv, a.n_out = 3 * D, a.K = D, a.ssp = ln.ssp, a.n_ssp = n_ssp;
+    a.mode = kDpQkv, a.w = w.sqkv, a.n_out = 3 * D, a.K = D, a.x = ln.hb, a.ssp = ln.ssp, a.n_ssp = n_ssp;
     if (!(skip & 2)) {
       prof_begin(base, s);
       a.st = stamp_slot(0, draft_proj_units(a));
@@ -418,7 +420,7 @@ void Engine::forward_draft(ModelDev& m, Lane& ln, const FwdShape& sh, AttnGeom g
       prof_end(s, wbytes(D, D));
     }
     n_ssp = D / 16;
-    a.mode = kDpGateUp, a.w = w.sgu, a.n_out = 2 * F, a.K = D, a.ssp = ln.ssp, a.n_ssp = n_ssp;
+    a.mode = kDpGateUp, a.w = w.sgu, a.n_out = 2 * F, a.K = D, a.x = ln.hb, a.ssp = ln.ssp, a.n_ssp = n_ssp;
     if (!(skip & 8)) {
       prof_begin(base, s);
       a.st = stamp_slot(3, draft_proj_units(a));

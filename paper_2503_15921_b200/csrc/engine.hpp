@@ -40,7 +40,8 @@ struct Lane {
   float* h = nullptr;
   bf16 *xn = nullptr, *attn = nullptr, *act = nullptr;
   float* q = nullptr;
-  float* ssp = nullptr;  // draft path: per-unit sums of squares of h [D / 16][T]
+  float* ssp = nullptr;  // draft path: per-unit sums of squares of h [T][D / 16]
+  bf16* hb = nullptr;    // draft path: bf16 copy of h [T][D]
   float* part = nullptr;
   AttnWork aw{};
   float* amax_val = nullptr;

@@ -113,11 +113,12 @@ struct DraftProj {
   int mode;
   const bf16* w;  // slab weights (launch_slab_weights), n_out x K
   int n_out, K, T;
-  float* h;            // QKV / GATE_UP: fp32 residual input (normalised on load); RESID: residual, updated
+  float* h;            // RESID: fp32 residual stream, updated
+  bf16* hb;            // RESID: bf16 copy of the updated residual (the norm consumers' token operand)
   const float* ssp;    // QKV / GATE_UP: [T][n_ssp] sums of squares of h
   int n_ssp;
   float eps;
-  const bf16* x;       // RESID: bf16 input [T][K]
+  const bf16* x;       // bf16 token operand [T][K]: attention out / SwiGLU out / bf16(h) for QKV, GATE_UP
   float* ssp_out;      // RESID: [T][n_out / 16]
   float* q;            // QKV: fp32 [T][D], RoPE applied; K/V appended to g's caches
   AttnGeom g;
@@ -135,7 +136,8 @@ size_t draft_slab_elems(int n_out, int K);
 void launch_slab_weights(const bf16* tiled, bf16* slab, int mode, int n_out, int K, int hd, cudaStream_t s);
 bool draft_fused_supported(int D, int H, int hd, int F, int T);
 cudaError_t launch_draft_proj(const DraftProj& a, cudaStream_t s);
-void launch_embed_ss(const bf16* emb, const FwdMeta& m, int T, int D, float* h, float* ssp, cudaStream_t s);
+void launch_embed_ss(const bf16* emb, const FwdMeta& m, int T, int D, float* h, bf16* hb, float* ssp,
+                     cudaStream_t s);
 void launch_norm_ss(const float* h, const float* ssp, int n_ssp, int T, int D, float eps, bf16* xn, cudaStream_t s);
 
 // Packed ragged causal attention over the KV cache (TMA-staged tiles) and the
