@@ -111,7 +111,7 @@ template <int NW, int NT, int MT, bool NORM>
 struct DpCfg {
   static constexpr int kSlab = MT * 16 * 128;                  // bytes of one 64-k atom of the unit
   static constexpr int kXRegs = NT * 4;                        // registers per 32-k step of the token operand
-  static constexpr int kBatch = kXRegs >= 48 ? 1 : 48 / kXRegs;  // 32-k steps loaded per round trip
+  static constexpr int kBatch = kXRegs >= 64 ? 1 : 64 / kXRegs;  // 32-k steps loaded per round trip
   static constexpr int kRed = NW * MT * NT * 32 * 4;           // cross-warp reduction floats
   static constexpr int kAtomsPerCopy = 8 / MT;                 // 16-KB bulk copies
   __host__ __device__ static constexpr size_t inv_off(int KB) {
