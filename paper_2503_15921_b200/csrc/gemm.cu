@@ -373,6 +373,13 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
     return e ? std::atoi(e) : kMaxStages;
   }();
   p.stages = static_cast<int>(std::min<size_t>(std::min(kMaxStages, cap), budget / stage_bytes));
+  // Draft-step lm_heads (few rows) run beside the other SSM's kernels: a small ring lets
+  // CTAs of both co-reside instead of one 227-KB CTA owning each SM.
+  static const int small_ring = [] {
+    const char* e = std::getenv("SPIN_GEMM_SMALL_RING");  // experiments only
+    return e ? std::atoi(e) : 4;
+  }();
+  if (mode == kGemmArgmax && t <= 32 && small_ring > 0) p.stages = std::min(p.stages, small_ring);
   p.smem_bytes = 1024 + p.stages * stage_bytes + (mode == kGemmPartial ? kStgBytes : kRedBytes) + kBarBytes;
   PieceMap& m = p.map;
   m.mode = mode;
