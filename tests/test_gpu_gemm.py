@@ -41,7 +41,7 @@ def test_gemm_partial_matches_torch(n_out, k, t):
     assert err <= 1e-4 * scale + 1e-5, f"max err {err} (scale {scale}, pieces {mp}, grid {grid}, bn {bn})"
 
 
-@pytest.mark.parametrize("n_out,k,t", [(4096, 256, 40), (32000, 4096, 160), (1000, 128, 5)])
+@pytest.mark.parametrize("n_out,k,t", [(4096, 256, 40), (32000, 4096, 160), (1000, 128, 5), (2048, 256, 520)])
 def test_gemm_argmax_matches_torch(n_out, k, t):
     lib = _lib.load()
     w = _rand((n_out, k), 3)
