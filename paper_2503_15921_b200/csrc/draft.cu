@@ -27,7 +27,6 @@
 // Results are deterministic (fixed-order reductions everywhere). Numerics follow
 // the reference model (oracle/ restatement): fp32 accumulation of bf16 products,
 // residual stream fp32, x = bf16(h / rms(h)).
-#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -138,8 +137,6 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
 
   // ---- weights first (never depend on the previous kernel): the unit's slab in 16-KB copies
   constexpr int APC = C::kAtomsPerCopy;
-  if (a.dbg & 4)
-    for (int i = threadIdx.x; i < KB * C::kSlab / 16; i += NW * 32) reinterpret_cast<uint4*>(slab)[i] = uint4{0, 0, 0, 0};
   if (threadIdx.x == 0) {
     const int n_copies = (KB + APC - 1) / APC;
     for (int c = 0; c < n_copies; ++c) ptx::mbar_init(&bar[c], 1);
@@ -148,10 +145,6 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
     const uint8_t* src = reinterpret_cast<const uint8_t*>(a.w) + static_cast<size_t>(u) * KB * C::kSlab;
     for (int c = 0; c < n_copies; ++c) {
       const uint32_t bytes = static_cast<uint32_t>(min(APC, KB - c * APC)) * C::kSlab;
-      if (a.dbg & 4) {  // timing experiment: no weight stream
-        ptx::mbar_arrive(&bar[c]);
-        continue;
-      }
       ptx::mbar_arrive_expect_tx(&bar[c], bytes);
       ptx::bulk_load(slab + static_cast<size_t>(c) * APC * C::kSlab, src + static_cast<size_t>(c) * APC * C::kSlab,
                      bytes, &bar[c], pol);
@@ -208,7 +201,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int tok = nt * 8 + g;
-        const bool ok = s < n_steps && tok < T && kk < K && !(a.dbg & 2);
+        const bool ok = s < n_steps && tok < T && kk < K;
         xr[b][nt] = ok ? __ldcg(reinterpret_cast<const uint4*>(a.x + static_cast<size_t>(tok) * K + kk))
                        : make_uint4(0u, 0u, 0u, 0u);
       }
@@ -226,7 +219,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int v = lane + 32 * r;
-        ss[j][r] = (t < T && v < a.n_ssp) ? ((a.dbg & 8) ? 1.f : __ldcg(a.ssp + static_cast<size_t>(t) * a.n_ssp + v)) : 0.f;
+        ss[j][r] = (t < T && v < a.n_ssp) ? __ldcg(a.ssp + static_cast<size_t>(t) * a.n_ssp + v) : 0.f;
       }
     }
 #pragma unroll
@@ -236,8 +229,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
       const int t = warp + NW * j;
       if (lane == 0 && t < NT * 8)
-        inv_s[t] = (a.dbg & 16) ? rsqrtf(x / K + a.eps)
-                                : __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(x, static_cast<float>(K)), a.eps)));
+        inv_s[t] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(x, static_cast<float>(K)), a.eps)));
     }
   }
   // (inv_s is published by the barrier before the cross-warp reduction: the RMSNorm
@@ -258,7 +250,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
       const int s = s0 + b;
       if (s >= n_steps) break;
       const int kb = warp + NW * (s >> 1);
-      if ((s & 1) == 0 && !(a.dbg & 1)) ptx::mbar_wait(&bar[kb / APC], 0);
+      if ((s & 1) == 0) ptx::mbar_wait(&bar[kb / APC], 0);
       const uint32_t chunk = static_cast<uint32_t>(((s & 1) * 4 + t4) ^ g) << 4;
       uint4 wa[MT], wb[MT];
 #pragma unroll
@@ -368,7 +360,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 8 ? 2 : 1) dproj_kernel(DraftPr
       if (tA + 1 < T) a.ssp_out[static_cast<size_t>(tA + 1) * (a.n_out / 16) + u] = ss[1];
     }
   }
-  if (stamp && !(a.dbg & 64)) a.st[4 * u + 3] = ptx::globaltimer();
+  if (stamp) a.st[4 * u + 3] = ptx::globaltimer();
 }
 
 // h = embedding rows (fp32), ssp[0][t] = sum of squares (one unit).
@@ -484,13 +476,7 @@ void launch_slab_weights(const bf16* tiled, bf16* slab, int mode, int n_out, int
   slab_weights_kernel<<<1184, 256, 0, s>>>(tiled, slab, mode, n_out, K, hd);
 }
 
-cudaError_t launch_draft_proj(const DraftProj& a_in, cudaStream_t s) {
-  static const int dbg = [] {
-    const char* e = std::getenv("SPIN_DPROJ_DBG");  // timing experiments only (results invalid)
-    return e ? std::atoi(e) : 0;
-  }();
-  DraftProj a = a_in;
-  a.dbg = dbg;
+cudaError_t launch_draft_proj(const DraftProj& a, cudaStream_t s) {
   switch (a.mode) {
     case kDpQkv:
       return launch_nt<1, true>(a, a.n_out / 16, s);

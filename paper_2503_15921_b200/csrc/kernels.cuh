@@ -128,7 +128,6 @@ struct DraftProj {
   const float* rsin;
   bf16* act;           // GATE_UP: SwiGLU output [T][n_out / 2]
   unsigned long long* st;  // optional timeline stamps [CTA][4] (SPIN_STAMPS)
-  int dbg;                 // timing experiments (SPIN_DPROJ_DBG)
 };
 int draft_proj_units(const DraftProj& a);
 // Slab copy of a tiled weight matrix for the draft projections (unit-contiguous).
