@@ -80,7 +80,7 @@ __device__ __forceinline__ void argmax_merge(float& v, int& i, float ov, int oi)
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __nv_bfloat16* __restrict__ w_tiled, const __grid_constant__ CUtensorMap tm_x,
                    const __grid_constant__ CUtensorMap tm_part, PieceMap pm, GemmEpilogue epi, int n_out, int t_total,
-                   int stages, int dbg) {
+                   int stages) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (s < stages && pre.next(pm, n_tiles, q)) {
           const int mt = q.tile / pm.n_ntiles;
           for (int kb = q.kb0; kb < q.kb1 && s < stages; ++kb, ++s) {
-            ptx::mbar_arrive_expect_tx(&full_bar[s], kTileABytes + ((dbg & 1) ? 0u : tile_b_bytes));
+            ptx::mbar_arrive_expect_tx(&full_bar[s], kTileABytes + tile_b_bytes);
             ptx::bulk_load(smem_a + static_cast<size_t>(s) * kTileABytes,
                            w_tiled + (static_cast<size_t>(mt) * pm.kb + kb) * (kBlockM * kBlockK), kTileABytes,
                            &full_bar[s], pol_w);
@@ -165,14 +165,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = p.kb0; kb < p.kb1; ++kb) {
           if (issued >= prefetched) {
             ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-            ptx::mbar_arrive_expect_tx(&full_bar[stage], kTileABytes + ((dbg & 1) ? 0u : tile_b_bytes));
+            ptx::mbar_arrive_expect_tx(&full_bar[stage], kTileABytes + tile_b_bytes);
             ptx::bulk_load(smem_a + static_cast<size_t>(stage) * kTileABytes,
                            w_tiled + (static_cast<size_t>(mt) * pm.kb + kb) * (kBlockM * kBlockK), kTileABytes,
                            &full_bar[stage], pol_w);
           }
-          if (!(dbg & 1))
-            ptx::tma_load_2d(smem_b + static_cast<size_t>(stage) * tile_b_bytes, &tm_x, &full_bar[stage],
-                             kb * kBlockK, nt * bn, pol_x);
+          ptx::tma_load_2d(smem_b + static_cast<size_t>(stage) * tile_b_bytes, &tm_x, &full_bar[stage],
+                           kb * kBlockK, nt * bn, pol_x);
           ++issued;
           if (++stage == stages) {
             stage = 0;
@@ -203,12 +202,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           const uint64_t da = ptx::smem_desc_sw128(smem_a + static_cast<size_t>(stage) * kTileABytes);
           const uint64_t db = ptx::smem_desc_sw128(smem_b + static_cast<size_t>(stage) * tile_b_bytes);
-          if (!(dbg & 2)) {
 #pragma unroll
-            for (int k = 0; k < kBlockK / 16; ++k) {
-              // +32 bytes per 16-element K step inside the 128-B swizzle atom.
-              ptx::umma_bf16(d_addr, da + 2 * k, db + 2 * k, idesc, (kb > p.kb0 || k > 0) ? 1u : 0u);
-            }
+          for (int k = 0; k < kBlockK / 16; ++k) {
+            // +32 bytes per 16-element K step inside the 128-B swizzle atom.
+            ptx::umma_bf16(d_addr, da + 2 * k, db + 2 * k, idesc, (kb > p.kb0 || k > 0) ? 1u : 0u);
           }
           ptx::umma_commit(&empty_bar[stage]);
           if (kb + 1 == p.kb1) ptx::umma_commit(&tfull_bar[acc]);
@@ -262,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 16; ++j) stg[j * kBlockM + row] = v[j];
           ptx::fence_proxy_async_smem();
           asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (ew == 0 && lane == 0 && !(dbg & 4)) {
+          if (ew == 0 && lane == 0) {
             ptx::tma_store_3d(&tm_part, stg, mt * kBlockM, nt * bn + c0, p.slot);
             ptx::bulk_commit();
           }
@@ -445,12 +442,8 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   GemmEpilogue e = epi;
-  static const int dbg = [] {
-    const char* s = std::getenv("SPIN_GEMM_DBG");  // timing experiments only: 1 no X, 2 no MMA, 4 no stores
-    return s ? std::atoi(s) : 0;
-  }();
   return cudaLaunchKernelEx(&cfg, gemm_tc_kernel, static_cast<const __nv_bfloat16*>(W), tm_x, tm_part, plan.map, e,
-                            plan.n_out, plan.t, plan.stages, epi.mode == kGemmPartial ? dbg : 0);
+                            plan.n_out, plan.t, plan.stages);
 }
 
 }  // namespace spin
