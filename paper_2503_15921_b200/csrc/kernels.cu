@@ -489,20 +489,27 @@ __global__ void __launch_bounds__(kRowThreads, 2) qkv_epilogue_kernel(const floa
                                                                    FwdMeta m, int T, AttnGeom g,
                                                                    const float* __restrict__ rcos,
                                                                    const float* __restrict__ rsin, float* q) {
-  ptx::grid_dep_wait();
-  ptx::grid_dep_launch();  // dependents (the next GEMM) may start their weight prefetch now
   const int t = blockIdx.x;
   const int H = g.n_heads, hd = g.head_dim, half = hd / 2, D = H * hd, N = 3 * D;
   const int p4 = 4 * (blockIdx.y * kRowThreads + threadIdx.x);  // first of 4 rotary pairs
-  if (p4 < H * half) {
-    const int slot = m.row_slot[t], pos = m.row_pos[t];
-    const int hh = p4 / half, i = p4 % half;
+  const bool active = p4 < H * half;
+  const int hh = p4 / half, i = p4 % half;
+  // The row metadata (meta_kernel, complete before the projection that precedes us
+  // triggered) and the RoPE tables are read before the dependency wait.
+  int slot = -1, pos = 0;
+  float4 c = make_float4(0.f, 0.f, 0.f, 0.f), s = c;
+  if (active) {
+    slot = m.row_slot[t], pos = m.row_pos[t];
+    c = *reinterpret_cast<const float4*>(rcos + static_cast<size_t>(pos) * half + i);
+    s = *reinterpret_cast<const float4*>(rsin + static_cast<size_t>(pos) * half + i);
+  }
+  ptx::grid_dep_wait();
+  ptx::grid_dep_launch();  // dependents (attention) may stage their work list now
+  if (active) {
     const int nq = hh * hd + i;
     const float4 q0 = sum_pieces4(part, pm, T, N, t, nq), q1 = sum_pieces4(part, pm, T, N, t, nq + half);
     const float4 k0 = sum_pieces4(part, pm, T, N, t, D + nq), k1 = sum_pieces4(part, pm, T, N, t, D + nq + half);
     const float4 v0 = sum_pieces4(part, pm, T, N, t, 2 * D + nq), v1 = sum_pieces4(part, pm, T, N, t, 2 * D + nq + half);
-    const float4 c = *reinterpret_cast<const float4*>(rcos + static_cast<size_t>(pos) * half + i);
-    const float4 s = *reinterpret_cast<const float4*>(rsin + static_cast<size_t>(pos) * half + i);
     const float qa[4] = {q0.x, q0.y, q0.z, q0.w}, qb[4] = {q1.x, q1.y, q1.z, q1.w};
     const float ka[4] = {k0.x, k0.y, k0.z, k0.w}, kb[4] = {k1.x, k1.y, k1.z, k1.w};
     const float cs[4] = {c.x, c.y, c.z, c.w}, sn[4] = {s.x, s.y, s.z, s.w};
