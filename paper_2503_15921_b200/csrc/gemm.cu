@@ -392,6 +392,29 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
     // on the config-2 draft loop).
     constexpr long long kMinUnits = 4;
     m.grid = static_cast<int>(std::min<long long>(num_sms, std::max<long long>(1, (m.units + kMinUnits - 1) / kMinUnits)));
+    // A few SMs fewer can cut the worst-case pieces per tile (e.g. 144 CTAs split every
+    // 64-k-block QKV tile into exactly 2 pieces where 148 leave some with 3): the consumer
+    // re-reads max_pieces partials per element. Search down to grid - kGridSlack.
+    static const int slack = [] {
+      const char* e = std::getenv("SPIN_GEMM_GRID_SLACK");  // tuning
+      return e ? std::atoi(e) : 8;
+    }();
+    auto worst = [&](int g) {
+      PieceMap q = m;
+      q.grid = g;
+      int w = 1;
+      for (long long tile = 0; tile < n_tiles; ++tile)
+        w = std::max(w, q.pieces(static_cast<int>((tile % p.n_ntiles) * p.bn), static_cast<int>((tile / p.n_ntiles) * kBlockM)));
+      return w;
+    };
+    if (m.grid == num_sms && n_tiles * p.kb <= (1 << 20)) {
+      int best = m.grid, best_w = worst(m.grid);
+      for (int g = m.grid - 1; g >= m.grid - slack && g > 0; --g) {
+        const int w = worst(g);
+        if (w < best_w) best = g, best_w = w;
+      }
+      m.grid = best;
+    }
     // Worst-case pieces per tile: a tile spans ceil(kb / per_cta) + 1 CTAs.
     int mp = 1;
     p.tile_pieces.resize(n_tiles);

@@ -17,7 +17,7 @@ constexpr unsigned kFull = 0xffffffffu;
 // (slot 0..np-1, deterministic); np comes from the plan's host-built piece table.
 // The first kUnrollPieces partial loads are predicated rather than looped so that a
 // caller summing several groups has all of their loads in flight at once.
-constexpr int kUnrollPieces = 4;
+constexpr int kUnrollPieces = 2;
 __device__ __forceinline__ float4 sum_pieces4(const float* __restrict__ part, const PieceMap& pm, int T, int n_out,
                                               int t, int n) {
   const int np = pm.tile_pieces(t, n);
