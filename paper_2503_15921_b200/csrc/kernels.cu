@@ -386,12 +386,12 @@ __global__ void __launch_bounds__(kRowThreads) embed_norm_kernel(const bf16* __r
   rmsnorm_row(s_row, D, eps, xn + static_cast<size_t>(t) * D, red);
 }
 
-// h += sum of the stream-K partials; xn = bf16(rmsnorm(h)). Each thread owns up to
-// kNormVec float4 groups of the row (D <= 8192) and keeps them in registers: every
-// partial / residual load of a piece round is issued before any add or store, so the
-// row costs max_pieces L2 round trips instead of one per group.
-constexpr int kNormVec = 8;
-__global__ void __launch_bounds__(kRowThreads) resid_norm_kernel(const float* __restrict__ part, PieceMap pm, int T,
+// h += sum of the stream-K partials; xn = bf16(rmsnorm(h)). Each thread owns NV float4
+// groups of the row (D <= NV * 1024) and keeps them in registers; the loads of PB pieces
+// for all groups are issued before any add or store, so the row costs
+// ceil((max_pieces - 1) / PB) + 1 L2 round trips.
+template <int NV, int PB>
+__global__ void __launch_bounds__(kRowThreads, 2) resid_norm_kernel(const float* __restrict__ part, PieceMap pm, int T,
                                                                  int D, float eps, float* __restrict__ h,
                                                                  bf16* __restrict__ xn) {
   __shared__ float red[32];
@@ -401,11 +401,11 @@ __global__ void __launch_bounds__(kRowThreads) resid_norm_kernel(const float* __
   const size_t stride = static_cast<size_t>(T) * D;
   const float* prow = part + static_cast<size_t>(t) * D;
   float4* hrow = reinterpret_cast<float4*>(h + static_cast<size_t>(t) * D);
-  float4 v[kNormVec], y[kNormVec];
-  int np[kNormVec];
+  float4 v[NV], y[NV];
+  int np[NV];
   int maxp = 0;
 #pragma unroll
-  for (int k = 0; k < kNormVec; ++k) {
+  for (int k = 0; k < NV; ++k) {
     const int i = 4 * (threadIdx.x + k * kRowThreads);
     np[k] = i < D ? pm.tile_pieces(t, i) : 0;
     maxp = max(maxp, np[k]);
@@ -414,21 +414,26 @@ __global__ void __launch_bounds__(kRowThreads) resid_norm_kernel(const float* __
       y[k] = __ldg(reinterpret_cast<const float4*>(prow + i));
     }
   }
-  for (int s = 1; s < maxp; ++s) {
-    float4 z[kNormVec];
+  for (int s0 = 1; s0 < maxp; s0 += PB) {
+    float4 z[PB][NV];
 #pragma unroll
-    for (int k = 0; k < kNormVec; ++k)
-      if (s < np[k]) z[k] = __ldg(reinterpret_cast<const float4*>(prow + s * stride + 4 * (threadIdx.x + k * kRowThreads)));
+    for (int b = 0; b < PB; ++b)
 #pragma unroll
-    for (int k = 0; k < kNormVec; ++k)
-      if (s < np[k]) {
-        y[k].x = __fadd_rn(y[k].x, z[k].x), y[k].y = __fadd_rn(y[k].y, z[k].y);
-        y[k].z = __fadd_rn(y[k].z, z[k].z), y[k].w = __fadd_rn(y[k].w, z[k].w);
-      }
+      for (int k = 0; k < NV; ++k)
+        if (s0 + b < np[k])
+          z[b][k] = __ldg(reinterpret_cast<const float4*>(prow + (s0 + b) * stride + 4 * (threadIdx.x + k * kRowThreads)));
+#pragma unroll
+    for (int b = 0; b < PB; ++b)
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        if (s0 + b < np[k]) {
+          y[k].x = __fadd_rn(y[k].x, z[b][k].x), y[k].y = __fadd_rn(y[k].y, z[b][k].y);
+          y[k].z = __fadd_rn(y[k].z, z[b][k].z), y[k].w = __fadd_rn(y[k].w, z[b][k].w);
+        }
   }
   float ss = 0.f;
 #pragma unroll
-  for (int k = 0; k < kNormVec; ++k) {
+  for (int k = 0; k < NV; ++k) {
     if (np[k] == 0) continue;
     v[k].x = __fadd_rn(v[k].x, y[k].x), v[k].y = __fadd_rn(v[k].y, y[k].y);
     v[k].z = __fadd_rn(v[k].z, y[k].z), v[k].w = __fadd_rn(v[k].w, y[k].w);
@@ -439,7 +444,7 @@ __global__ void __launch_bounds__(kRowThreads) resid_norm_kernel(const float* __
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(tot, static_cast<float>(D)), eps)));
   bf16* xrow = xn + static_cast<size_t>(t) * D;
 #pragma unroll
-  for (int k = 0; k < kNormVec; ++k) {
+  for (int k = 0; k < NV; ++k) {
     if (np[k] == 0) continue;
     __nv_bfloat162 a = __floats2bfloat162_rn(__fmul_rn(v[k].x, inv), __fmul_rn(v[k].y, inv));
     __nv_bfloat162 b = __floats2bfloat162_rn(__fmul_rn(v[k].z, inv), __fmul_rn(v[k].w, inv));
@@ -772,7 +777,10 @@ void launch_qkv_epilogue(const float* part, const PieceMap& pm, const FwdMeta& m
 
 void launch_resid_norm(const float* part, const PieceMap& pm, int T, int D, float eps, float* h, bf16* xn,
                        cudaStream_t s) {
-  launch_pdl(resid_norm_kernel, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, D, eps, h, xn);
+  if (D <= 4 * 4 * kRowThreads)
+    launch_pdl(resid_norm_kernel<4, 4>, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, D, eps, h, xn);
+  else
+    launch_pdl(resid_norm_kernel<8, 1>, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, D, eps, h, xn);
 }
 
 void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* act, cudaStream_t s) {
