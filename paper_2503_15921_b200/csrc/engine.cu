@@ -444,8 +444,9 @@ void Engine::forward_draft(ModelDev& m, Lane& ln, const FwdShape& sh, AttnGeom g
     eh.amax_val = ln.amax_val;
     eh.amax_idx = ln.amax_idx;
     prof_begin(base + 1, s);
-    check_cuda(gemm_launch(plan(m.V, D, T, kGemmArgmax), m.head, ln.xn, eh, s, opts_.use_pdl != 0),
-               "gemm lm_head");
+    const GemmPlan& ph = plan(m.V, D, T, kGemmArgmax);
+    eh.st = stamp_slot(15, 2 * ph.grid);
+    check_cuda(gemm_launch(ph, m.head, ln.xn, eh, s, opts_.use_pdl != 0), "gemm lm_head");
     prof_end(s, wbytes(m.V, D));
   }
   check_cuda(cudaGetLastError(), "draft forward launch");
