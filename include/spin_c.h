@@ -66,11 +66,22 @@ spin_status spin_naive_padding(const int32_t* kv_lens, int32_t n, int64_t* paddi
 spin_status spin_verify_batch_cost(const int32_t* kv_lens, int32_t n, int32_t window, int32_t packing,
                                    int32_t pack_width, int64_t* tokens, int64_t* padding);
 
+/* Device request decomposition: the packer the hot path runs (meta_kernel, one warp:
+ * ballot first-fit + warp-scan splits), launched on its own. Same contract and error
+ * taxonomy as spin_pack; bit-identical to it (tests/test_gpu_pack_device.py pins it to
+ * the reference goldens). n <= 1024. */
+spin_status spin_pack_device(const int32_t* kv_lens, int32_t n, int32_t width, int32_t* length, int32_t* rows,
+                             spin_segment* segments, int32_t seg_cap, int32_t* n_segments,
+                             int64_t* padding_tokens, int32_t* q_replica_rows);
+
 /* ------------------------------------------------------------------------
- * Packed (decomposed) attention operator on the GPU. Host buffers in fp64 like
- * the reference Matrix; computed on the device in fp32 by the same ragged
- * split-KV kernel family the verifier uses, with scale = 1 and no causal mask
- * (attention.cpp:67-96 semantics). q/k/v are the per-request matrices
+ * Packed (decomposed) attention operator in the reference's toy mode
+ * (attention.cpp:67-162: fp64, scale 1, no causal mask, any dim). Host buffers
+ * in fp64 like the reference Matrix; computed on the device in fp64 by a
+ * dedicated split-KV kernel (launch_toy_attention in kernels.cu) -- one partial
+ * per (segment, query) and the shared-max combine across a request's segments.
+ * It is NOT the production verifier kernel (bf16 KV, head_dim 64/128, causal);
+ * spin_attention below runs that one. q/k/v are the per-request matrices
  * concatenated row-major: q rows sum(q_rows[i]), k/v rows sum(kv_rows[i]).
  * mask (width*length owner ids, -1 empty) is checked against the layout like
  * check_layout_consistency (attention.cpp:23-63); pass NULL to skip.
@@ -142,9 +153,13 @@ typedef struct spin_round_out {
 spin_status spin_round(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
                        spin_round_out* out);
 
-/* Device-resident loop: `rounds` rounds back to back on the current assignment
- * with no host round trip; per-round accepted+bonus totals land in
- * emitted[rounds] (host) after the final synchronisation. */
+/* Device-resident loop: one host-driven spin_round first (validation, SSM
+ * switches, graph capture; its outcome is not reported), then `rounds` rounds
+ * back to back on the current assignment with no host round trip -- rounds + 1
+ * rounds in total, so every active slot needs committed + (rounds + 1) * (window + 1)
+ * <= max_ctx (else SPIN_CAPACITY_ERROR, nothing runs). Per-round accepted+bonus
+ * totals of the `rounds` timed rounds land in emitted[rounds] (host) after the
+ * final synchronisation. */
 spin_status spin_run_rounds(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
                             int32_t rounds, int64_t* emitted, float* device_ms);
 
@@ -205,6 +220,16 @@ typedef struct spin_verify_stats {
 } spin_verify_stats;
 spin_status spin_verify_bench(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* draft_lens,
                               const int32_t* drafts, int32_t packed, int32_t iters, spin_verify_stats* out);
+
+/* ------------------------------------------------------------------------
+ * Device plumbing: lets callers (and the parity tests) hold device buffers
+ * without any framework. spin_device_count reports 0 (status OK) when there is
+ * no driver or device. spin_device_alloc zero-fills. kind: 1 H2D, 2 D2H, 3 D2D.
+ * ---------------------------------------------------------------------- */
+spin_status spin_device_count(int32_t* count);
+spin_status spin_device_alloc(int32_t device, size_t bytes, void** ptr);
+spin_status spin_device_free(void* ptr);
+spin_status spin_memcpy(void* dst, const void* src, size_t bytes, int32_t kind);
 
 /* ------------------------------------------------------------------------
  * Kernel-level entry points (device pointers; stream = cudaStream_t or NULL).

@@ -73,6 +73,10 @@ def load_oracle() -> C.CDLL:
         lib.so_engine_set_gap_outputs.argtypes = [C.c_void_p, C.c_void_p]
         lib.so_engine_set_hints.argtypes = [C.c_void_p, C.c_void_p, C.c_float]
         lib.so_engine_forced_count.restype = C.c_long
+        lib.so_engine_forced_deficit.restype = C.c_float
+        lib.so_engine_verify_ragged.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                C.c_void_p, C.c_void_p]
+        lib.so_engine_fake_context.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64]
         lib.so_engine_last_timing.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         lib.so_debug_layer.argtypes = [C.c_int, C.c_void_p, C.c_int]
         lib.so_debug_inner.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int]
@@ -183,7 +187,44 @@ class OracleEngine:
         return out
 
     def forced(self) -> int:
+        """Near-tie decisions adopted from the GPU since the last reset (process-wide)."""
         return int(self.lib.so_engine_forced_count())
+
+    def forced_deficit(self) -> float:
+        """Largest (own max logit - adopted logit) over those decisions."""
+        return float(self.lib.so_engine_forced_deficit())
+
+    def reset_forced(self) -> None:
+        self.lib.so_engine_reset_forced()
+
+    def verify_ragged(self, slots, draft_lens, drafts, hint=None, tau=0.0, want_logits=False):
+        """Target argmax of every row of a ragged verification (spin_verify_bench contract)."""
+        import numpy as np
+
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        lens = np.ascontiguousarray(draft_lens, dtype=np.int32)
+        dr = np.ascontiguousarray(drafts, dtype=np.int32)
+        rows = int(lens.sum()) + len(lens)
+        out = np.zeros(rows, np.int32)
+        hv = None
+        if hint is not None:
+            hv = np.ascontiguousarray(hint, dtype=np.int32)
+            self.lib.so_engine_set_hints(None, None, tau)
+        logits = np.zeros(rows * self.vocab, np.float32) if want_logits else None
+        st = self.lib.so_engine_verify_ragged(self.e, len(slots), slots.ctypes.data, lens.ctypes.data, dr.ctypes.data,
+                                              hv.ctypes.data if hv is not None else None, out.ctypes.data,
+                                              logits.ctypes.data if want_logits else None)
+        self.lib.so_engine_set_hints(None, None, 0.0)
+        assert st == 0, st
+        return (out, logits.reshape(rows, self.vocab)) if want_logits else out
+
+    def fake_context(self, slots, lens, seed: int = 2503):
+        """Seeded histories + KV rows instead of a prefill forward (CPU-baseline timing only)."""
+        import numpy as np
+
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        lens = np.ascontiguousarray(lens, dtype=np.int32)
+        assert self.lib.so_engine_fake_context(self.e, len(slots), slots.ctypes.data, lens.ctypes.data, seed) == 0
 
     def last_timing(self):
         a, b, c = C.c_double(), C.c_double(), C.c_double()

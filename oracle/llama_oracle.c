@@ -204,6 +204,7 @@ static void model_destroy(model* m) {
 /* Tie-aware argmax state (so_engine_set_hints). */
 static float g_tau = 0.0f;
 static long g_forced = 0;
+static float g_forced_deficit = 0.0f; /* largest (own max - adopted logit) over forced decisions */
 
 /* Debug knob (sensitivity experiments only): number of partial sums. */
 static int g_lanes = 16;
@@ -412,6 +413,7 @@ static void model_forward_gap(model* m, int T, const int* tok, const int* slot, 
     if (hint && hint[t] >= 0 && hint[t] < V && hint[t] != best && r[hint[t]] >= r[best] - g_tau) {
       amax[t] = hint[t];
       ++g_forced;
+      if (r[best] - r[hint[t]] > g_forced_deficit) g_forced_deficit = r[best] - r[hint[t]];
     }
     if (gap) {
       float second = -INFINITY;
@@ -522,6 +524,11 @@ void so_engine_set_hints(const int* draft_hint, const int* target_hint, float ta
   g_tau = tau;
 }
 long so_engine_forced_count(void) { return g_forced; }
+float so_engine_forced_deficit(void) { return g_forced_deficit; }
+void so_engine_reset_forced(void) {
+  g_forced = 0;
+  g_forced_deficit = 0.0f;
+}
 static float* g_draft_gap = NULL;  /* [n][window] per next so_engine_round, optional */
 static float* g_target_gap = NULL; /* [rows] */
 void so_engine_set_gap_outputs(float* draft_gap, float* target_gap) {
@@ -673,4 +680,73 @@ double so_engine_verify_seconds(so_engine* e, int n, const int* slots) {
   clock_gettime(CLOCK_MONOTONIC, &b);
   free(tok), free(sl), free(ps), free(am);
   return (double)(b.tv_sec - a.tv_sec) + 1e-9 * (double)(b.tv_nsec - a.tv_nsec);
+}
+
+/* Ragged verification without commit (BASELINE config 3): request i verifies
+ * draft_lens[i] drafts -- rows (pending, d_1..d_len) at positions c-1 .. c-1+len --
+ * through the target; target_out gets the argmax of every row (request-major,
+ * sum(len+1) entries). KV rows at those positions are (re)written, nothing is
+ * committed (the GPU's spin_verify_bench contract). hint: GPU argmax per row or
+ * NULL (tie-aware, see so_engine_set_hints); logits: [rows][vocab] or NULL. */
+int so_engine_verify_ragged(so_engine* e, int n, const int* slots, const int* draft_lens, const int* drafts,
+                            const int* hint, int* target_out, float* logits) {
+  int T = 0;
+  for (int i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= e->slots || draft_lens[i] < 0) return 3;
+    if (e->committed[slots[i]] + draft_lens[i] > e->ctx) return 2;
+    T += draft_lens[i] + 1;
+  }
+  int *tok = (int*)malloc(sizeof(int) * (T + 1)), *sl = (int*)malloc(sizeof(int) * (T + 1)),
+      *ps = (int*)malloc(sizeof(int) * (T + 1));
+  int k = 0, d = 0;
+  for (int i = 0; i < n; ++i) {
+    const int s = slots[i], c = e->committed[s];
+    for (int r = 0; r <= draft_lens[i]; ++r) {
+      tok[k] = r == 0 ? e->tokens[(size_t)s * e->ctx + c - 1] : drafts[d + r - 1];
+      sl[k] = s, ps[k] = c - 1 + r;
+      ++k;
+    }
+    d += draft_lens[i];
+  }
+  if (T > 0) model_forward_gap(e->target, T, tok, sl, ps, target_out, logits, NULL, hint);
+  free(tok), free(sl), free(ps);
+  return 0;
+}
+
+/* CPU-baseline setup (bench.py): admits slots with a committed history of lens[i]
+ * seeded tokens and fills every model's KV cache rows [0, lens[i]-1) with seeded
+ * bf16 values in [-1, 1) instead of running the prefill forward. The timed
+ * verify / draft work on such a context costs exactly what it costs after a real
+ * prefill of the same length; the outcomes are not comparable with the GPU. */
+static void fill_kv(model* m, int slot, int upto, uint64_t seed) {
+  const so_model_desc* d = &m->d;
+  const int64_t per = (int64_t)upto * d->head_dim;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int l = 0; l < d->n_layers; ++l)
+    for (int h = 0; h < d->n_heads; ++h) {
+      uint16_t* kd = m->kc + kv_index(m, l, slot, h, 0);
+      uint16_t* vd = m->vc + kv_index(m, l, slot, h, 0);
+      const uint64_t st = so_mix_seed(seed, (uint64_t)slot, (uint64_t)l, (uint64_t)h);
+      for (int64_t i = 0; i < per; ++i) {
+        kd[i] = f2bf(uniform_pm1(st, (uint64_t)(2 * i)));
+        vd[i] = f2bf(uniform_pm1(st, (uint64_t)(2 * i + 1)));
+      }
+    }
+}
+
+int so_engine_fake_context(so_engine* e, int n, const int* slots, const int* lens, uint64_t seed) {
+  for (int i = 0; i < n; ++i) {
+    const int s = slots[i], L = lens[i];
+    if (s < 0 || s >= e->slots || L < 2 || L > e->ctx) return 3;
+    for (int p = 0; p < L; ++p)
+      e->tokens[(size_t)s * e->ctx + p] = (int)(so_splitmix64(so_mix_seed(seed, 7, (uint64_t)s, (uint64_t)p)) %
+                                                (uint64_t)e->target->d.vocab);
+    e->committed[s] = L;
+    fill_kv(e->target, s, L - 1, so_mix_seed(seed, 1, 0, 0));
+    for (int j = 0; j < e->n_ssm; ++j) {
+      fill_kv(e->ssm[j], s, L - 1, so_mix_seed(seed, 2, (uint64_t)j, 0));
+      e->ssm_len[(size_t)j * e->slots + s] = L - 1;
+    }
+  }
+  return 0;
 }

@@ -127,6 +127,12 @@ _SIGNATURES = {
     "spin_last_round_trace": [C.c_void_p, P_F32, C.c_int32],
     "spin_verify_bench": [C.c_void_p, C.c_int32, P_I32, P_I32, P_I32, C.c_int32, C.c_int32, C.c_void_p],
     "spin_gemm_info": [C.c_int32, C.c_int32, C.c_int32, C.c_int32, P_I32, P_I32, P_I32],
+    "spin_pack_device": [P_I32, C.c_int32, C.c_int32, P_I32, P_I32, C.POINTER(Segment), C.c_int32, P_I32, P_I64,
+                         P_I32],
+    "spin_device_count": [P_I32],
+    "spin_device_alloc": [C.c_int32, C.c_size_t, C.POINTER(C.c_void_p)],
+    "spin_device_free": [C.c_void_p],
+    "spin_memcpy": [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32],
     "spin_gemm": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                   C.c_void_p, C.c_void_p, C.c_void_p],
 }
@@ -159,3 +165,55 @@ def check(status: int) -> None:
 
 def exported_symbols() -> list[str]:
     return ["spin_abi_version", "spin_last_error", *_SIGNATURES.keys()]
+
+
+def device_count() -> int:
+    """CUDA devices visible to libspin.so (0 when there is no driver or device)."""
+    n = C.c_int32(0)
+    check(load().spin_device_count(C.byref(n)))
+    return n.value
+
+
+class DeviceBuffer:
+    """A zero-filled device allocation owned by libspin.so (no framework needed)."""
+
+    def __init__(self, nbytes: int, device: int = 0):
+        self.nbytes = int(nbytes)
+        p = C.c_void_p()
+        check(load().spin_device_alloc(device, self.nbytes, C.byref(p)))
+        self.ptr = p.value
+
+    @classmethod
+    def from_array(cls, a, device: int = 0) -> "DeviceBuffer":
+        import numpy as np
+
+        a = np.ascontiguousarray(a)
+        buf = cls(a.nbytes, device)
+        buf.upload(a)
+        return buf
+
+    def upload(self, a) -> None:
+        import numpy as np
+
+        a = np.ascontiguousarray(a)
+        assert a.nbytes <= self.nbytes
+        check(load().spin_memcpy(self.ptr, a.ctypes.data, a.nbytes, 1))
+
+    def download(self, dtype, shape):
+        import numpy as np
+
+        out = np.empty(shape, dtype=dtype)
+        assert out.nbytes <= self.nbytes
+        check(load().spin_memcpy(out.ctypes.data, self.ptr, out.nbytes, 2))
+        return out
+
+    def free(self) -> None:
+        if self.ptr:
+            check(load().spin_device_free(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

@@ -783,12 +783,7 @@ template <int HD>
 void launch_decode(const FwdMeta& m, int n_rows, const AttnGeom& g, const float* q, const AttnWork& w, bf16* out,
                    cudaStream_t s) {
   using DC = DecCfg<HD>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(attn_decode_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(DC::kTotal));
-    configured = true;
-  }
+  ensure_smem_optin(reinterpret_cast<const void*>(attn_decode_kernel<HD>), DC::kTotal);
   const int n_items = n_rows * std::max(1, w.chunks);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -815,12 +810,7 @@ template <int HD, int NQT>
 void launch_t(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m, int n_rows, const AttnGeom& g,
               const float* q, const AttnWork& w, bf16* out, cudaStream_t s) {
   using C = Cfg<HD, NQT, kVW>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(attn_kernel<HD, NQT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(C::kTotal));
-    configured = true;
-  }
+  ensure_smem_optin(reinterpret_cast<const void*>(attn_kernel<HD, NQT>), C::kTotal);
   const int n_items = n_rows * std::max(1, w.chunks);
   static const int early = [] {
     const char* e = std::getenv("SPIN_ATTN_EARLY");  // experiments only: 0 disables

@@ -25,6 +25,54 @@ int num_sms_cached() {
   }();
   return n;
 }
+
+// Device allocations released at scope exit (kernel-level entry points).
+struct DevAllocs {
+  std::vector<void*> ptrs;
+  void* get(size_t bytes) {
+    void* p = nullptr;
+    check_cuda(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "malloc");
+    ptrs.push_back(p);
+    return p;
+  }
+  ~DevAllocs() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+// Per-forward metadata of an extend-mode meta launch over n_req requests
+// packed into `rows` pack rows with `chunks` attention chunks per row.
+FwdMeta alloc_meta(DevAllocs& A, int n_req, int rows, int chunks) {
+  const int seg_cap = n_req + rows;
+  const int piece_cap = seg_cap + rows * chunks;
+  FwdMeta m{};
+  m.req_slot = static_cast<int32_t*>(A.get(4 * n_req));
+  m.req_qstart = static_cast<int32_t*>(A.get(4 * n_req));
+  m.req_qlen = static_cast<int32_t*>(A.get(4 * n_req));
+  m.req_kvlen = static_cast<int32_t*>(A.get(4 * n_req));
+  m.seg = static_cast<int32_t*>(A.get(20 * seg_cap));
+  m.row_ptr = static_cast<int32_t*>(A.get(4 * (rows + 1)));
+  m.row_len = static_cast<int32_t*>(A.get(4 * rows));
+  m.row_seg = static_cast<int32_t*>(A.get(4 * seg_cap));
+  m.req_seg0 = static_cast<int32_t*>(A.get(4 * n_req));
+  m.req_nseg = static_cast<int32_t*>(A.get(4 * n_req));
+  m.n_seg = static_cast<int32_t*>(A.get(8));
+  m.item_ptr = static_cast<int32_t*>(A.get(4 * (rows * chunks + 1)));
+  m.pieces = static_cast<int32_t*>(A.get(64 * static_cast<size_t>(piece_cap)));
+  m.req_pptr = static_cast<int32_t*>(A.get(4 * (n_req + 1)));
+  m.req_plist = static_cast<int32_t*>(A.get(4 * static_cast<size_t>(piece_cap)));
+  m.n_pieces = static_cast<int32_t*>(A.get(4));
+  m.err = static_cast<int32_t*>(A.get(4));
+  check_cuda(cudaMemset(m.err, 0, 4), "memset");
+  m.piece_cap = piece_cap;
+  return m;
+}
+
+void check_meta_status(const FwdMeta& m, const char* who) {
+  int32_t e = 0;
+  check_cuda(cudaMemcpy(&e, m.err, 4, cudaMemcpyDeviceToHost), "d2h status");
+  if (e != 0) fail(SPIN_CAPACITY_ERROR, std::string(who) + ": attention work list exceeds its buffers");
+}
 }  // namespace
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 }  // namespace spin
@@ -377,39 +425,10 @@ spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int3
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int rows = width > 0 ? std::min<int>(width, n_req) : n_req;
     const int chunks = attn_chunks(rows, n_heads, sms);
-    const int seg_cap = n_req + rows;
-    const int piece_cap = seg_cap + rows * chunks;
-    std::vector<void*> allocs;
-    auto dal = [&](size_t bytes) {
-      void* p = nullptr;
-      check_cuda(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "malloc");
-      allocs.push_back(p);
-      return p;
-    };
-    struct Free {
-      std::vector<void*>* a;
-      ~Free() {
-        for (void* p : *a) cudaFree(p);
-      }
-    } freer{&allocs};
-    FwdMeta m{};
-    m.req_slot = static_cast<int32_t*>(dal(4 * n_req));
-    m.req_qstart = static_cast<int32_t*>(dal(4 * n_req));
-    m.req_qlen = static_cast<int32_t*>(dal(4 * n_req));
-    m.req_kvlen = static_cast<int32_t*>(dal(4 * n_req));
-    m.seg = static_cast<int32_t*>(dal(20 * seg_cap));
-    m.row_ptr = static_cast<int32_t*>(dal(4 * (rows + 1)));
-    m.row_len = static_cast<int32_t*>(dal(4 * rows));
-    m.row_seg = static_cast<int32_t*>(dal(4 * seg_cap));
-    m.req_seg0 = static_cast<int32_t*>(dal(4 * n_req));
-    m.req_nseg = static_cast<int32_t*>(dal(4 * n_req));
-    m.n_seg = static_cast<int32_t*>(dal(4));
-    m.item_ptr = static_cast<int32_t*>(dal(4 * (rows * chunks + 1)));
-    m.pieces = static_cast<int32_t*>(dal(64 * piece_cap));
-    m.req_pptr = static_cast<int32_t*>(dal(4 * (n_req + 1)));
-    m.req_plist = static_cast<int32_t*>(dal(4 * piece_cap));
-    m.n_pieces = static_cast<int32_t*>(dal(4));
-    m.piece_cap = piece_cap;
+    DevAllocs allocs;
+    FwdMeta m = alloc_meta(allocs, n_req, rows, chunks);
+    const int piece_cap = m.piece_cap;
+    auto dal = [&](size_t bytes) { return allocs.get(bytes); };
     const int qpad = 8 * ((qmax + 7) / 8);
     const size_t np = static_cast<size_t>(piece_cap) * n_heads * qpad;
     AttnWork w{};
@@ -443,6 +462,102 @@ spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int3
     launch_attention(tk, tv, m, rows, n_req, g, static_cast<const float*>(q), w, static_cast<bf16*>(out), s);
     check_cuda(cudaGetLastError(), "attention launch");
     check_cuda(cudaStreamSynchronize(s), "attention");
+    check_meta_status(m, "spin_attention");
+  });
+}
+
+// ---------------------------------------------------------------- device plumbing
+// Torch-free device memory for callers and tests (the product needs no framework).
+spin_status spin_device_count(int32_t* count) {
+  if (!count) {
+    set_last_error("spin_device_count: null argument");
+    return SPIN_INPUT_ERROR;
+  }
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  *count = e == cudaSuccess ? n : 0;
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    set_last_error(std::string("no CUDA device: ") + cudaGetErrorString(e));
+  } else {
+    set_last_error("");
+  }
+  return SPIN_OK;
+}
+
+spin_status spin_device_alloc(int32_t device, size_t bytes, void** ptr) {
+  return guarded([&] {
+    if (!ptr) fail(SPIN_INPUT_ERROR, "spin_device_alloc: null argument");
+    check_cuda(cudaSetDevice(device), "cudaSetDevice");
+    check_cuda(cudaMalloc(ptr, std::max<size_t>(bytes, 16)), "cudaMalloc");
+    check_cuda(cudaMemset(*ptr, 0, std::max<size_t>(bytes, 16)), "cudaMemset");
+  });
+}
+
+spin_status spin_device_free(void* ptr) {
+  return guarded([&] { check_cuda(cudaFree(ptr), "cudaFree"); });
+}
+
+spin_status spin_memcpy(void* dst, const void* src, size_t bytes, int32_t kind) {
+  return guarded([&] {
+    if (kind < 1 || kind > 3) fail(SPIN_INPUT_ERROR, "spin_memcpy: kind must be 1 (H2D), 2 (D2H) or 3 (D2D)");
+    const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice : kind == 2 ? cudaMemcpyDeviceToHost
+                                                                           : cudaMemcpyDeviceToDevice;
+    if (bytes > 0) check_cuda(cudaMemcpy(dst, src, bytes, k), "cudaMemcpy");
+  });
+}
+
+// Device request decomposition (the meta kernel's packer, kernels.cu) on its own:
+// same contract as spin_pack, computed on the GPU; used to pin the device packer
+// to the reference goldens (packing.cpp:16-103).
+spin_status spin_pack_device(const int32_t* kv_lens, int32_t n, int32_t width, int32_t* length, int32_t* rows,
+                             spin_segment* segments, int32_t seg_cap, int32_t* n_segments, int64_t* padding_tokens,
+                             int32_t* q_replica_rows) {
+  return guarded([&] {
+    if (n < 0 || (n > 0 && kv_lens == nullptr)) fail(SPIN_INPUT_ERROR, "spin_pack_device: bad input arrays");
+    // validation and error taxonomy identical to the host packer (pack.cpp)
+    pack_validate(kv_lens, n, width);
+    if (n == 0) {
+      if (length) *length = 0;
+      if (rows) *rows = 0;
+      if (n_segments) *n_segments = 0;
+      if (padding_tokens) *padding_tokens = 0;
+      return;
+    }
+    if (n > 1024) fail(SPIN_SIZE_ERROR, "spin_pack_device: at most 1024 requests per pack");
+    const int nrows = std::min<int>(width, n);
+    DevAllocs allocs;
+    FwdMeta m = alloc_meta(allocs, n, nrows, 1);
+    std::vector<int32_t> ones(n, 1), qs(n), zeros(n, 0);
+    for (int i = 0; i < n; ++i) qs[i] = i;
+    check_cuda(cudaMemcpy(m.req_slot, zeros.data(), 4 * n, cudaMemcpyHostToDevice), "h2d");
+    check_cuda(cudaMemcpy(m.req_qstart, qs.data(), 4 * n, cudaMemcpyHostToDevice), "h2d");
+    check_cuda(cudaMemcpy(m.req_qlen, ones.data(), 4 * n, cudaMemcpyHostToDevice), "h2d");
+    check_cuda(cudaMemcpy(m.req_kvlen, kv_lens, 4 * n, cudaMemcpyHostToDevice), "h2d");
+    MetaArgs a{};
+    a.mode = kMetaExtend;
+    a.n_req = n;
+    a.width = nrows;
+    a.chunks = 1;
+    SlotState st{};
+    launch_meta(a, st, m, nullptr);
+    check_cuda(cudaGetLastError(), "meta launch");
+    check_cuda(cudaDeviceSynchronize(), "meta");
+    check_meta_status(m, "spin_pack_device");
+    int32_t ns[2] = {0, 0};
+    check_cuda(cudaMemcpy(ns, m.n_seg, 8, cudaMemcpyDeviceToHost), "d2h");
+    if (ns[0] > seg_cap) fail(SPIN_SIZE_ERROR, "spin_pack_device: segment buffer too small");
+    std::vector<int32_t> seg(static_cast<size_t>(ns[0]) * 5), nseg(n);
+    check_cuda(cudaMemcpy(seg.data(), m.seg, seg.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+    check_cuda(cudaMemcpy(nseg.data(), m.req_nseg, 4 * n, cudaMemcpyDeviceToHost), "d2h");
+    int64_t total = 0;
+    for (int i = 0; i < n; ++i) total += kv_lens[i];
+    if (length) *length = ns[1];
+    if (rows) *rows = nrows;
+    if (n_segments) *n_segments = ns[0];
+    if (padding_tokens) *padding_tokens = static_cast<int64_t>(nrows) * ns[1] - total;
+    if (segments) std::memcpy(segments, seg.data(), seg.size() * 4);
+    if (q_replica_rows) std::memcpy(q_replica_rows, nseg.data(), 4 * n);
   });
 }
 

@@ -438,12 +438,7 @@ cudaError_t launch_t(const DraftProj& a, int units, cudaStream_t s) {
   const int KB = (a.K + 63) / 64;
   const size_t smem = C::smem_bytes(KB);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(dproj_kernel<NW, NT, MT, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    configured = smem;
-  }
+  ensure_smem_optin(reinterpret_cast<const void*>(dproj_kernel<NW, NT, MT, NORM>), smem);
   return launch_pdl(dproj_kernel<NW, NT, MT, NORM>, dim3(units), dim3(NW * 32), smem, s, a);
 }
 

@@ -214,7 +214,8 @@ void Engine::init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool l
   ln.meta.row_seg = dalloc<int32_t>(A, ln.seg_cap);
   ln.meta.req_seg0 = dalloc<int32_t>(A, R_cap);
   ln.meta.req_nseg = dalloc<int32_t>(A, R_cap);
-  ln.meta.n_seg = dalloc<int32_t>(A, 1);
+  ln.meta.n_seg = dalloc<int32_t>(A, 2);
+  ln.meta.err = d_err_;
   ln.h = dalloc<float>(A, static_cast<size_t>(T_cap) * m.D);
   ln.xn = dalloc<bf16>(A, static_cast<size_t>(T_cap) * m.D);
   ln.q = dalloc<float>(A, static_cast<size_t>(T_cap) * m.D);
@@ -502,6 +503,14 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
   check_cuda(cudaStreamCreateWithFlags(&sv_, cudaStreamNonBlocking), "stream");
   ss_.resize(n_ssm);
   for (auto& s : ss_) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  // sticky device status word (FwdMeta::err), host-mapped: read after every synchronisation
+  void* err_host = nullptr;
+  check_cuda(cudaHostAlloc(&err_host, 4, cudaHostAllocMapped), "pinned status");
+  h_err_ = static_cast<volatile int32_t*>(err_host);
+  *h_err_ = 0;
+  void* err_dev = nullptr;
+  check_cuda(cudaHostGetDevicePointer(&err_dev, err_host, 0), "mapped status");
+  d_err_ = static_cast<int32_t*>(err_dev);
   init_model(target_, target, false);
   ssm_.resize(n_ssm);
   for (int j = 0; j < n_ssm; ++j) init_model(ssm_[j], ssms[j], true);
@@ -542,7 +551,7 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
   ev_spec_end_.resize(n_ssm);  // per-SSM draft end (timing; the event trace)
   for (auto& e : ev_spec_end_) check_cuda(cudaEventCreate(&e), "event");
   last_spec_ms_.assign(n_ssm, -1.f);
-  check_cuda(cudaStreamSynchronize(sv_), "init sync");
+  sync_sv("init sync");
 }
 
 Engine::~Engine() {
@@ -562,6 +571,7 @@ Engine::~Engine() {
   cudaFree(st_.tokens), cudaFree(st_.committed), cudaFree(st_.ssm_len), cudaFree(st_.drafts);
   for (void* p : plan_tables_) cudaFree(p);
   if (stamps_) cudaFree(stamps_);
+  cudaFreeHost(const_cast<int32_t*>(h_err_));
   cudaFreeHost(pin_in_), cudaFreeHost(pin_out_), cudaFree(d_in_), cudaFree(d_out_), cudaFree(d_emitted_);
   cudaEventDestroy(ev_fork_), cudaEventDestroy(ev_start_), cudaEventDestroy(ev_draft_), cudaEventDestroy(ev_end_);
   for (auto& e : ev_join_) cudaEventDestroy(e);
@@ -570,9 +580,20 @@ Engine::~Engine() {
   cudaStreamDestroy(sv_);
 }
 
+void Engine::sync_sv(const char* what) {
+  check_cuda(cudaStreamSynchronize(sv_), what);
+  if (*h_err_ != 0) {
+    const int e = *h_err_;
+    *h_err_ = 0;
+    fail(SPIN_CAPACITY_ERROR, std::string(what) + (e == 2 ? ": a round would commit past max_ctx"
+                                                           : ": attention work list exceeds its buffers") +
+                                  " (device status " + std::to_string(e) + ")");
+  }
+}
+
 void Engine::sync_state_from_device() {
   if (!mirror_stale_) return;
-  check_cuda(cudaStreamSynchronize(sv_), "sync");
+  sync_sv("sync");
   check_cuda(cudaMemcpy(h_tokens_.data(), st_.tokens, h_tokens_.size() * 4, cudaMemcpyDeviceToHost), "d2h");
   check_cuda(cudaMemcpy(h_committed_.data(), st_.committed, h_committed_.size() * 4, cudaMemcpyDeviceToHost), "d2h");
   check_cuda(cudaMemcpy(h_ssm_len_.data(), st_.ssm_len, h_ssm_len_.size() * 4, cudaMemcpyDeviceToHost), "d2h");
@@ -603,7 +624,7 @@ void Engine::extend(int model, const std::vector<std::tuple<int, int, int>>& ran
     a.chunks = attn_chunks(R, m.H, num_sms_);
     launch_meta(a, st_, ln.meta, sv_);
     forward(m, ln, FwdShape{T, R, R, kExtendQ}, sv_, 0);
-    check_cuda(cudaStreamSynchronize(sv_), "extend");  // host vectors are reused
+    sync_sv("extend");  // host vectors are reused
     rt.clear(), rs.clear(), rp.clear(), qs_.clear(), ql.clear(), kv.clear(), sl.clear();
   };
   for (const auto& [slot, from, to] : ranges) {
@@ -665,7 +686,7 @@ void Engine::prefill(int n, const int32_t* slots, const int32_t* lens, const int
                  "h2d");
     }
   }
-  check_cuda(cudaStreamSynchronize(sv_), "prefill");
+  sync_sv("prefill");
 }
 
 void Engine::switch_ssm(int n, const int32_t* slots, const int32_t* ssm_of) {
@@ -691,7 +712,7 @@ void Engine::switch_ssm(int n, const int32_t* slots, const int32_t* ssm_of) {
                                  cudaMemcpyHostToDevice, sv_),
                  "h2d");
     }
-    check_cuda(cudaStreamSynchronize(sv_), "switch");
+    sync_sv("switch");
   }
 }
 
@@ -855,7 +876,7 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, spin_roun
   } else {
     capture_round(p);
   }
-  check_cuda(cudaStreamSynchronize(sv_), "round");
+  sync_sv("round");
   dump_stamps();
   float draft_ms = 0.f, total_ms = 0.f;
   check_cuda(cudaEventElapsedTime(&draft_ms, ev_start_, ev_draft_), "event timing");
@@ -912,7 +933,8 @@ void Engine::run_rounds(int n, const int32_t* slots, const int32_t* ssm_of, int 
   sync_state_from_device();
   const int W = opts_.window;
   for (int i = 0; i < n; ++i) {
-    if (ssm_of[i] >= 0 && h_committed_[slots[i]] + rounds * (W + 1) + 1 > opts_.max_ctx)
+    // the host-driven warm-up round + `rounds` graph replays, each committing up to W + 1
+    if (ssm_of[i] >= 0 && h_committed_[slots[i]] + static_cast<int64_t>(rounds + 1) * (W + 1) > opts_.max_ctx)
       fail(SPIN_CAPACITY_ERROR, "run_rounds: context would overflow max_ctx");
   }
   // one host-driven round first: validates, switches SSMs, captures the graph
@@ -935,7 +957,7 @@ void Engine::run_rounds(int n, const int32_t* slots, const int32_t* ssm_of, int 
     check_cuda(cudaMemcpyAsync(d_counts + r, d_emitted_, 8, cudaMemcpyDeviceToDevice, sv_), "count");
   }
   check_cuda(cudaEventRecord(b, sv_), "event");
-  check_cuda(cudaStreamSynchronize(sv_), "rounds");
+  sync_sv("rounds");
   float t = 0.f;
   cudaEventElapsedTime(&t, a, b);
   check_cuda(cudaMemcpy(counts.data(), d_counts, rounds * 8, cudaMemcpyDeviceToHost), "d2h");
@@ -1043,7 +1065,7 @@ void Engine::kernel_bench(int kind, int iters, double* us_per_launch, double* by
   check_cuda(cudaEventRecord(a, sv_), "event");
   for (int i = 0; i < iters; ++i) check_cuda(cudaGraphLaunch(exec, sv_), "graph");
   check_cuda(cudaEventRecord(b, sv_), "event");
-  check_cuda(cudaStreamSynchronize(sv_), "sync");
+  sync_sv("sync");
   float ms = 0.f;
   cudaEventElapsedTime(&ms, a, b);
   cudaEventDestroy(a);
@@ -1131,7 +1153,7 @@ void Engine::verify_bench(int n, const int32_t* slots, const int32_t* draft_lens
   check_cuda(cudaEventRecord(e0, sv_), "event");
   for (int i = 0; i < iters; ++i) check_cuda(cudaGraphLaunch(exec, sv_), "graph");
   check_cuda(cudaEventRecord(e1, sv_), "event");
-  check_cuda(cudaStreamSynchronize(sv_), "verify_bench");
+  sync_sv("verify_bench");
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0), cudaEventDestroy(e1);

@@ -126,6 +126,9 @@ class Engine {
   };
   std::vector<ProfRec> prof_recs_;
   void sync_state_from_device();
+  void sync_sv(const char* what);  // synchronise sv_ and raise a flagged device status
+  volatile int32_t* h_err_ = nullptr;
+  int32_t* d_err_ = nullptr;
 
   spin_engine_opts opts_{};
   int num_sms_ = 148;

@@ -450,10 +450,7 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  });
+  ensure_smem_optin(reinterpret_cast<const void*>(gemm_tc_kernel), 227 * 1024);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(plan.grid);
   cfg.blockDim = dim3(kThreads);

@@ -91,4 +91,9 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
 bool encode_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                       uint32_t box_cols, bool swizzle128);
 
+// Dynamic shared-memory opt-in of `kernel` on the CURRENT device, set once per
+// (kernel, device) and raised when a larger size is requested (thread-safe; the
+// attribute is per device context, so a second spin_ctx on another GPU needs its own).
+cudaError_t ensure_smem_optin(const void* kernel, size_t bytes);
+
 }  // namespace spin

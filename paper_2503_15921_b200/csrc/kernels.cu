@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
         sg[0] = i, sg[1] = i, sg[2] = 0, sg[3] = longest, sg[4] = 0;
       }
       nseg = n;
+      if (lane == 0) s_misc[2] = longest;
     } else {
       long long total = 0;
       for (int i = lane; i < n; i += 32) total += s_len[i];
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
       // always fits (capacity >= total), so the reference's upward search
       // stops at its first iteration.
       const int L = static_cast<int>((total + rows - 1) / rows);
+      if (lane == 0) s_misc[2] = L;
       for (int k = 0; k < n; ++k) {
         const int id = s_order[k];
         const int need = s_len[id];
@@ -250,7 +252,11 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
   const int nseg = s_misc[0];
   const int nch = max(1, a.chunks);
   // ---- segments out; per-request segment ranges (a request's segments are consecutive)
-  if (tid == 0) s_misc[1] = 0;
+  if (tid == 0) {
+    s_misc[1] = 0;
+    m.n_seg[0] = nseg;
+    m.n_seg[1] = s_misc[2];
+  }
   __syncthreads();
   for (int s = tid; s < nseg; s += kMetaThreads) {
 #pragma unroll
@@ -316,7 +322,15 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
     if (lane == 0) dst[cnt] = carry;
   }
   __syncthreads();
-  if (s_rbase[rows] > m.piece_cap) __trap();  // piece buffers sized by the engine
+  if (s_rbase[rows] > m.piece_cap) {  // piece buffers sized by the engine: flag, leave no work
+    for (int r = tid; r <= rows * nch; r += kMetaThreads) m.item_ptr[r] = 0;
+    for (int r = tid; r <= n; r += kMetaThreads) m.req_pptr[r] = 0;
+    if (tid == 0) {
+      m.n_pieces[0] = 0;
+      if (m.err) *reinterpret_cast<volatile int32_t*>(m.err) = 1;  // may be host-mapped
+    }
+    return;
+  }
   for (int r = tid; r <= rows; r += kMetaThreads) m.row_ptr[r] = s_ptr[r];
   for (int r = tid; r <= n; r += kMetaThreads) m.req_pptr[r] = s_rptr[r];
   if (tid == 0) {
@@ -580,6 +594,10 @@ __global__ void accept_kernel(FwdMeta m, int n_req, int W, const int32_t* list, 
       }
     }
   }
+  if (c + W + 1 > st.ctx) {  // the host refuses such rounds; never commit past the slot's context
+    if (lane == 0 && m.err) *reinterpret_cast<volatile int32_t*>(m.err) = 2;
+    return;
+  }
   if (lane == 0) {
     for (int k = 0; k < a; ++k) hist[c + k] = dr[k];
     hist[c + a] = bonus;
@@ -754,11 +772,7 @@ void launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Ar
 }  // namespace
 
 void launch_meta(const MetaArgs& a, const SlotState& st, const FwdMeta& m, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(meta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMetaSmem));
-    configured = true;
-  }
+  ensure_smem_optin(reinterpret_cast<const void*>(meta_kernel), kMetaSmem);
   launch_pdl(meta_kernel, dim3(1), dim3(kMetaThreads), kMetaSmem, s, a, st, m);
 }
 

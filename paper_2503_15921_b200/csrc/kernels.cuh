@@ -39,7 +39,9 @@ struct FwdMeta {
   int32_t* row_seg;    // [S] segment ids grouped by pack row, column order
   int32_t* req_seg0;   // [R] first segment (segments of a request are contiguous)
   int32_t* req_nseg;   // [R]
-  int32_t* n_seg;      // [1]
+  int32_t* n_seg;      // [2] segment count, pack length L (packing.hpp PackedLayout::length)
+  int32_t* err;        // [1] sticky device status: 1 = attention piece buffer overflow (the host
+                       //     reads it back with the outcome and raises SPIN_CAPACITY_ERROR)
 };
 
 // Persistent per-slot state on the device.

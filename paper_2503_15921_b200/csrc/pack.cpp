@@ -60,10 +60,14 @@ bool place_at_length(const int32_t* len, int32_t n, int32_t rows, int32_t L, con
 
 }  // namespace
 
-PackResult pack_lengths(const int32_t* kv_lens, int32_t n, int32_t width) {
+void pack_validate(const int32_t* kv_lens, int32_t n, int32_t width) {
   if (width < 1) fail(SPIN_CONFIG_ERROR, "pack: width must be at least 1");
   for (int32_t i = 0; i < n; ++i)
     if (kv_lens[i] < 1) fail(SPIN_CONFIG_ERROR, "pack: kv lengths must be at least 1");
+}
+
+PackResult pack_lengths(const int32_t* kv_lens, int32_t n, int32_t width) {
+  pack_validate(kv_lens, n, width);
   PackResult res;
   if (n <= 0) return res;
   const int32_t rows = std::min(width, n);

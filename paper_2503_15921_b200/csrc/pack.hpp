@@ -1,6 +1,6 @@
 // Request decomposition: the host restatement of the reference packer
 // (packing.cpp:16-103) plus the verify cost accounting (slot_engine.cpp:24-45).
-// The same algorithm runs on the device in pack_kernel (kernels.cu) so that the
+// The same algorithm runs on the device in meta_kernel (kernels.cu) so that the
 // device-resident round loop needs no host round trip; the parity tests check
 // the two bit-for-bit.
 #pragma once
@@ -21,6 +21,7 @@ struct PackResult {
 };
 
 // Throws SpinError(SPIN_CONFIG_ERROR) on width < 1 or any length < 1.
+void pack_validate(const int32_t* kv_lens, int32_t n, int32_t width);
 PackResult pack_lengths(const int32_t* kv_lens, int32_t n, int32_t width);
 int64_t naive_padding_of(const int32_t* kv_lens, int32_t n);  // SPIN_INPUT_ERROR on n == 0
 

@@ -54,7 +54,10 @@ class RoundTrace:
                             "slot": self.slot})
         self.llm_busy += v1 - v0
         self.llm_idle += v0 - t0
-        self.accepted += int(np.asarray(out["accepted"])[ssm_of >= 0].sum())
+        # accepted + bonus per served request: EventTrace.accepted_tokens sums
+        # apply_outcome() (pipeline.cpp:26-35), which counts the bonus token
+        served = ssm_of >= 0
+        self.accepted += int(np.asarray(out["accepted"])[served].sum()) + int(served.sum())
         self.t = v1
         self.slot += 1
 

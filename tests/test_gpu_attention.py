@@ -1,54 +1,63 @@
-"""Packed ragged causal attention kernel (attention.cu) against a plain PyTorch
-fp32 reference of the same op."""
+"""Packed ragged causal attention kernel (attention.cu) against a plain fp32
+reference of the same op (numpy, on the same bf16 K/V). Device buffers through
+libspin.so only."""
 import numpy as np
 import pytest
 
 from paper_2503_15921_b200 import _lib
+from tests._dev import DeviceBuffer, bf16_bits_to_f32, f32_to_bf16_bits
 
 pytestmark = pytest.mark.gpu
-torch = pytest.importorskip("torch")
 
 
-def torch_ref(q, kc, vc, layer, slots, qlens, kvlens, H, hd):
-    out = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
+def fp32_ref(q, kc, vc, layer, slots, qlens, kvlens, H, hd):
+    out = np.zeros(q.shape, np.float32)
     r0 = 0
     for s, ql, kv in zip(slots, qlens, kvlens):
         for h in range(H):
-            qq = q[r0:r0 + ql, h * hd:(h + 1) * hd].float()
-            k = kc[layer, s, h, :kv].float()
-            v = vc[layer, s, h, :kv].float()
-            sc = (qq @ k.t()) * (1.0 / np.sqrt(hd))
-            pos = torch.arange(kv, device=q.device)
-            qpos = torch.arange(kv - ql, kv, device=q.device)
-            sc = sc.masked_fill(pos[None, :] > qpos[:, None], float("-inf"))
-            out[r0:r0 + ql, h * hd:(h + 1) * hd] = torch.softmax(sc, -1) @ v
+            qq = q[r0:r0 + ql, h * hd:(h + 1) * hd]
+            k = kc[layer, s, h, :kv]
+            v = vc[layer, s, h, :kv]
+            sc = (qq @ k.T) * np.float32(1.0 / np.sqrt(hd))
+            pos = np.arange(kv)
+            qpos = np.arange(kv - ql, kv)
+            sc = np.where(pos[None, :] > qpos[:, None], -np.inf, sc)
+            sc = np.exp(sc - sc.max(1, keepdims=True))
+            out[r0:r0 + ql, h * hd:(h + 1) * hd] = (sc / sc.sum(1, keepdims=True)) @ v
         r0 += ql
     return out
 
 
+def run(hd, H, L, S, ctx, layer, slots, qls, kvl, width, seed):
+    rng = np.random.default_rng(seed)
+    kb = f32_to_bf16_bits(rng.standard_normal((L, S, H, ctx, hd), dtype=np.float32))
+    vb = f32_to_bf16_bits(rng.standard_normal((L, S, H, ctx, hd), dtype=np.float32))
+    T = int(qls.sum())
+    q = rng.standard_normal((T, H * hd), dtype=np.float32)
+    kd, vd, qd = DeviceBuffer.from_array(kb), DeviceBuffer.from_array(vb), DeviceBuffer.from_array(q)
+    od = DeviceBuffer(2 * T * H * hd)
+    P = lambda a: a.ctypes.data_as(_lib.P_I32)
+    _lib.check(_lib.load().spin_attention(None, H, hd, L, S, ctx, layer, kd.ptr, vd.ptr, qd.ptr, len(slots), P(slots),
+                                          P(qls), P(kvl), width, od.ptr))
+    out = bf16_bits_to_f32(od.download(np.uint16, (T, H * hd)))
+    kc = bf16_bits_to_f32(kb).reshape(L, S, H, ctx, hd)
+    vc = bf16_bits_to_f32(vb).reshape(L, S, H, ctx, hd)
+    return out, fp32_ref(q, kc, vc, layer, slots, qls, kvl, H, hd)
+
+
 @pytest.mark.parametrize("hd,H,width,qlen", [(128, 4, 0, 5), (64, 3, 0, 2), (128, 2, 3, 1), (64, 2, 5, 8),
                                              (128, 2, 0, 17)])
-def test_attention_matches_torch(hd, H, width, qlen):
-    g = torch.Generator(device="cpu").manual_seed(hd + H + width + qlen)
+def test_attention_matches_fp32(hd, H, width, qlen):
     L, S, ctx = 2, 6, 700
-    kc = torch.randn((L, S, H, ctx, hd), generator=g).to(torch.bfloat16).cuda()
-    vc = torch.randn((L, S, H, ctx, hd), generator=g).to(torch.bfloat16).cuda()
     rng = np.random.default_rng(qlen)
     slots = np.array([4, 0, 2, 5, 1], np.int32)
     kvl = rng.integers(qlen, 650, len(slots)).astype(np.int32)
     kvl[1] = qlen  # a request that sees only its own queries
     qls = np.full(len(slots), qlen, np.int32)
-    T = int(qls.sum())
-    q = torch.randn((T, H * hd), generator=g).cuda()
-    out = torch.empty((T, H * hd), dtype=torch.bfloat16, device="cuda")
-    lib = _lib.load()
-    P = lambda a: a.ctypes.data_as(_lib.P_I32)
-    _lib.check(lib.spin_attention(None, H, hd, L, S, ctx, 1, kc.data_ptr(), vc.data_ptr(), q.data_ptr(), len(slots),
-                                  P(slots), P(qls), P(kvl), width, out.data_ptr()))
-    ref = torch_ref(q, kc, vc, 1, slots, qls, kvl, H, hd)
-    err = (out.float() - ref).abs().max().item()
+    out, ref = run(hd, H, L, S, ctx, 1, slots, qls, kvl, width, hd + H + width + qlen)
+    err = float(np.abs(out - ref).max())
     assert err <= 1e-2, err  # bf16 output rounding (|o| ~ 1)
-    mism = (out.float() != ref.to(torch.bfloat16).float()).float().mean().item()
+    mism = float((out != bf16_bits_to_f32(f32_to_bf16_bits(ref))).mean())
     assert mism < 0.02, mism
 
 
@@ -56,18 +65,10 @@ def test_attention_matches_torch(hd, H, width, qlen):
 def test_attention_many_segments_per_row(hd, qlen, width):
     """Rows holding several segments whose tile counts are not multiples of the
     consumer-warp count (ring-stage ownership across segment boundaries)."""
-    g = torch.Generator(device="cpu").manual_seed(7 * hd + qlen)
     H, L, S, ctx = 2, 1, 12, 1100
-    kc = torch.randn((L, S, H, ctx, hd), generator=g).to(torch.bfloat16).cuda()
-    vc = torch.randn((L, S, H, ctx, hd), generator=g).to(torch.bfloat16).cuda()
     slots = np.arange(S, dtype=np.int32)[::-1].copy()
     kvl = np.array([37, 101, 1033, 64, 65, 200, 300, 33, 511, 97, 129, 700], np.int32)
     kvl = np.maximum(kvl, qlen).astype(np.int32)
     qls = np.full(S, qlen, np.int32)
-    q = torch.randn((int(qls.sum()), H * hd), generator=g).cuda()
-    out = torch.empty((int(qls.sum()), H * hd), dtype=torch.bfloat16, device="cuda")
-    P = lambda a: a.ctypes.data_as(_lib.P_I32)
-    _lib.check(_lib.load().spin_attention(None, H, hd, L, S, ctx, 0, kc.data_ptr(), vc.data_ptr(), q.data_ptr(), S,
-                                          P(slots), P(qls), P(kvl), width, out.data_ptr()))
-    ref = torch_ref(q, kc, vc, 0, slots, qls, kvl, H, hd)
-    assert (out.float() - ref).abs().max().item() <= 1e-2
+    out, ref = run(hd, H, L, S, ctx, 0, slots, qls, kvl, width, 7 * hd + qlen)
+    assert float(np.abs(out - ref).max()) <= 1e-2

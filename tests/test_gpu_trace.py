@@ -21,11 +21,14 @@ def test_trace_schema_and_invariants():
     eng.prefill(range(B), synthetic_prompts(B, 16, 64, TINY_TARGET.vocab, 99))
     slots = np.arange(B, dtype=np.int32)
     tr = RoundTrace()
+    emitted = 0
     for r in range(4):
         assign = np.array([(i + r) % 2 for i in range(B)], np.int32)
         if r == 3:
             assign[:4] = -1  # idle requests
-        tr.record(eng, assign, eng.round(slots, assign))
+        out = eng.round(slots, assign)
+        tr.record(eng, assign, out)
+        emitted += int(out["accepted"][assign >= 0].sum()) + int((assign >= 0).sum())
     eng.close()
     rows = list(csv.DictReader(io.StringIO(tr.csv())))
     assert list(rows[0].keys()) == ["time_sec", "resource", "kind", "micro_batch", "slot"]
@@ -41,4 +44,4 @@ def test_trace_schema_and_invariants():
         assert ends and max(ends) <= s0 + 1e-9  # causality
     makespan = verify[-1][1]
     assert abs(doc["totals"]["llm_busy_sec"] + doc["totals"]["llm_idle_sec"] - makespan) < 1e-6
-    assert doc["totals"]["accepted_tokens"] >= 0
+    assert doc["totals"]["accepted_tokens"] == emitted  # accepted + bonus (pipeline.cpp:26-35)
