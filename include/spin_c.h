@@ -222,6 +222,55 @@ spin_status spin_verify_bench(spin_ctx* ctx, int32_t n, const int32_t* slots, co
                               const int32_t* drafts, int32_t packed, int32_t iters, spin_verify_stats* out);
 
 /* ------------------------------------------------------------------------
+ * Multi-GPU exchange: requests shard across ranks
+ * (one process per GPU, replicated weights); the only collective of the path is
+ * an all-gather of the selector's per-(request, SSM) ArmEstimate{sum, count}
+ * rows (bandit.hpp:24-39; update sites bandit.cpp:166-169, policies.cpp:69-72).
+ * A communicator spans processes, so it is its own handle (one per device)
+ * rather than part of spin_ctx. Backends: NCCL (ncclAllGather over NVLink,
+ * libnccl loaded at first use) and TCP (same semantics, no GPU: CPU tests).
+ * id: NCCL -> the ncclUniqueId bytes from rank 0's spin_comm_unique_id, shared
+ * out of band; TCP -> "ipv4:port" of rank 0 (spin_comm_unique_id picks a free
+ * loopback port). Results are rank-ordered and identical on every rank.
+ * ---------------------------------------------------------------------- */
+#define SPIN_COMM_ID_BYTES 128
+enum { SPIN_COMM_NCCL = 0, SPIN_COMM_TCP = 1 };
+enum { SPIN_REDUCE_SUM = 0, SPIN_REDUCE_MAX = 1 };
+typedef struct spin_comm spin_comm;
+spin_status spin_comm_unique_id(int32_t backend, uint8_t* id /* SPIN_COMM_ID_BYTES */);
+spin_status spin_comm_create(int32_t backend, int32_t device, int32_t rank, int32_t world, const uint8_t* id,
+                             spin_comm** out);
+spin_status spin_comm_destroy(spin_comm* comm);
+spin_status spin_comm_info(spin_comm* comm, int32_t* rank, int32_t* world, int32_t* backend);
+/* local: this rank's rows [rows][m][2] = {sum, count} (every rank passes the same
+ * `rows`: pad the shards to the largest); global: [world * rows][m][2], rank-major. */
+spin_status spin_stats_allgather(spin_comm* comm, const double* local, double* global, int32_t rows, int32_t m);
+/* In-place element-wise reduction over ranks (rank order, deterministic). */
+spin_status spin_comm_allreduce(spin_comm* comm, double* values, int32_t n, int32_t op);
+spin_status spin_comm_barrier(spin_comm* comm);
+
+/* ------------------------------------------------------------------------
+ * LBSS, the learning-based SSM selector (host side; bandit.cpp:11-332 restated in
+ * C++: same Rng draw order, schedule and tie-breaking as the reference, pinned by
+ * tests/test_lbss.py to traces of the reference's own functions). Every request is
+ * admitted. next() yields the slot's assignment [n] (ssm or -1), the prewarm
+ * destinations [n] (exploration: the chunk's draw; exploitation: the optimistic
+ * argmax decided before the matching), the explore flag and the epoch. observe()
+ * is ArmEstimate::add(observed_goodput) (bandit.cpp:166-169). rows() reads (set=0)
+ * or replaces (set=1) all estimates as [n][m][2] = {sum, count}: the multi-GPU
+ * driver replaces them with the all-gathered rows every slot.
+ * ---------------------------------------------------------------------- */
+typedef struct spin_lbss spin_lbss;
+spin_status spin_lbss_create(int32_t n_requests, int32_t n_ssm, const int32_t* capacities, int32_t alpha,
+                             int32_t beta, uint64_t seed, spin_lbss** out);
+spin_status spin_lbss_destroy(spin_lbss* sel);
+spin_status spin_lbss_next(spin_lbss* sel, int32_t* assignment, int32_t* prewarm, int32_t* explore, int32_t* epoch);
+spin_status spin_lbss_observe(spin_lbss* sel, int32_t request, int32_t ssm, double goodput);
+spin_status spin_lbss_rows(spin_lbss* sel, double* rows, int32_t set);
+/* plan_exploitation on the current estimates (no schedule state change). */
+spin_status spin_lbss_plan(spin_lbss* sel, int32_t* assignment);
+
+/* ------------------------------------------------------------------------
  * Device plumbing: lets callers (and the parity tests) hold device buffers
  * without any framework. spin_device_count reports 0 (status OK) when there is
  * no driver or device. spin_device_alloc zero-fills. kind: 1 H2D, 2 D2H, 3 D2D.

@@ -12,6 +12,11 @@ Cases follow the reference's own tests:
   verify_batch_cost     slot_engine.cpp:24-45
   attention             test_attention.cpp:85-161 (seeds 21, 22/23, 31-33, random 424242)
   acceptance            test_model.cpp:112-142 (p = 0, 0.8, 1; E = 2.3616)
+
+`python oracle/make_golden.py lbss` writes tests/golden/lbss_golden.json: the
+reference selector's assignment / prewarm / explore trace (run_lbss control flow,
+bandit.cpp:248-332, replayed by ref_lbss_trace in oracle/ref_shim.cpp) on seeded
+synthetic goodput tables, binding and non-binding capacities.
 """
 from __future__ import annotations
 
@@ -158,5 +163,44 @@ def main():
     print("wrote", OUT, os.path.getsize(OUT), "bytes")
 
 
+LBSS_OUT = os.path.join(os.path.dirname(OUT), "lbss_golden.json")
+LBSS_CASES = [  # n, caps, alpha, beta, seed, slots
+    (8, [8, 8], 8, 2, 2503, 40),
+    (12, [4, 4, 4], 8, 2, 11, 40),
+    (6, [2, 1, 2], 4, 2, 12, 30),
+    (32, [32, 32, 32], 8, 2, 2503, 50),
+    (20, [5, 20], 6, 3, 99, 45),
+    (10, [3, 3, 3, 3], 4, 4, 7, 36),
+]
+
+
+def lbss_main():
+    lib = load_ref()
+    lib.ref_lbss_trace.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_ulonglong, C.c_int,
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(31337)
+    out = []
+    for n, caps, alpha, beta, seed, slots in LBSS_CASES:
+        m = len(caps)
+        g = np.round(rng.uniform(1.0, 100.0, (n, m)), 3)
+        if n == 32:
+            g[:, 1] = g[:, 0]  # exact ties: lowest ssm id wins
+        a = np.zeros((slots, n), np.int32)
+        pw = np.zeros((slots, n), np.int32)
+        ex = np.zeros(slots, np.int32)
+        caps_a = np.array(caps, np.int32)
+        gg = np.ascontiguousarray(g, dtype=np.float64)
+        st = lib.ref_lbss_trace(n, m, ptr(caps_a), alpha, beta, seed, slots, ptr(gg), ptr(a), ptr(pw), ptr(ex))
+        assert st == 0, st
+        out.append({"n": n, "caps": caps, "alpha": alpha, "beta": beta, "seed": seed, "slots": slots,
+                    "goodput": g.tolist(), "assignment": a.tolist(), "prewarm": pw.tolist(), "explore": ex.tolist()})
+    with open(LBSS_OUT, "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+    print("wrote", LBSS_OUT, os.path.getsize(LBSS_OUT), "bytes")
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "lbss":
+        lbss_main()
+    else:
+        main()

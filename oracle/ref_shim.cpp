@@ -4,10 +4,12 @@
 // the oracle and to generate tests/golden/ fixtures; never shipped or linked
 // by libspin.so. Output goes to oracle/_ref/ (git-ignored).
 #include <cstring>
+#include <numeric>
 #include <exception>
 #include <vector>
 
 #include "specsim/attention.hpp"
+#include "specsim/bandit.hpp"
 #include "specsim/errors.hpp"
 #include "specsim/model.hpp"
 #include "specsim/packing.hpp"
@@ -145,5 +147,50 @@ int ref_sample_accepted_prefix(double p, int window, unsigned long long seed, in
 }
 
 double ref_expected_accepted_prefix(double p, int window) { return expected_accepted_prefix(p, window); }
+
+// Replays run_lbss's control flow (bandit.cpp:248-332) with the reference's own
+// selector functions (draw_exploration_assignment, prewarm_destination,
+// plan_exploitation, exploitation_duration) on a synthetic observation table:
+// at slot t every served request i on ssm j observes
+//   goodput = g[i*m + j] * (1 + 0.05 * ((i + 3*j + t) % 5)).
+// Writes assignment / prewarm [slots][n] and the explore flag per slot.
+int ref_lbss_trace(int n, int m, const int* caps, int alpha, int beta, unsigned long long seed, int slots,
+                   const double* g, int* assign_out, int* prewarm_out, int* explore_out) {
+  return run([&] {
+    BanditConfig cfg;
+    cfg.alpha = alpha;
+    cfg.beta = beta;
+    cfg.max_slots = slots;
+    validate(cfg);
+    std::vector<SsmProfile> ssms(m);
+    for (int j = 0; j < m; ++j) ssms[j].id = j, ssms[j].batch_capacity = caps[j];
+    std::vector<int> admitted(n);
+    std::iota(admitted.begin(), admitted.end(), 0);
+    BanditState st = BanditState::make(n, m);
+    Rng rng(mix_seed(seed, kStreamPolicy));
+    int t = 0;
+    auto emit_observe = [&](const std::vector<int>& a, const std::vector<int>& pw, int explore) {
+      std::memcpy(assign_out + static_cast<size_t>(t) * n, a.data(), sizeof(int) * n);
+      std::memcpy(prewarm_out + static_cast<size_t>(t) * n, pw.data(), sizeof(int) * n);
+      explore_out[t] = explore;
+      for (int i = 0; i < n; ++i)
+        if (a[i] >= 0) st.estimates[i][a[i]].add(g[i * m + a[i]] * (1.0 + 0.05 * ((i + 3 * a[i] + t) % 5)));
+      ++t;
+    };
+    while (t < slots) {
+      for (int chunk = 0; chunk < alpha / beta && t < slots; ++chunk) {
+        std::vector<int> a = draw_exploration_assignment(admitted, ssms, n, rng);
+        st.prewarmed = a;
+        for (int s = 0; s < beta && t < slots; ++s) emit_observe(a, st.prewarmed, 1);
+      }
+      if (t >= slots) break;
+      st.prewarmed = prewarm_destination(st, admitted);
+      const std::vector<int> plan = plan_exploitation(st, admitted, ssms);
+      const long long dur = exploitation_duration(st.epoch, slots - t);
+      for (long long s = 0; s < dur; ++s) emit_observe(plan, st.prewarmed, 0);
+      ++st.epoch;
+    }
+  });
+}
 
 }  // extern "C"

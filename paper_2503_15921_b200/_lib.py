@@ -130,6 +130,19 @@ _SIGNATURES = {
     "spin_pack_device": [P_I32, C.c_int32, C.c_int32, P_I32, P_I32, C.POINTER(Segment), C.c_int32, P_I32, P_I64,
                          P_I32],
     "spin_device_count": [P_I32],
+    "spin_comm_unique_id": [C.c_int32, C.c_void_p],
+    "spin_comm_create": [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)],
+    "spin_comm_destroy": [C.c_void_p],
+    "spin_comm_info": [C.c_void_p, P_I32, P_I32, P_I32],
+    "spin_stats_allgather": [C.c_void_p, P_F64, P_F64, C.c_int32, C.c_int32],
+    "spin_comm_allreduce": [C.c_void_p, P_F64, C.c_int32, C.c_int32],
+    "spin_comm_barrier": [C.c_void_p],
+    "spin_lbss_create": [C.c_int32, C.c_int32, P_I32, C.c_int32, C.c_int32, C.c_uint64, C.POINTER(C.c_void_p)],
+    "spin_lbss_destroy": [C.c_void_p],
+    "spin_lbss_next": [C.c_void_p, P_I32, P_I32, P_I32, P_I32],
+    "spin_lbss_observe": [C.c_void_p, C.c_int32, C.c_int32, C.c_double],
+    "spin_lbss_rows": [C.c_void_p, P_F64, C.c_int32],
+    "spin_lbss_plan": [C.c_void_p, P_I32],
     "spin_device_alloc": [C.c_int32, C.c_size_t, C.POINTER(C.c_void_p)],
     "spin_device_free": [C.c_void_p],
     "spin_memcpy": [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32],
