@@ -9,12 +9,20 @@ synthetic random-init weights with a planted next-token map.
          rounds back to back on the device, CUDA-event timed, max over ranks.
   e2e    the same metric through the public per-slot C-ABI call spin_round
          (host buffers; H2D of the assignment and D2H of the outcome inside
-         every step) plus the per-step NCCL all-gather of per-(request, SSM)
-         acceptance statistics at N > 1; wall-clock timed, max over ranks.
+         every step) plus, at N > 1, the per-step all-gather of per-(request, SSM)
+         acceptance statistics (spin_stats_allgather over NCCL); wall-clock
+         timed, max over ranks.
+
+Multi-GPU: one process per GPU. Under torchrun the ranks come from the
+environment; `python bench.py --gpus N` without WORLD_SIZE spawns the N ranks
+itself. Collectives go through libspin's communicator (NCCL); torch only hands rank
+0's NCCL id to the other ranks when torchrun launched them.
 
 `--impl reference` times the CPU implementation of the same path on the host
-cores (the oracle port; the reference itself only simulates this path) on a
-bounded sample of the workload and prints the same JSON line.
+cores (the oracle port of the reference's semantics: the reference itself only
+simulates this path) on a bounded sample of the workload, and the reference's
+own single-threaded hot-path functions (pack, verify_batch_cost,
+decomposed_attention, SlotEngine::run_slot), and prints the same JSON line.
 """
 from __future__ import annotations
 
@@ -115,39 +123,125 @@ def path_roofline_us(target, committed, window, hbm_gbs, tflops):
     return max(t_hbm, t_tc), bytes_, flops
 
 
-def cpu_sample(steps: int, warm: int = 1):
-    """Oracle port on the host cores: config-2 round on a bounded sample.
+# ---------------------------------------------------------------- ranks and collectives
+class Ranks:
+    """rank / world / local device, and libspin's communicator (NCCL) for N > 1."""
 
-    Sample: 4 of the 32 requests (same prompt distribution), full-depth SSMs,
-    the 7B-shaped target with 1 of its 32 layers instantiated; the round time
-    is extrapolated as draft + 32 x (one verify layer) + lm_head. The CPU
-    verify is FLOP-bound, so tokens/s does not depend on the batch sampled.
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.comm = None
+        if self.world > 1:
+            from paper_2503_15921_b200 import dist
+
+            uid = os.environ.get("SPIN_COMM_ID")
+            if uid is None:  # launched by torchrun: rank 0's NCCL id travels over torch's CPU store
+                import torch.distributed as tdist
+
+                tdist.init_process_group("gloo")
+                obj = [dist.unique_id(dist.NCCL).hex() if self.rank == 0 else None]
+                tdist.broadcast_object_list(obj, src=0)
+                uid = obj[0]
+                tdist.destroy_process_group()
+            self.comm = dist.Comm(dist.NCCL, self.rank, self.world, bytes.fromhex(uid), self.local)
+
+    def barrier(self):
+        if self.comm is not None:
+            self.comm.barrier()
+
+    def max(self, x):
+        return self.comm.max(x) if self.comm is not None else x
+
+    def sum(self, x):
+        return self.comm.sum(x) if self.comm is not None else x
+
+    def close(self):
+        if self.comm is not None:
+            self.comm.close()
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without WORLD_SIZE: one process per GPU, NCCL id from here."""
+    from paper_2503_15921_b200 import dist
+
+    uid = dist.unique_id(dist.NCCL).hex()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(n), LOCAL_RANK=str(r), LOCAL_WORLD_SIZE=str(n),
+                   SPIN_COMM_ID=uid, MASTER_ADDR="127.0.0.1")
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    return max(p.wait() for p in procs)
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle port)
+def cpu_sample(steps: int, warm: int = 1, bs: int = 4):
+    """Oracle port on the host cores: config-2 rounds on a bounded sample, no extrapolation.
+
+    Sample: the first `bs` of the 32 requests with their real config-2 context lengths
+    (the KV caches of target and SSMs filled with seeded values instead of running
+    the prefill forward -- a verify over a context costs the same either way), the
+    full 32-layer 7B-shaped target and full-depth SSMs, greedy rounds exactly as the
+    GPU path runs them. Accepted tokens / wall seconds of the rounds.
     """
     from oracle import OracleEngine
     from paper_2503_15921_b200.models import LLAMA_7B, LLAMA_68M, LLAMA_160M, synthetic_prompts
 
-    bs = 4
-    tgt = dataclasses.replace(LLAMA_7B, n_layers=1)
     prompts = synthetic_prompts(BATCH, PROMPT_LO, PROMPT_HI, LLAMA_7B.vocab, SEED)[:bs]
-    eng = OracleEngine(tgt, (LLAMA_68M, LLAMA_160M), max_requests=bs, max_ctx=PROMPT_HI + 8 * (steps + warm + 2),
-                       window=WINDOW, threads=0)
-    eng.prefill(range(bs), prompts)
+    lens = np.array([len(p) for p in prompts], np.int32)
+    eng = OracleEngine(LLAMA_7B, (LLAMA_68M, LLAMA_160M), max_requests=bs,
+                       max_ctx=PROMPT_HI + (WINDOW + 1) * (steps + warm + 2) + 8, window=WINDOW, threads=0)
     slots = np.arange(bs, dtype=np.int32)
+    eng.fake_context(slots, lens, SEED)
     assign = np.array([i % 2 for i in range(bs)], np.int32)
     times, toks = [], []
     for i in range(warm + steps):
+        t0 = time.perf_counter()
         out = eng.round(slots, assign)
-        d, vb, vh = eng.last_timing()
+        dt = time.perf_counter() - t0
         if i >= warm:
-            times.append(d + LLAMA_7B.n_layers * vb + vh)
+            times.append(dt)
             toks.append(int(out["accepted"].sum()) + bs)
     eng.close()
     value = sum(toks) / sum(times)
     return {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": (f"oracle port (C, OpenMP, {os.cpu_count()} threads): {steps} config-2 rounds on 4 of 32 "
-                       "requests, SSMs full depth, target block time measured on 1 of 32 layers and scaled x32, "
-                       "lm_head full"),
-            "s_per_round": sum(times) / len(times), "accepted_per_round": sum(toks) / len(toks)}
+            "sample": (f"oracle port (C, OpenMP, {os.cpu_count()} threads): {steps} full config-2 rounds (SSM drafts, "
+                       f"32-layer 7B-shaped verify, accept) on {bs} of the 32 requests at their config-2 context "
+                       "lengths; KV filled with seeded values instead of a prefill forward; no extrapolation"),
+            "s_per_round": sum(times) / len(times), "accepted_per_round": sum(toks) / len(toks),
+            "requests_sampled": bs}
+
+
+def reference_functions():
+    """The reference's own single-threaded hot-path functions (oracle/_ref, built from
+    /root/reference sources) on the config-2 shapes: BASELINE.md section 4 row 1."""
+    import ctypes as C
+
+    from oracle import REF_SO
+
+    if not os.path.exists(REF_SO):
+        return {"unavailable": "oracle/_ref/libspecsim_ref.so not built (needs /root/reference at build time)"}
+    lib = C.CDLL(REF_SO)
+    for f in ("ref_time_pack", "ref_time_verify_batch_cost", "ref_time_decomposed_attention", "ref_time_run_slot"):
+        getattr(lib, f).restype = C.c_double
+    from paper_2503_15921_b200.models import LLAMA_7B, synthetic_prompts
+
+    prompts = synthetic_prompts(BATCH, PROMPT_LO, PROMPT_HI, LLAMA_7B.vocab, SEED)
+    kv = np.array([len(p) + WINDOW for p in prompts], np.int32)  # Request::kv_len (model.hpp:26-28)
+    p = kv.ctypes.data_as(C.c_void_p)
+    head = lib.ref_time_decomposed_attention(p, BATCH, WINDOW + 1, LLAMA_7B.head_dim, BATCH, C.c_int(2))
+    heads = LLAMA_7B.n_heads * LLAMA_7B.n_layers
+    return {"cores": 1, "kind": "reference", "batch": BATCH, "window": WINDOW,
+            "pack_us": lib.ref_time_pack(p, BATCH, BATCH, 2000) * 1e6,
+            "verify_batch_cost_us": lib.ref_time_verify_batch_cost(p, BATCH, WINDOW, 1, BATCH, 2000) * 1e6,
+            "decomposed_attention_ms_per_head": head * 1e3,
+            "decomposed_attention_s_per_verify_step": head * heads,
+            "decomposed_attention_note": (f"measured on one head (d={LLAMA_7B.head_dim}, {WINDOW + 1} queries per "
+                                          f"request, config-2 kv lengths); a 7B verify step runs {heads} "
+                                          "head-layers, so the per-step figure is that product"),
+            "run_slot_us": lib.ref_time_run_slot(BATCH, PROMPT_LO, PROMPT_HI, WINDOW, 500) * 1e6,
+            "run_slot_note": "cost-model simulation of one slot (32 requests, 2 SSMs, packing on)"}
 
 
 def run_reference(args):
@@ -161,9 +255,33 @@ def run_reference(args):
             "impl": "reference", "config": workload_config(None),
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_functions": reference_functions(),
             "note": ("the reference (specsim) only simulates this path with cost models; its CPU implementation "
-                     "of the real computation is the oracle port of its semantics")}
+                     "of the real computation is the oracle port of its semantics (value); the reference's own "
+                     "single-threaded hot-path functions are timed in reference_functions")}
     print(json.dumps(line), flush=True)
+
+
+def parity_spot_check():
+    """c2-shaped GPU-vs-oracle rounds (7B target, 68M/160M SSMs, 4 requests, short
+    prompts, 2 rounds): the bit-exactness contract of tests/_parity.py, summarised."""
+    sys.path.insert(0, ROOT)
+    from paper_2503_15921_b200.models import LLAMA_7B, LLAMA_68M, LLAMA_160M
+    from tests._parity import ParityRun
+
+    run = ParityRun(LLAMA_7B, (LLAMA_68M, LLAMA_160M), batch=4, prompt_lo=16, prompt_hi=40, seed=7002, window=WINDOW,
+                    max_ctx=96, device=int(os.environ.get("LOCAL_RANK", "0")))
+    for _ in range(2):
+        run.round(np.array([0, 1, 0, 1], np.int32))
+    try:
+        st = run.check()
+        ok = True
+    except AssertionError:
+        st, ok = run.stats, False
+    run.close()
+    return {"workload": "c2 shapes, 4 requests, prompts U[16,40], 2 rounds", "bit_exact": ok,
+            "decisions": st["decisions"], "forced_near_ties": st["forced"], "max_forced_deficit": st["deficit"],
+            "twin_floor": st["floor"], "logits_rel_error_fro": st["worst_rel_fro"]}
 
 
 def run_c3(args):
@@ -173,12 +291,10 @@ def run_c3(args):
     reference's verify_batch_cost token accounting (slot_engine.cpp:24-45) for the same batch."""
     import ctypes as C
 
-    import torch
-
     from paper_2503_15921_b200 import _lib
     from paper_2503_15921_b200.models import LLAMA_7B, LLAMA_68M, Engine, synthetic_prompts
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
     B, W = 64, 16
     rng = np.random.default_rng(SEED + 3)
     prompts = synthetic_prompts(B, PROMPT_LO, PROMPT_HI, LLAMA_7B.vocab, SEED + 3)
@@ -191,7 +307,7 @@ def run_c3(args):
     lib = _lib.load()
     kv_lens = np.array([len(p) + int(l) for p, l in zip(prompts, lens)], np.int32)  # kv_len = committed + window
     for width in (B, B // 2, B // 4):
-        eng = Engine(LLAMA_7B, (LLAMA_68M,), max_requests=B, max_ctx=max_ctx, window=W, pack_width=width)
+        eng = Engine(LLAMA_7B, (LLAMA_68M,), max_requests=B, max_ctx=max_ctx, window=W, pack_width=width, device=dev)
         eng.prefill(range(B), prompts)
         slots = np.arange(B, dtype=np.int32)
         res = {}
@@ -218,74 +334,121 @@ def run_c3(args):
     print(json.dumps(out), flush=True)
 
 
+def serve(eng, sel, n_total, n_ssm, local_slots, slots_to_run, comm=None, prewarm=True):
+    """spin_lbss_serve: the native multi-GPU LBSS loop (csrc/serve.cpp) on this rank."""
+    import ctypes as C
+
+    from paper_2503_15921_b200 import _lib
+
+    rep = _lib.ServeReport()
+    final = np.zeros(n_total, np.int32)
+    ls = np.ascontiguousarray(local_slots, dtype=np.int32)
+    _lib.check(eng.lib.spin_lbss_serve(eng.ctx, comm.h if comm is not None else None, sel.h, n_total, n_ssm,
+                                       ls.ctypes.data_as(_lib.P_I32), len(ls), slots_to_run, int(prewarm),
+                                       C.byref(rep), final.ctypes.data_as(_lib.P_I32)))
+    return {k: getattr(rep, k) for k, _ in rep._fields_}, final
+
+
 def run_c4(args):
     """BASELINE config 4: LLaMA-13B-shaped target, 3 heterogeneous SSMs (68M, 160M, 160M-b) with
-    LBSS selection on measured goodput (selector.Lbss restating bandit.cpp), the SSM drafts of a
-    slot running concurrently on their own CUDA streams. Reports accepted tokens/s of the LBSS run
-    and of every homogeneous assignment (all requests on one SSM) on the same prompts."""
-    import torch
-
+    LBSS selection on measured goodput -- the native loop spin_lbss_serve (C++ selector, per-SSM
+    wall times, switch catch-up charged, next-slot destinations prewarmed on idle streams) -- the
+    SSM drafts of a slot running concurrently on their own CUDA streams. Every policy starts from
+    the same freshly prefilled state and runs the same number of slots: LBSS with and without
+    prewarm, and every homogeneous assignment (all requests on one SSM)."""
     from paper_2503_15921_b200.models import LLAMA_13B, LLAMA_68M, LLAMA_160M, LLAMA_160M_B, Engine, synthetic_prompts
     from paper_2503_15921_b200.selector import Lbss
-    from paper_2503_15921_b200.trace import RoundTrace
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
     ssms = (LLAMA_68M, LLAMA_160M, LLAMA_160M_B)
-    slots_n = max(args.steps, 24)
-    rounds_cap = slots_n + 3 * 6 + 8
-    max_ctx = ((PROMPT_HI + (WINDOW + 1) * rounds_cap + 8 + 63) // 64) * 64
+    slots_n = max(args.steps, 128)
+    max_ctx = ((PROMPT_HI + (WINDOW + 1) * (slots_n + 4) + 8 + 63) // 64) * 64
     prompts = synthetic_prompts(BATCH, PROMPT_LO, PROMPT_HI, LLAMA_13B.vocab, SEED + 4)
     slots = np.arange(BATCH, dtype=np.int32)
     out = {"metric": "accepted tokens/sec (c4: 13B target, 3 SSMs, LBSS)", "unit": "tokens/s",
            "higher_is_better": True, "config": {"workload": "c4", "target": LLAMA_13B.name,
                                                 "ssms": [s.name for s in ssms], "batch": BATCH, "window": WINDOW,
-                                                "slots": slots_n, "alpha": 8, "beta": 2}}
-    eng = Engine(LLAMA_13B, ssms, max_requests=BATCH, max_ctx=max_ctx, window=WINDOW)
-    eng.prefill(range(BATCH), prompts)
-    # homogeneous baselines (vanilla: every request on SSM j), 6 slots each after 2 warm-up slots
+                                                "slots_per_policy": slots_n, "alpha": 8, "beta": 2}}
+    eng = Engine(LLAMA_13B, ssms, max_requests=BATCH, max_ctx=max_ctx, window=WINDOW, device=dev)
     homo = {}
-    for j, s in enumerate(ssms):
+    for j, s in enumerate(ssms):  # vanilla: every request on SSM j
+        eng.prefill(range(BATCH), prompts)
         assign = np.full(BATCH, j, np.int32)
-        for _ in range(2):
-            eng.round(slots, assign)
-        toks, ms = 0, 0.0
-        for _ in range(6):
+        toks, ms, t0 = 0, 0.0, time.perf_counter()
+        for _ in range(slots_n):
             r = eng.round(slots, assign)
             toks += int(r["accepted"].sum()) + BATCH
             ms += r["round_ms"]
-        homo[s.name] = {"tokens_per_s": toks / (ms / 1e3), "mean_accepted": toks / (6 * BATCH) - 1}
-    # LBSS on measured goodput
-    sel = Lbss(BATCH, [BATCH] * len(ssms), alpha=8, beta=2, seed=SEED)
-    trace = RoundTrace()  # the LBSS run's event trace in the reference schema (trace_io.cpp)
-    toks, ms, wall0 = 0, 0.0, time.perf_counter()
-    explore_slots = 0
-    for _ in range(slots_n):
-        assign, explore = sel.next_slot()
-        assign = assign.astype(np.int32)
-        r = eng.round(slots, assign)
-        trace.record(eng, assign, r)
-        sec = r["round_ms"] / 1e3
-        for i in range(BATCH):
-            if assign[i] >= 0:
-                sel.add(i, int(assign[i]), (int(r["accepted"][i]) + 1) / sec)
-        toks += int(r["accepted"].sum()) + int((assign >= 0).sum())
-        ms += r["round_ms"]
-        explore_slots += int(explore)
-    wall = time.perf_counter() - wall0
-    final = sel.exploitation()
-    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "c4_trace.csv"), "w") as f:
-        f.write(trace.csv())
+        homo[s.name] = {"tokens_per_s_device": toks / (ms / 1e3),
+                        "tokens_per_s_wall": toks / (time.perf_counter() - t0),
+                        "mean_accepted": toks / (slots_n * BATCH) - 1}
+    runs = {}
+    for prewarm in (True, False):
+        eng.prefill(range(BATCH), prompts)
+        sel = Lbss(BATCH, [BATCH] * len(ssms), alpha=8, beta=2, seed=SEED)
+        rep, final = serve(eng, sel, BATCH, len(ssms), slots, slots_n, prewarm=prewarm)
+        sel.close()
+        runs["prewarm" if prewarm else "no_prewarm"] = {
+            "tokens_per_s_device": rep["tokens"] / (rep["device_ms"] / 1e3),
+            "tokens_per_s_wall": rep["tokens"] / (rep["wall_ms"] / 1e3), "switch_ms": rep["switch_ms"],
+            "switch_tokens": rep["switch_tokens"], "explore_slots": rep["explore_slots"], "epochs": rep["epochs"],
+            "final_plan_histogram": np.bincount(final[final >= 0], minlength=len(ssms)).tolist()}
     eng.close()
-    out["value"] = toks / (ms / 1e3)
-    out["lbss"] = {"tokens_per_s_device": toks / (ms / 1e3), "tokens_per_s_wall": toks / wall,
-                   "explore_slots": explore_slots, "epochs": sel.epoch,
-                   "llm_busy_sec": trace.llm_busy, "llm_idle_sec": trace.llm_idle,
-                   "final_assignment_histogram": np.bincount(final, minlength=len(ssms)).tolist()}
+    best = max(homo, key=lambda k: homo[k]["tokens_per_s_device"])
+    out["value"] = runs["prewarm"]["tokens_per_s_device"]
+    out["lbss"] = runs
     out["homogeneous"] = homo
-    out["note"] = ("wall time includes host-side SSM switches (KV recompute on the destination SSM, "
-                   "switching_cost slot_engine.cpp:12-22) and the selector")
+    out["lbss_over_best_homogeneous"] = {"best": best, "device": out["value"] / homo[best]["tokens_per_s_device"],
+                                         "wall": runs["prewarm"]["tokens_per_s_wall"] / homo[best]["tokens_per_s_wall"]}
+    out["note"] = ("device time of every slot includes the synchronous KV catch-up of switched requests "
+                   "(switching_cost, slot_engine.cpp:12-22); wall time adds the host selector and launch overheads")
     print(json.dumps(out), flush=True)
+
+
+def run_c5(args, ranks):
+    """BASELINE config 5: 256 requests sharded over the ranks (strong scaling), replicated weights,
+    the native LBSS loop on every rank with the per-slot NCCL all-gather of ArmEstimate rows
+    (spin_stats_allgather). value = all tokens / max over ranks of the device time."""
+    from paper_2503_15921_b200.dist import shard
+    from paper_2503_15921_b200.models import LLAMA_7B, LLAMA_68M, LLAMA_160M, Engine, synthetic_prompts
+    from paper_2503_15921_b200.selector import Lbss
+
+    N = 256
+    ssms = (LLAMA_68M, LLAMA_160M)
+    mine = shard(N, ranks.world, ranks.rank)
+    n_local = len(mine)
+    slots_n = args.steps + args.warmup
+    max_ctx = ((PROMPT_HI + (WINDOW + 1) * (slots_n + 4) + 8 + 63) // 64) * 64
+    prompts = synthetic_prompts(N, PROMPT_LO, PROMPT_HI, LLAMA_7B.vocab, SEED + 5)
+    eng = Engine(LLAMA_7B, ssms, max_requests=n_local, max_ctx=max_ctx, window=WINDOW, device=ranks.local)
+    eng.prefill(range(n_local), [prompts[i] for i in mine])
+    slots = np.arange(n_local, dtype=np.int32)
+    sel = Lbss(N, [N] * len(ssms), alpha=8, beta=2, seed=SEED)
+    # warm-up slots (graph capture per assignment shape), then the timed slots
+    serve(eng, sel, N, len(ssms), slots, args.warmup, ranks.comm)
+    ranks.barrier()
+    with ClockSampler(ranks.local) as clk:
+        rep, final = serve(eng, sel, N, len(ssms), slots, args.steps, ranks.comm)
+        ranks.barrier()
+    dev_ms = ranks.max(rep["device_ms"])
+    wall_ms = ranks.max(rep["wall_ms"])
+    tokens = ranks.sum(float(rep["tokens"]))
+    eng.close()
+    sel.close()
+    line = {"metric": "accepted tokens/sec (c5: batch 256 sharded, LBSS with NCCL stats all-gather)",
+            "value": tokens / (dev_ms / 1e3), "unit": UNIT, "n_gpus": ranks.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "c5: 256 requests sharded over the ranks, LLaMA-7B-shaped target, "
+                                   "LLaMA-68M/160M-shaped SSMs, LBSS (alpha 8, beta 2) on every rank",
+                       "requests_per_gpu": n_local, "parallelism": f"request-sharded dp{ranks.world}"},
+            "e2e": {"value": tokens / (wall_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * 3 * n_local,
+                    "d2h_bytes_per_step": 4 * n_local * (3 + 2 * WINDOW + 1)},
+            "lbss": {"explore_slots": rep["explore_slots"], "epochs": rep["epochs"], "switch_ms": rep["switch_ms"],
+                     "final_plan_histogram": np.bincount(final[final >= 0], minlength=len(ssms)).tolist()},
+            "clocks": clk.summary()}
+    if ranks.rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 def workload_config(eng_info):
@@ -295,12 +458,36 @@ def workload_config(eng_info):
            "batch_per_gpu": BATCH, "window": WINDOW, "prompt_len": f"U[{PROMPT_LO},{PROMPT_HI}]",
            "target": LLAMA_7B.name, "ssms": [LLAMA_68M.name, LLAMA_160M.name], "assignment": "request i -> ssm i%2",
            "l2": "no flush needed: 13.5 GB of target weights stream through the 126 MB L2 every step"}
-    if BATCH != 32:
-        cfg["workload"] = (f"c5: batch 256 sharded, {BATCH} requests per GPU; LLaMA-7B-shaped target verifying "
-                           "LLaMA-68M/160M-shaped SSM drafts, greedy")
     if eng_info:
         cfg.update(eng_info)
     return cfg
+
+
+def gemm_roofline(eng, target, T, hbm, tflops, peak_src):
+    """Dominant kernel class: the target's projection GEMMs, replayed in situ (spin_kernel_bench).
+    HBM-bound below the ridge (T < ~250 rows), tensor-bound above it."""
+    g_us, g_bytes = eng.kernel_bench("gemm", 5)
+    D, F, L = target.d_model, target.ffn, target.n_layers
+    g_flops = 2.0 * T * L * (4 * D * D + 3 * D * F) / (4 * L)  # per launch (4 GEMMs per layer)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gemm_dram_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get("bytes_per_launch_target_gemm")
+        except Exception:
+            traffic = None
+    tensor = g_flops / g_bytes > hbm * 1e9 / (tflops * 1e12)  # arithmetic intensity above the ridge
+    if tensor:
+        achieved = g_flops / (g_us * 1e-6) / 1e12
+        return {"bound": "tensor", "kernel": "tcgen05 weight-streaming GEMM (target projections)",
+                "achieved": achieved, "peak": tflops, "unit": "TFLOP/s", "frac": achieved / tflops,
+                "traffic": None, "peak_source": peak_src, "alg_flops_per_launch": g_flops,
+                "alg_bytes_per_launch": g_bytes, "us_per_launch": g_us}
+    achieved = g_bytes / (g_us * 1e-6) / 1e9
+    return {"bound": "hbm", "kernel": "tcgen05 weight-streaming GEMM (target projections)", "achieved": achieved,
+            "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
+            "alg_bytes_per_launch": g_bytes, "us_per_launch": g_us}
 
 
 def main():
@@ -310,39 +497,33 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="spin", choices=["spin", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--pack-width", type=int, default=0)
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    if args.config == "c3" and args.impl != "reference":
-        run_c3(args)
-        return
-    if args.config == "c4" and args.impl != "reference":
-        run_c4(args)
-        return
-    global BATCH
-    if args.config == "c5":  # batch 256 requests sharded over the ranks (strong scaling)
-        BATCH = 256 // int(os.environ.get("WORLD_SIZE", "1"))
-        args.no_cpu_baseline = True
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.config == "c3":
+        run_c3(args)
+        return
+    if args.config == "c4":
+        run_c4(args)
+        return
+    ranks = Ranks()
+    if args.config == "c5":
+        run_c5(args, ranks)
+        ranks.close()
+        return
 
-    import torch
-
+    from paper_2503_15921_b200.dist import AcceptanceStats
     from paper_2503_15921_b200.models import LLAMA_7B, LLAMA_68M, LLAMA_160M, Engine, synthetic_prompts
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world, rank, local = ranks.world, ranks.rank, ranks.local
     hbm, tflops, peak_src = peaks()
-
     rounds_total = 2 * (args.warmup + args.steps) + 4
     max_ctx = ((PROMPT_HI + (WINDOW + 1) * rounds_total + 8 + 63) // 64) * 64
     eng = Engine(LLAMA_7B, (LLAMA_68M, LLAMA_160M), max_requests=BATCH, max_ctx=max_ctx, window=WINDOW, device=local,
@@ -351,79 +532,51 @@ def main():
     eng.prefill(range(BATCH), prompts)
     slots = np.arange(BATCH, dtype=np.int32)
     assign = np.array([i % 2 for i in range(BATCH)], np.int32)
-
-    def barrier():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def gmax(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return t.item()
-
-    def gsum(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t)
-        return t.item()
-
     # per-(request, SSM) acceptance statistics, ArmEstimate{sum,count} (bandit.hpp:24-39),
-    # all-gathered over NCCL every step (the only collective of the path)
-    from paper_2503_15921_b200.dist import AcceptanceStats
-
-    stats = AcceptanceStats(BATCH * world, 2, world, rank, device="cuda")
+    # all-gathered every e2e step through libspin (the only collective of the path)
+    stats = AcceptanceStats(BATCH * world, 2, world, rank)
 
     # ---- warm-up (graph capture, clocks, caches)
     for _ in range(args.warmup):
         eng.round(slots, assign)
     with ClockSampler(local) as clk:
         # ---- value: device-resident rounds
-        barrier()
+        ranks.barrier()
         emitted, dev_ms = eng.run_rounds(slots, assign, args.steps)
-        barrier()
-        dev_ms_max = gmax(dev_ms)
-        tokens_total = gsum(float(emitted.sum()))
+        ranks.barrier()
+        dev_ms_max = ranks.max(dev_ms)
+        tokens_total = ranks.sum(float(emitted.sum()))
         value = tokens_total / (dev_ms_max / 1e3)
         # ---- e2e: public per-slot call with host buffers + per-step stats gather
         verify_us, draft_us, committed = [], [], None
-        barrier()
+        ranks.barrier()
         t0 = time.perf_counter()
         e2e_tokens = 0
         for _ in range(args.steps):
             out = eng.round(slots, assign)
             e2e_tokens += int(out["accepted"].sum()) + BATCH
-            wall = out["round_ms"] / 1e3
-            stats.add_many(np.arange(BATCH), assign, (out["accepted"] + 1) / wall)
-            stats.gather(dist)
+            stats.add_many(np.arange(BATCH), assign, (out["accepted"] + 1) / (out["wall_ms"] / 1e3))
+            stats.gather(ranks.comm)
             verify_us.append(out["verify_ms"] * 1e3)
             draft_us.append(out["draft_ms"] * 1e3)
             committed = out["committed"]
-        barrier()
-        e2e_s = gmax(time.perf_counter() - t0)
-        e2e_value = gsum(float(e2e_tokens)) / e2e_s
+        ranks.barrier()
+        e2e_s = ranks.max(time.perf_counter() - t0)
+        e2e_value = ranks.sum(float(e2e_tokens)) / e2e_s
     clocks = clk.summary()
     launches = eng.launches_per_round(slots, assign)
     # ---- per-kernel-class device time of one (un-graphed) round
     prof = eng.profile(slots, assign)
     eng.round(slots, assign)  # graph round: leaves the target's verify state for the in-situ replays
-    g_us, g_bytes = eng.kernel_bench("gemm", 5)
+    T = BATCH * (WINDOW + 1)
+    roof = gemm_roofline(eng, LLAMA_7B, T, hbm, tflops, peak_src)
     a_us, a_bytes = eng.kernel_bench("attention", 5)
-    achieved = g_bytes / (g_us * 1e-6) / 1e9
     a_achieved = a_bytes / (a_us * 1e-6) / 1e9
-    g_n = 4 * LLAMA_7B.n_layers
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "gemm_dram_traffic.json")
-    if os.path.exists(tp):
-        try:
-            with open(tp) as f:
-                traffic = json.load(f).get("bytes_per_launch_target_gemm")
-        except Exception:
-            traffic = None
+    roof["method"] = ("the 128 projection GEMMs (4 per layer) of the last verify replayed as one CUDA graph with "
+                      "PDL, CUDA events on the launch stream, 5 replays")
+    roof["attention"] = {"achieved": a_achieved, "frac": a_achieved / hbm, "us_per_launch": a_us,
+                         "alg_bytes_per_launch": a_bytes, "bound": "hbm",
+                         "kernel": "packed ragged causal attention + shared-max combine"}
     t_roof_us, alg_bytes, alg_flops = path_roofline_us(LLAMA_7B, committed - 0, WINDOW, hbm, tflops)
     verify_med = statistics.median(verify_us)
     round_ms = dev_ms_max / args.steps
@@ -437,31 +590,20 @@ def main():
             "mean_accepted_per_request": mean_acc, "per_class_ms_one_round": {k: v[0] for k, v in prof.items()},
             "per_class_launches": {k: v[2] for k, v in prof.items()}}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round_ms, "higher_is_better": True,
-            "scaling": "strong" if args.config == "c5" else "weak",
+            "warmup": args.warmup, "ms_per_step": round_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded random-init weights, planted bigram)",
             "config": workload_config(info),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": int(launches) * args.steps,
-            "roofline": {"bound": "hbm", "kernel": "tcgen05 weight-streaming GEMM (target projections)",
-                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm if achieved else None, "traffic": traffic,
-                         "peak_source": peak_src,
-                         "alg_bytes_per_launch": g_bytes, "us_per_launch": g_us,
-                         "method": ("the 128 projection GEMMs (4 per layer) of the last verify replayed as one "
-                                    "CUDA graph with PDL, CUDA events on the launch stream, 5 replays"),
-                         "attention": {"achieved": a_achieved, "frac": a_achieved / hbm, "us_per_launch": a_us,
-                                       "alg_bytes_per_launch": a_bytes, "bound": "hbm",
-                                       "kernel": "packed ragged causal attention + shared-max combine"}},
-            "clocks": clocks}
+            "gpu_launches": int(launches) * args.steps, "roofline": roof, "clocks": clocks}
+    eng.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_sample(2, 1)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        if not args.no_parity:
+            line["parity"] = parity_spot_check()
     if rank == 0:
         print(json.dumps(line), flush=True)
-    eng.close()
-    if dist is not None:
-        dist.destroy_process_group()
+    ranks.close()
 
 
 if __name__ == "__main__":

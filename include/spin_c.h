@@ -28,7 +28,8 @@
 extern "C" {
 #endif
 
-#define SPIN_ABI_VERSION 1
+#define SPIN_ABI_VERSION 2
+#define SPIN_MAX_SSM 8
 
 typedef enum spin_status {
   SPIN_OK = 0,
@@ -144,7 +145,13 @@ typedef struct spin_round_out {
   int32_t* target_tokens; /* [n*(window+1)] target argmax rows or NULL  */
   float draft_ms;         /* device time: all SSM draft loops           */
   float verify_ms;        /* device time: pack + verify forward + accept */
-  float round_ms;         /* device time: whole round                   */
+  float round_ms;         /* device time: whole round, switch catch-up included */
+  float switch_ms;        /* device time of the synchronous KV catch-up of requests whose SSM
+                             cache lags (switches, switching_cost slot_engine.cpp:12-22); 0 if none */
+  int32_t switch_tokens;  /* KV positions recomputed by that catch-up */
+  float spec_end_ms[SPIN_MAX_SSM]; /* per SSM: draft end, ms after the draft start (-1: idle); the
+                             request's wall time is spec_end_ms[ssm] + verify_ms (slot_engine.cpp:145) */
+  int32_t* switch_tokens_per_request; /* [n] or NULL: positions recomputed per request */
 } spin_round_out;
 
 /* One speculation + verification slot for n admitted requests. ssm_of[i] is
@@ -152,6 +159,13 @@ typedef struct spin_round_out {
  * buffers; H2D of the assignment and D2H of the outcome are inside the call. */
 spin_status spin_round(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
                        spin_round_out* out);
+/* spin_round plus prewarm (run_slot's `prewarm`, slot_engine.hpp:50-88): prewarm[i]
+ * (or -1) names the SSM request i is expected to move to; its KV is recomputed up
+ * to the committed prefix on that SSM's idle stream WHILE this round runs
+ * (prewarm_destination, bandit.cpp:122-139), so the later switch only catches up
+ * the last round's commits. Later calls order themselves after it on the device. */
+spin_status spin_round_prewarm(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
+                               const int32_t* prewarm, spin_round_out* out);
 
 /* Device-resident loop: one host-driven spin_round first (validation, SSM
  * switches, graph capture; its outcome is not reported), then `rounds` rounds
@@ -269,6 +283,31 @@ spin_status spin_lbss_observe(spin_lbss* sel, int32_t request, int32_t ssm, doub
 spin_status spin_lbss_rows(spin_lbss* sel, double* rows, int32_t set);
 /* plan_exploitation on the current estimates (no schedule state change). */
 spin_status spin_lbss_plan(spin_lbss* sel, int32_t* assignment);
+/* The next slot's assignment where already determined (prewarm planning): the
+ * current one inside a chunk / stage, the next chunk's draw at a chunk boundary
+ * (same Rng sequence), prewarm_destination before the first exploitation slot. */
+spin_status spin_lbss_peek(spin_lbss* sel, int32_t* assignment);
+
+/* The multi-GPU serving loop (csrc/serve.cpp): `slots_to_run` LBSS slots over
+ * this rank's contiguous shard (local_slots, n_local = the shard size of n_total
+ * requests over the communicator's ranks; comm may be NULL for one rank): per slot
+ * the selector's assignment, spin_round_prewarm (next slot's destinations warmed),
+ * observed goodput into the local ArmEstimate rows, spin_stats_allgather, and the
+ * gathered rows replacing the selector's estimates on every rank. */
+typedef struct spin_serve_report {
+  double device_ms;       /* sum of round_ms (switch catch-up included), this rank */
+  double wall_ms;         /* host wall time of the loop, this rank (gathers included) */
+  int64_t tokens;         /* accepted + bonus, this rank */
+  int64_t served;         /* request-slots served, this rank */
+  int32_t explore_slots;
+  int32_t epochs;
+  double switch_ms;       /* synchronous switch catch-up inside device_ms */
+  int64_t switch_tokens;  /* KV positions recomputed synchronously */
+} spin_serve_report;
+spin_status spin_lbss_serve(spin_ctx* ctx, spin_comm* comm, spin_lbss* sel, int32_t n_total, int32_t n_ssm,
+                            const int32_t* local_slots, int32_t n_local, int32_t slots_to_run, int32_t use_prewarm,
+                            spin_serve_report* rep, int32_t* final_assignment /* [n_total]: the plan on the
+                                                                                final estimates, or NULL */);
 
 /* ------------------------------------------------------------------------
  * Device plumbing: lets callers (and the parity tests) hold device buffers

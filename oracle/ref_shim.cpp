@@ -3,6 +3,7 @@
 // (see oracle/Makefile, target `ref`). TEST INFRASTRUCTURE ONLY: used to pin
 // the oracle and to generate tests/golden/ fixtures; never shipped or linked
 // by libspin.so. Output goes to oracle/_ref/ (git-ignored).
+#include <chrono>
 #include <cstring>
 #include <numeric>
 #include <exception>
@@ -191,6 +192,79 @@ int ref_lbss_trace(int n, int m, const int* caps, int alpha, int beta, unsigned 
       ++st.epoch;
     }
   });
+}
+
+// ---- single-threaded timings of the reference's own hot-path functions
+// (BASELINE.md section 4 row 1), on the caller's config-2 shapes. Seconds per call.
+namespace {
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+volatile long long g_sink = 0;
+}  // namespace
+
+double ref_time_pack(const int* kv_lens, int n, int width, int iters) {
+  const std::vector<int> lens(kv_lens, kv_lens + n);
+  const double t0 = now_s();
+  for (int i = 0; i < iters; ++i) g_sink = g_sink + pack(lens, width).padding_tokens;
+  return (now_s() - t0) / iters;
+}
+
+double ref_time_verify_batch_cost(const int* kv_lens, int n, int window, int packing, int width, int iters) {
+  const std::vector<int> lens(kv_lens, kv_lens + n);
+  const double t0 = now_s();
+  for (int i = 0; i < iters; ++i) g_sink = g_sink + verify_batch_cost(lens, window, packing != 0, width).tokens;
+  return (now_s() - t0) / iters;
+}
+
+// One head of the paper's decomposed attention (attention.cpp:98-162) over the
+// batch: request i has q_rows queries against kv_lens[i] keys of width dim
+// (make_toy_input data), packed by pack(kv_lens, width). Seconds per call.
+double ref_time_decomposed_attention(const int* kv_lens, int n, int q_rows, int dim, int width, int iters) {
+  std::vector<ToyAttentionInput> in;
+  std::vector<int> lens(kv_lens, kv_lens + n);
+  for (int i = 0; i < n; ++i) in.push_back(make_toy_input(1000 + i, q_rows, kv_lens[i], dim));
+  const PackedLayout L = pack(lens, width);
+  const IndicatorMask mask = build_indicator(L);
+  const double t0 = now_s();
+  for (int i = 0; i < iters; ++i) g_sink = g_sink + static_cast<long long>(decomposed_attention(in, L, mask).size());
+  return (now_s() - t0) / iters;
+}
+
+// SlotEngine::run_slot (slot_engine.cpp:70-167) on a config-2-like spec: n requests
+// with prompts U[lo, hi], 2 SSMs of capacity n, packing on; every request on ssm i%2.
+// Seconds per slot over `slots` slots.
+double ref_time_run_slot(int n, int prompt_lo, int prompt_hi, int window, int slots) {
+  WorkloadSpec spec;
+  spec.num_requests = n;
+  spec.window = window;
+  spec.seed = 2503;
+  for (int j = 0; j < 2; ++j) {
+    SsmProfile p;
+    p.id = j;
+    p.tokens_per_sec = j == 0 ? 400.0 : 150.0;
+    p.batch_capacity = n;
+    p.batch_slowdown = 0.01;
+    spec.ssm_profiles.push_back(p);
+  }
+  spec.llm.fixed_overhead_sec = 0.02;
+  spec.llm.per_token_sec = 1e-5;
+  DifficultyClass c;
+  c.name = "mix";
+  c.accept_range = {{0.5, 0.8}, {0.6, 0.9}};
+  c.prompt_len_lo = prompt_lo;
+  c.prompt_len_hi = prompt_hi;
+  c.target_len_lo = 1000000;
+  c.target_len_hi = 1000000;
+  spec.difficulty_mix.push_back(c);
+  EngineOptions opt;
+  opt.packing = true;
+  SlotEngine eng(spec, generate_workload(spec), opt);
+  std::vector<int> assign(n), prewarm(n, -1);
+  for (int i = 0; i < n; ++i) assign[i] = i % 2;
+  const double t0 = now_s();
+  for (int t = 0; t < slots; ++t) g_sink = g_sink + eng.run_slot(assign, prewarm, false, nullptr).served;
+  return (now_s() - t0) / slots;
 }
 
 }  // extern "C"

@@ -82,6 +82,12 @@ class VerifyStats(C.Structure):
                 ("target_tokens", C.POINTER(C.c_int32))]
 
 
+class ServeReport(C.Structure):
+    _fields_ = [("device_ms", C.c_double), ("wall_ms", C.c_double), ("tokens", C.c_int64), ("served", C.c_int64),
+                ("explore_slots", C.c_int32), ("epochs", C.c_int32), ("switch_ms", C.c_double),
+                ("switch_tokens", C.c_int64)]
+
+
 class RoundOut(C.Structure):
     _fields_ = [
         ("accepted", C.POINTER(C.c_int32)),
@@ -92,6 +98,10 @@ class RoundOut(C.Structure):
         ("draft_ms", C.c_float),
         ("verify_ms", C.c_float),
         ("round_ms", C.c_float),
+        ("switch_ms", C.c_float),
+        ("switch_tokens", C.c_int32),
+        ("spec_end_ms", C.c_float * 8),
+        ("switch_tokens_per_request", C.POINTER(C.c_int32)),
     ]
 
 
@@ -115,6 +125,7 @@ _SIGNATURES = {
     "spin_ctx_destroy": [C.c_void_p],
     "spin_prefill": [C.c_void_p, C.c_int32, P_I32, P_I32, P_I32],
     "spin_round": [C.c_void_p, C.c_int32, P_I32, P_I32, C.POINTER(RoundOut)],
+    "spin_round_prewarm": [C.c_void_p, C.c_int32, P_I32, P_I32, P_I32, C.POINTER(RoundOut)],
     "spin_run_rounds": [C.c_void_p, C.c_int32, P_I32, P_I32, C.c_int32, P_I64, P_F32],
     "spin_read_tokens": [C.c_void_p, C.c_int32, P_I32, C.c_int32, P_I32],
     "spin_read_logits": [C.c_void_p, P_F32, C.c_int64, P_I32],
@@ -143,6 +154,9 @@ _SIGNATURES = {
     "spin_lbss_observe": [C.c_void_p, C.c_int32, C.c_int32, C.c_double],
     "spin_lbss_rows": [C.c_void_p, P_F64, C.c_int32],
     "spin_lbss_plan": [C.c_void_p, P_I32],
+    "spin_lbss_peek": [C.c_void_p, P_I32],
+    "spin_lbss_serve": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, P_I32, C.c_int32, C.c_int32,
+                        C.c_int32, C.c_void_p, P_I32],
     "spin_device_alloc": [C.c_int32, C.c_size_t, C.POINTER(C.c_void_p)],
     "spin_device_free": [C.c_void_p],
     "spin_memcpy": [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32],

@@ -325,7 +325,15 @@ spin_status spin_prefill(spin_ctx* ctx, int32_t n, const int32_t* slots, const i
 spin_status spin_round(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of, spin_round_out* out) {
   return guarded([&] {
     if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
-    ctx->eng->round(n, slots, ssm_of, out);
+    ctx->eng->round(n, slots, ssm_of, nullptr, out);
+  });
+}
+
+spin_status spin_round_prewarm(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
+                               const int32_t* prewarm, spin_round_out* out) {
+  return guarded([&] {
+    if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
+    ctx->eng->round(n, slots, ssm_of, prewarm, out);
   });
 }
 
@@ -394,7 +402,7 @@ spin_status spin_last_round_trace(spin_ctx* ctx, float* spec_end_ms, int32_t cap
 spin_status spin_switch_ssm(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of) {
   return guarded([&] {
     if (!ctx) fail(SPIN_INPUT_ERROR, "null ctx");
-    ctx->eng->switch_ssm(n, slots, ssm_of);
+    (void)ctx->eng->switch_ssm(n, slots, ssm_of);
   });
 }
 

@@ -180,6 +180,7 @@ void Engine::init_model(ModelDev& m, const spin_model_desc& d, bool draft) {
 }
 
 const GemmPlan& Engine::plan(int n_out, int k, int t, int mode) {
+  std::lock_guard<std::mutex> lock(plan_mu_);  // std::map references stay valid across inserts
   const auto key = std::make_tuple(n_out, k, t, mode);
   auto it = plans_.find(key);
   if (it == plans_.end()) {
@@ -546,6 +547,13 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
   check_cuda(cudaEventCreate(&ev_start_), "event");
   check_cuda(cudaEventCreate(&ev_draft_), "event");
   check_cuda(cudaEventCreate(&ev_end_), "event");
+  check_cuda(cudaEventCreate(&ev_r0_), "event");
+  check_cuda(cudaEventCreate(&ev_r1_), "event");
+  ps_.resize(n_ssm);
+  for (auto& st : ps_) check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  ev_pw_.resize(n_ssm);
+  for (auto& e : ev_pw_) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  pw_pending_.assign(n_ssm, 0);
   ev_join_.resize(n_ssm);
   for (auto& e : ev_join_) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   ev_spec_end_.resize(n_ssm);  // per-SSM draft end (timing; the event trace)
@@ -555,6 +563,7 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
 }
 
 Engine::~Engine() {
+  if (pw_thread_.joinable()) pw_thread_.join();
   cudaDeviceSynchronize();
   for (auto& kv : rounds_) {
     if (kv.second->exec) cudaGraphExecDestroy(kv.second->exec);
@@ -574,6 +583,13 @@ Engine::~Engine() {
   cudaFreeHost(const_cast<int32_t*>(h_err_));
   cudaFreeHost(pin_in_), cudaFreeHost(pin_out_), cudaFree(d_in_), cudaFree(d_out_), cudaFree(d_emitted_);
   cudaEventDestroy(ev_fork_), cudaEventDestroy(ev_start_), cudaEventDestroy(ev_draft_), cudaEventDestroy(ev_end_);
+  cudaEventDestroy(ev_r0_), cudaEventDestroy(ev_r1_);
+  for (auto& e : ev_pw_) cudaEventDestroy(e);
+  for (auto& st : ps_) cudaStreamDestroy(st);
+  for (auto& l : pwlane_)
+    for (void* p : l.allocs) cudaFree(p);
+  for (int32_t* p : pw_pin_) cudaFreeHost(p);
+  for (int32_t* p : pw_len_pin_) cudaFreeHost(p);
   for (auto& e : ev_join_) cudaEventDestroy(e);
   for (auto& e : ev_spec_end_) cudaEventDestroy(e);
   for (auto& s : ss_) cudaStreamDestroy(s);
@@ -603,28 +619,41 @@ void Engine::sync_state_from_device() {
 // Ragged extend of one model over positions [from, to) of each slot: the
 // prompt prefill, and the KV recompute of an SSM switch (switching_cost,
 // slot_engine.cpp:12-22). Rows are cut into virtual requests of <= 8 queries.
-void Engine::extend(int model, const std::vector<std::tuple<int, int, int>>& ranges) {
+// Synchronous on sv_ (lane = the model's own lane) unless `pinned` is given: then
+// the chunks are staged in that pinned buffer and enqueued on `s` without any host
+// wait (the prewarm path; the caller owns the ordering).
+void Engine::extend(int model, const std::vector<std::tuple<int, int, int>>& ranges, cudaStream_t s, Lane* lane,
+                    int32_t* pinned, size_t pinned_cap) {
   ModelDev& m = model < 0 ? target_ : ssm_[model];
-  Lane& ln = model < 0 ? tlane_ : slane_[model];
+  Lane& ln = lane ? *lane : (model < 0 ? tlane_ : slane_[model]);
+  if (!s) s = sv_;
   std::vector<int32_t> rt, rs, rp, qs_, ql, kv, sl;
+  size_t pin_used = 0;
   auto flush = [&]() {
     if (rt.empty()) return;
     const int T = static_cast<int>(rt.size()), R = static_cast<int>(sl.size());
-    check_cuda(cudaMemcpyAsync(ln.meta.row_tok, rt.data(), T * 4, cudaMemcpyHostToDevice, sv_), "h2d");
-    check_cuda(cudaMemcpyAsync(ln.meta.row_slot, rs.data(), T * 4, cudaMemcpyHostToDevice, sv_), "h2d");
-    check_cuda(cudaMemcpyAsync(ln.meta.row_pos, rp.data(), T * 4, cudaMemcpyHostToDevice, sv_), "h2d");
-    check_cuda(cudaMemcpyAsync(ln.meta.req_slot, sl.data(), R * 4, cudaMemcpyHostToDevice, sv_), "h2d");
-    check_cuda(cudaMemcpyAsync(ln.meta.req_qstart, qs_.data(), R * 4, cudaMemcpyHostToDevice, sv_), "h2d");
-    check_cuda(cudaMemcpyAsync(ln.meta.req_qlen, ql.data(), R * 4, cudaMemcpyHostToDevice, sv_), "h2d");
-    check_cuda(cudaMemcpyAsync(ln.meta.req_kvlen, kv.data(), R * 4, cudaMemcpyHostToDevice, sv_), "h2d");
+    const int32_t* src[7] = {rt.data(), rs.data(), rp.data(), sl.data(), qs_.data(), ql.data(), kv.data()};
+    int32_t* dst[7] = {ln.meta.row_tok, ln.meta.row_slot, ln.meta.row_pos, ln.meta.req_slot, ln.meta.req_qstart,
+                       ln.meta.req_qlen, ln.meta.req_kvlen};
+    const int cnt[7] = {T, T, T, R, R, R, R};
+    for (int k = 0; k < 7; ++k) {
+      const int32_t* from = src[k];
+      if (pinned) {  // stage in pinned memory: the copy is truly asynchronous
+        if (pin_used + cnt[k] > pinned_cap) fail(SPIN_CAPACITY_ERROR, "extend: prewarm staging buffer exhausted");
+        std::memcpy(pinned + pin_used, src[k], cnt[k] * 4);
+        from = pinned + pin_used;
+        pin_used += cnt[k];
+      }
+      check_cuda(cudaMemcpyAsync(dst[k], from, cnt[k] * 4, cudaMemcpyHostToDevice, s), "h2d");
+    }
     MetaArgs a{};
     a.mode = kMetaExtend;
     a.n_req = R;
     a.width = R;
     a.chunks = attn_chunks(R, m.H, num_sms_);
-    launch_meta(a, st_, ln.meta, sv_);
-    forward(m, ln, FwdShape{T, R, R, kExtendQ}, sv_, 0);
-    sync_sv("extend");  // host vectors are reused
+    launch_meta(a, st_, ln.meta, s);
+    forward(m, ln, FwdShape{T, R, R, kExtendQ}, s, 0);
+    if (!pinned) sync_sv("extend");  // host vectors are reused
     rt.clear(), rs.clear(), rp.clear(), qs_.clear(), ql.clear(), kv.clear(), sl.clear();
   };
   for (const auto& [slot, from, to] : ranges) {
@@ -645,8 +674,94 @@ void Engine::extend(int model, const std::vector<std::tuple<int, int, int>>& ran
   flush();
 }
 
+// Device-side ordering: work on sv_ after this waits for every enqueued prewarm.
+void Engine::join_prewarm() {
+  if (pw_thread_.joinable()) pw_thread_.join();
+  if (pw_error_) {
+    pw_error_ = false;
+    fail(SPIN_CUDA_ERROR, "prewarm: " + pw_error_msg_);
+  }
+  for (size_t j = 0; j < pw_pending_.size(); ++j) {
+    if (!pw_pending_[j]) continue;
+    check_cuda(cudaStreamWaitEvent(sv_, ev_pw_[j], 0), "join prewarm");
+    pw_pending_[j] = 0;
+  }
+}
+
+// KV catch-up of SSM j for the listed requests on j's prewarm stream, concurrently
+// with whatever the device runs next (the destination of a future switch is warmed
+// in idle time: prewarm_destination, bandit.cpp:122-139; switching_cost = 0 when
+// prewarmed, slot_engine.cpp:12-22). Positions up to committed - 2 of the host
+// mirror; the round that later uses SSM j only catches up its own commits.
+void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm, const int32_t* ssm_of) {
+  const int M = static_cast<int>(ssm_.size()), R = opts_.max_requests;
+  if (pw_thread_.joinable()) pw_thread_.join();
+  std::vector<std::vector<std::tuple<int, int, int>>> jobs(M);
+  bool any = false;
+  for (int j = 0; j < M; ++j) {
+    for (int i = 0; i < n; ++i) {
+      if (prewarm[i] != j || (ssm_of && ssm_of[i] == j)) continue;
+      const int s = slots[i];
+      const int need = h_committed_[s] - 2;
+      int32_t& len = h_ssm_len_[static_cast<size_t>(j) * R + s];
+      if (len < need) {
+        jobs[j].emplace_back(s, len, need);
+        pw_tokens_ += need - len;
+        len = need;  // the host mirror; the device copy is written by the prewarm stream
+        any = true;
+      }
+    }
+  }
+  if (!any) return;
+  if (pwlane_.empty()) init_prewarm();
+  for (int j = 0; j < M; ++j)
+    if (!jobs[j].empty()) pw_pending_[j] = 1;
+  // The enqueue (staging + ~100 launches per 512-row chunk) runs on a worker thread
+  // while this thread waits for the round. It reads h_tokens_ positions < committed - 2
+  // of the prewarmed slots, which the round's host update (positions >= committed)
+  // never touches; join_prewarm() joins it before anything else is enqueued.
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "device");
+  pw_thread_ = std::thread([this, dev, jobs = std::move(jobs)]() {
+    try {
+      check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+      for (size_t j = 0; j < jobs.size(); ++j) {
+        if (jobs[j].empty()) continue;
+        cudaStream_t ps = ps_[j];
+        check_cuda(cudaEventSynchronize(ev_pw_[j]), "prewarm staging");  // staging reuse
+        extend(static_cast<int>(j), jobs[j], ps, &pwlane_[j], pw_pin_[j], pw_pin_cap_);
+        for (const auto& r : jobs[j]) {
+          const size_t idx = j * opts_.max_requests + std::get<0>(r);
+          pw_len_pin_[j][std::get<0>(r)] = std::get<2>(r);
+          check_cuda(cudaMemcpyAsync(st_.ssm_len + idx, pw_len_pin_[j] + std::get<0>(r), 4, cudaMemcpyHostToDevice,
+                                     ps),
+                     "h2d");
+        }
+        check_cuda(cudaEventRecord(ev_pw_[j], ps), "prewarm event");
+      }
+    } catch (const std::exception& e) {
+      pw_error_msg_ = e.what();
+      pw_error_ = true;
+    }
+  });
+}
+
+void Engine::init_prewarm() {
+  const int M = static_cast<int>(ssm_.size()), R = opts_.max_requests;
+  pwlane_.resize(M);
+  pw_pin_.assign(M, nullptr);
+  pw_pin_cap_ = static_cast<size_t>(8) * (static_cast<size_t>(R) * opts_.max_ctx + kExtendRows);
+  pw_len_pin_.assign(M, nullptr);
+  for (int j = 0; j < M; ++j) {
+    init_lane(pwlane_[j], ssm_[j], kExtendRows, kExtendRows, false);
+    check_cuda(cudaMallocHost(&pw_pin_[j], pw_pin_cap_ * 4), "prewarm staging");
+    check_cuda(cudaMallocHost(&pw_len_pin_[j], static_cast<size_t>(R) * 4), "prewarm staging");
+  }
+}
+
 void Engine::prefill(int n, const int32_t* slots, const int32_t* lens, const int32_t* prompts) {
   sync_state_from_device();
+  join_prewarm();
   std::vector<std::tuple<int, int, int>> ranges;
   std::vector<char> seen(opts_.max_requests, 0);
   size_t off = 0;
@@ -689,17 +804,25 @@ void Engine::prefill(int n, const int32_t* slots, const int32_t* lens, const int
   sync_sv("prefill");
 }
 
-void Engine::switch_ssm(int n, const int32_t* slots, const int32_t* ssm_of) {
+// Synchronous KV catch-up of requests whose SSM cache lags (a switch, or the
+// commits since a prewarm): recomputed on sv_ before the round. Returns the
+// positions recomputed per request in `per_req` (optional, [n]).
+int64_t Engine::switch_ssm(int n, const int32_t* slots, const int32_t* ssm_of, int32_t* per_req) {
   sync_state_from_device();
+  join_prewarm();
+  int64_t total = 0;
   for (int j = 0; j < static_cast<int>(ssm_.size()); ++j) {
     std::vector<std::tuple<int, int, int>> ranges;
     for (int i = 0; i < n; ++i) {
+      if (per_req && j == 0) per_req[i] = 0;
       if (ssm_of[i] != j) continue;
       const int s = slots[i];
       const int need = h_committed_[s] - 2;
       int32_t& len = h_ssm_len_[static_cast<size_t>(j) * opts_.max_requests + s];
       if (len < need) {
         ranges.emplace_back(s, len, need);
+        if (per_req) per_req[i] = need - len;
+        total += need - len;
         len = need;
       }
     }
@@ -714,6 +837,7 @@ void Engine::switch_ssm(int n, const int32_t* slots, const int32_t* ssm_of) {
     }
     sync_sv("switch");
   }
+  return total;
 }
 
 Engine::RoundPlan& Engine::plan_round(int n, const int32_t* slots, const int32_t* ssm_of) {
@@ -835,7 +959,7 @@ void Engine::capture_round(RoundPlan& p) {
   p.launches = launches_ - launches_before;
 }
 
-void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, spin_round_out* out) {
+void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, const int32_t* prewarm, spin_round_out* out) {
   sync_state_from_device();
   const int M = static_cast<int>(ssm_.size()), W = opts_.window, R = opts_.max_requests;
   if (n < 0 || n > R) fail(SPIN_CAPACITY_ERROR, "round: batch exceeds max_requests");
@@ -846,12 +970,18 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, spin_roun
     if (seen[s]) fail(SPIN_INPUT_ERROR, "round: duplicate slot");
     seen[s] = 1;
     if (ssm_of[i] < -1 || ssm_of[i] >= M) fail(SPIN_INPUT_ERROR, "round: unknown ssm in assignment");
+    if (prewarm && (prewarm[i] < -1 || prewarm[i] >= M)) fail(SPIN_INPUT_ERROR, "round: unknown ssm in prewarm");
     if (ssm_of[i] >= 0) {
       if (h_committed_[s] < 2) fail(SPIN_INPUT_ERROR, "round: slot was not prefilled");
       if (h_committed_[s] + W + 1 > opts_.max_ctx) fail(SPIN_CAPACITY_ERROR, "round: slot context is full");
     }
   }
-  switch_ssm(n, slots, ssm_of);
+  // The round's clock starts before the synchronous KV catch-up of switched
+  // requests: switching costs real device time and is charged to the round.
+  check_cuda(cudaEventRecord(ev_r0_, sv_), "event");
+  std::vector<int32_t> sw_tok(n, 0);
+  const int64_t sw_total = switch_ssm(n, slots, ssm_of, sw_tok.data());
+  check_cuda(cudaEventRecord(ev_r1_, sv_), "event");
   RoundPlan& p = plan_round(n, slots, ssm_of);
   // stage the lists
   std::vector<int> act;
@@ -876,6 +1006,8 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, spin_roun
   } else {
     capture_round(p);
   }
+  // destinations of future switches recomputed on idle streams while this round runs
+  if (prewarm) enqueue_prewarm(n, slots, prewarm, ssm_of);
   sync_sv("round");
   dump_stamps();
   float draft_ms = 0.f, total_ms = 0.f;
@@ -921,10 +1053,17 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, spin_roun
     ++a;
   }
   last_verify_rows_ = na * (W + 1);
+  float switch_ms = 0.f;
+  if (sw_total > 0) check_cuda(cudaEventElapsedTime(&switch_ms, ev_r0_, ev_r1_), "event timing");
+  last_switch_ms_ = switch_ms;
   if (out) {
     out->draft_ms = draft_ms;
-    out->round_ms = total_ms;
+    out->round_ms = total_ms + switch_ms;
     out->verify_ms = total_ms - draft_ms;
+    out->switch_ms = switch_ms;
+    out->switch_tokens = static_cast<int32_t>(sw_total);
+    for (int j = 0; j < SPIN_MAX_SSM; ++j) out->spec_end_ms[j] = j < M ? last_spec_ms_[j] : -1.f;
+    if (out->switch_tokens_per_request) std::memcpy(out->switch_tokens_per_request, sw_tok.data(), n * 4);
   }
 }
 
@@ -939,7 +1078,7 @@ void Engine::run_rounds(int n, const int32_t* slots, const int32_t* ssm_of, int 
   }
   // one host-driven round first: validates, switches SSMs, captures the graph
   spin_round_out tmp{};
-  round(n, slots, ssm_of, &tmp);
+  round(n, slots, ssm_of, nullptr, &tmp);
   RoundPlan& p = plan_round(n, slots, ssm_of);
   std::vector<unsigned long long> counts(rounds, 0);
   unsigned long long* d_counts = nullptr;
@@ -975,12 +1114,13 @@ void Engine::run_rounds(int n, const int32_t* slots, const int32_t* ssm_of, int 
 
 void Engine::profile_round(int n, const int32_t* slots, const int32_t* ssm_of, double* ms, double* bytes,
                            int64_t* launches) {
+  join_prewarm();
   const int saved = opts_.use_graphs;
   opts_.use_graphs = 0;
   prof_ = true;
   prof_recs_.clear();
   try {
-    round(n, slots, ssm_of, nullptr);
+    round(n, slots, ssm_of, nullptr, nullptr);
   } catch (...) {
     prof_ = false;
     opts_.use_graphs = saved;
@@ -1007,6 +1147,7 @@ void Engine::profile_round(int n, const int32_t* slots, const int32_t* ssm_of, d
 // time and algorithmic bytes (weights + activations in/out, or KV read + q/out).
 void Engine::kernel_bench(int kind, int iters, double* us_per_launch, double* bytes_per_launch) {
   sync_state_from_device();
+  join_prewarm();
   const int T = last_verify_rows_;
   if (T <= 0) fail(SPIN_INPUT_ERROR, "kernel_bench: run a round first");
   if (iters < 1) fail(SPIN_INPUT_ERROR, "kernel_bench: iters must be >= 1");
@@ -1086,6 +1227,7 @@ void Engine::kernel_bench(int kind, int iters, double* us_per_launch, double* by
 void Engine::verify_bench(int n, const int32_t* slots, const int32_t* draft_lens, const int32_t* drafts, int packed,
                           int iters, spin_verify_stats* out) {
   sync_state_from_device();
+  join_prewarm();
   const int W = opts_.window, R = opts_.max_requests;
   if (n < 1 || n > R) fail(SPIN_CAPACITY_ERROR, "verify_bench: batch exceeds max_requests");
   if (iters < 1) fail(SPIN_INPUT_ERROR, "verify_bench: iters must be >= 1");

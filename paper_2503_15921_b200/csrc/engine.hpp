@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <atomic>
 #include <map>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <memory>
 #include <tuple>
@@ -78,9 +81,11 @@ class Engine {
   ~Engine();
 
   void prefill(int n, const int32_t* slots, const int32_t* lens, const int32_t* prompts);
-  void round(int n, const int32_t* slots, const int32_t* ssm_of, spin_round_out* out);
+  // prewarm (optional, [n]): destination SSM to warm for request i while this round runs
+  void round(int n, const int32_t* slots, const int32_t* ssm_of, const int32_t* prewarm, spin_round_out* out);
   void run_rounds(int n, const int32_t* slots, const int32_t* ssm_of, int rounds, int64_t* emitted, float* ms);
-  void switch_ssm(int n, const int32_t* slots, const int32_t* ssm_of);
+  // synchronous KV catch-up (switches); positions recomputed, per request in per_req
+  int64_t switch_ssm(int n, const int32_t* slots, const int32_t* ssm_of, int32_t* per_req = nullptr);
   void read_tokens(int slot, int32_t* tokens, int cap, int32_t* len);
   void read_logits(float* logits, int64_t cap, int32_t* rows);
   // One round without graphs, with CUDA events around every launch; per
@@ -110,7 +115,25 @@ class Engine {
   std::string stamp_path_;
   unsigned long long* stamp_slot(int kind, int ctas);
   void dump_stamps();
-  void extend(int model, const std::vector<std::tuple<int, int, int>>& ranges);  // (slot, from, to)
+  void extend(int model, const std::vector<std::tuple<int, int, int>>& ranges, cudaStream_t s = nullptr,
+              Lane* lane = nullptr, int32_t* pinned = nullptr, size_t pinned_cap = 0);  // (slot, from, to)
+  void join_prewarm();
+  void enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm, const int32_t* ssm_of);
+  void init_prewarm();
+  // prewarm: per SSM a lane, a stream, staging and a completion event
+  std::vector<Lane> pwlane_;
+  std::vector<cudaStream_t> ps_;
+  std::vector<cudaEvent_t> ev_pw_;
+  std::vector<int32_t*> pw_pin_;
+  size_t pw_pin_cap_ = 0;
+  std::vector<char> pw_pending_;
+  std::thread pw_thread_;  // enqueues the prewarm extends while the round runs
+  std::vector<int32_t*> pw_len_pin_;  // pinned ssm_len values the prewarm stream uploads
+  bool pw_error_ = false;
+  std::string pw_error_msg_;
+  int64_t pw_tokens_ = 0;
+  float last_switch_ms_ = 0.f;
+  cudaEvent_t ev_r0_ = nullptr, ev_r1_ = nullptr;
   RoundPlan& plan_round(int n, const int32_t* slots, const int32_t* ssm_of);
   void capture_round(RoundPlan& p);
   void record_timing(cudaEvent_t ev, cudaStream_t s);
@@ -118,7 +141,8 @@ class Engine {
   void prof_end(cudaStream_t s, double bytes);
   bool capturing_ = false;
   bool prof_ = false;
-  int64_t launches_ = 0;
+  std::atomic<int64_t> launches_{0};
+  std::mutex plan_mu_;  // plans_ is shared with the prewarm thread
   struct ProfRec {
     int cat;
     cudaEvent_t a, b;

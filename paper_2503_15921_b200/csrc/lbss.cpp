@@ -139,6 +139,8 @@ struct Lbss {
   int chunk = 0, in_chunk = 0;
   long long exploit_left = 0;
   std::vector<int> assign, prewarm;
+  bool predrawn = false;
+  std::vector<int> next_draw;
 
   bool observed(int i, int j) const { return cnt[static_cast<size_t>(i) * m + j] > 0; }
   double mean(int i, int j) const {
@@ -273,11 +275,35 @@ struct Lbss {
     return out;
   }
 
+  // The assignment of the NEXT slot where it is already determined, for prewarm
+  // planning: inside a chunk or an exploitation stage it is the current one; at an
+  // exploration chunk boundary the next chunk is drawn now (the same draws in the
+  // same order as when next() reaches it: observations never touch the Rng); before
+  // the first exploitation slot it is the reference's own prewarm choice,
+  // prewarm_destination on the current estimates (bandit.cpp:296-299).
+  void peek(int32_t* out) {
+    if (exploring) {
+      if (in_chunk == 0) {
+        if (!predrawn) {
+          next_draw = draw();
+          predrawn = true;
+        }
+        std::copy(next_draw.begin(), next_draw.end(), out);
+      } else {
+        std::copy(assign.begin(), assign.end(), out);
+      }
+      return;
+    }
+    const std::vector<int> v = exploit_left == 0 ? prewarm_destination() : assign;
+    std::copy(v.begin(), v.end(), out);
+  }
+
   void next(int32_t* a, int32_t* pw, int32_t* explore, int32_t* ep) {
     if (ep) *ep = epoch;
     if (exploring) {
       if (in_chunk == 0) {
-        assign = draw();
+        assign = predrawn ? next_draw : draw();
+        predrawn = false;
         prewarm = assign;  // drawn one chunk ahead: destinations are prewarmed (bandit.cpp:157-160)
       }
       if (explore) *explore = 1;
@@ -362,6 +388,13 @@ spin_status spin_lbss_observe(spin_lbss* sel, int32_t request, int32_t ssm, doub
     if (request < 0 || request >= s.n || ssm < 0 || ssm >= s.m) fail(SPIN_INPUT_ERROR, "lbss: arm out of range");
     s.sum[static_cast<size_t>(request) * s.m + ssm] += goodput;
     ++s.cnt[static_cast<size_t>(request) * s.m + ssm];
+  });
+}
+
+spin_status spin_lbss_peek(spin_lbss* sel, int32_t* assignment) {
+  return guarded([&] {
+    if (!sel || !assignment) fail(SPIN_INPUT_ERROR, "spin_lbss_peek: null argument");
+    sel->s.peek(assignment);
   });
 }
 

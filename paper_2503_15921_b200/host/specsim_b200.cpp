@@ -415,13 +415,19 @@ SlotStats SlotEngine::run_slot(const std::vector<int>& assignment, const std::ve
   }
   stats.served = static_cast<int>(slots.size());
   const int n = stats.served, W = spec_.window;
-  std::vector<int32_t> acc(n), bonus(n), comm(n);
+  std::vector<int32_t> acc(n), bonus(n), comm(n), sw_tok(n, 0), pw;
+  for (int id : admitted_) {
+    if (assignment[id] < 0) continue;
+    pw.push_back(id < static_cast<int>(prewarm.size()) ? prewarm[id] : -1);
+  }
   spin_round_out out{};
   out.accepted = acc.data();
   out.bonus_token = bonus.data();
   out.committed = comm.data();
+  out.switch_tokens_per_request = sw_tok.data();
   if (n > 0) {
-    check(spin_round(ctx_, n, slots.data(), ssm_of.data(), &out));
+    // the caller's prewarm destinations are warmed on idle streams during this round
+    check(spin_round_prewarm(ctx_, n, slots.data(), ssm_of.data(), pw.data(), &out));
     const VerifyBatchCost cost = verify_batch_cost(kv_lens, W, options_.packing, options_.pack_width);
     stats.verify_tokens = cost.tokens;
     stats.padding_tokens = cost.padding;
@@ -441,14 +447,16 @@ SlotStats SlotEngine::run_slot(const std::vector<int>& assignment, const std::ve
     if (j >= 0) {
       const int prev = last_ssm_[id];
       rec.switched = prev >= 0 && prev != j;
-      if (rec.switched)
-        rec.switch_cost_sec = switching_cost(r, prev, j, id < static_cast<int>(prewarm.size()) ? prewarm[id] : -1,
-                                             spec_.ssm_profiles);
+      // measured switching cost: this request's share (by recomputed KV positions) of
+      // the round's synchronous catch-up; 0 when the destination was prewarmed
+      if (rec.switched && out.switch_tokens > 0)
+        rec.switch_cost_sec = out.switch_ms * 1e-3 * sw_tok[k] / static_cast<double>(out.switch_tokens);
       r.active_ssm = j;
       rec.proposed = W;
       rec.accepted = acc[k];
       rec.bonus = 1;
-      rec.wall_time_sec = stats.duration_sec;
+      // slot_engine.cpp:145: the request's own SSM's speculation time + the verify time
+      rec.wall_time_sec = (out.spec_end_ms[j] + out.verify_ms) * 1e-3;
       stats.outcomes.push_back({id, j, W, acc[k], 1, rec.wall_time_sec});
       const long long emitted = acc[k] + 1;
       r.generated_len = std::min(r.target_len, r.generated_len + emitted);

@@ -111,7 +111,9 @@ class Engine:
         flat = np.concatenate(prompts).astype(np.int32)
         _lib.check(self.lib.spin_prefill(self.ctx, len(slots), _p(slots), _p(lens), _p(flat)))
 
-    def round(self, slots, ssm_of):
+    def round(self, slots, ssm_of, prewarm=None):
+        """One speculation + verification slot (spin_round / spin_round_prewarm).
+        prewarm[i] (or -1): SSM whose KV is warmed for request i while the round runs."""
         slots = np.ascontiguousarray(slots, dtype=np.int32)
         ssm_of = np.ascontiguousarray(ssm_of, dtype=np.int32)
         n, W = len(slots), self.window
@@ -120,11 +122,21 @@ class Engine:
         comm = np.zeros(n, np.int32)
         drafts = np.zeros(n * W, np.int32)
         tgt = np.zeros(n * (W + 1), np.int32)
+        sw = np.zeros(n, np.int32)
         out = _lib.RoundOut(_p(acc), _p(bonus), _p(comm), _p(drafts), _p(tgt), 0.0, 0.0, 0.0)
-        _lib.check(self.lib.spin_round(self.ctx, n, _p(slots), _p(ssm_of), C.byref(out)))
+        out.switch_tokens_per_request = _p(sw)
+        if prewarm is None:
+            _lib.check(self.lib.spin_round(self.ctx, n, _p(slots), _p(ssm_of), C.byref(out)))
+        else:
+            pw = np.ascontiguousarray(prewarm, dtype=np.int32)
+            _lib.check(self.lib.spin_round_prewarm(self.ctx, n, _p(slots), _p(ssm_of), _p(pw), C.byref(out)))
+        spec_end = np.array(out.spec_end_ms[: len(self.ssms)], np.float32)
+        # per-request wall time (SlotRecord.wall_time_sec, slot_engine.cpp:145): own SSM's draft end + verify
+        wall_ms = np.where(ssm_of >= 0, spec_end[np.maximum(ssm_of, 0)] + out.verify_ms, 0.0)
         return {"accepted": acc, "bonus": bonus, "committed": comm, "drafts": drafts.reshape(n, W),
                 "target": tgt.reshape(n, W + 1), "draft_ms": out.draft_ms, "verify_ms": out.verify_ms,
-                "round_ms": out.round_ms}
+                "round_ms": out.round_ms, "switch_ms": out.switch_ms, "switch_tokens": out.switch_tokens,
+                "switch_tokens_per_request": sw, "spec_end_ms": spec_end, "wall_ms": wall_ms}
 
     def run_rounds(self, slots, ssm_of, rounds: int):
         slots = np.ascontiguousarray(slots, dtype=np.int32)

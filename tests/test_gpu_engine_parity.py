@@ -68,3 +68,34 @@ def test_wide_batch_mixed_draft_paths_vs_oracle():
         run.round(assign)
     run.check()
     run.close()
+
+
+def test_prewarm_hides_switch_catch_up_and_keeps_outcomes():
+    """spin_round_prewarm warms next slot's destinations on idle streams during the
+    round: the later switch only catches up the last round's commits (charged in
+    round_ms), and every token is identical to the unprewarmed run."""
+    prompts = synthetic_prompts(B, 16, 64, TINY_TARGET.vocab, 2503)
+    a = Engine(TINY_TARGET, TINY_SSMS, max_requests=B, max_ctx=CTX, window=W)
+    b = Engine(TINY_TARGET, TINY_SSMS, max_requests=B, max_ctx=CTX, window=W)
+    a.prefill(range(B), prompts)
+    b.prefill(range(B), prompts)
+    slots = np.arange(B, dtype=np.int32)
+    plans = [np.array([0, 1] * 4, np.int32), np.array([1, 0] * 4, np.int32), np.array([1, 0, 0, 1] * 2, np.int32)]
+    sw_a = sw_b = 0
+    for r in range(6):
+        cur, nxt = plans[r % 3], plans[(r + 1) % 3]
+        ra = a.round(slots, cur)
+        rb = b.round(slots, cur, prewarm=np.where(nxt != cur, nxt, -1))
+        for k in ("drafts", "target", "accepted", "bonus", "committed"):
+            assert np.array_equal(ra[k], rb[k]), (r, k)
+        if r > 0:
+            sw_a += ra["switch_tokens"]
+            sw_b += rb["switch_tokens"]
+            assert ra["switch_tokens"] > 0 and ra["switch_ms"] > 0
+            assert rb["round_ms"] >= rb["verify_ms"] + rb["draft_ms"] - 1e-3
+            assert np.all(rb["switch_tokens_per_request"] <= W + 1)  # only the last round's commits
+    assert sw_b < sw_a
+    for s in range(B):
+        assert np.array_equal(a.tokens(s), b.tokens(s))
+    a.close()
+    b.close()
