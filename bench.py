@@ -418,11 +418,14 @@ def run_c5(args, ranks):
     mine = shard(N, ranks.world, ranks.rank)
     n_local = len(mine)
     slots_n = args.steps + args.warmup
-    max_ctx = ((PROMPT_HI + (WINDOW + 1) * (slots_n + 4) + 8 + 63) // 64) * 64
+    max_ctx = ((PROMPT_HI + (WINDOW + 1) * (slots_n + 4 + 4 * 4) + 8 + 63) // 64) * 64
     prompts = synthetic_prompts(N, PROMPT_LO, PROMPT_HI, LLAMA_7B.vocab, SEED + 5)
     eng = Engine(LLAMA_7B, ssms, max_requests=n_local, max_ctx=max_ctx, window=WINDOW, device=ranks.local)
     eng.prefill(range(n_local), [prompts[i] for i in mine])
     slots = np.arange(n_local, dtype=np.int32)
+    # f1: pipelining plan tuned on measured throughput on this rank's shard (i % 2 assignment)
+    chosen, curve = eng.tune_micro_batches(slots, np.array([i % 2 for i in range(n_local)], np.int32),
+                                           max_micro_batches=4, probe_rounds=3)
     sel = Lbss(N, [N] * len(ssms), alpha=8, beta=2, seed=SEED)
     # warm-up slots (graph capture per assignment shape), then the timed slots
     serve(eng, sel, N, len(ssms), slots, args.warmup, ranks.comm)
@@ -446,6 +449,8 @@ def run_c5(args, ranks):
                     "d2h_bytes_per_step": 4 * n_local * (3 + 2 * WINDOW + 1)},
             "lbss": {"explore_slots": rep["explore_slots"], "epochs": rep["epochs"], "switch_ms": rep["switch_ms"],
                      "final_plan_histogram": np.bincount(final[final >= 0], minlength=len(ssms)).tolist()},
+            "pipelining": {"chosen_per_ssm": chosen.tolist(), "curve_tokens_per_s": curve, "probe_rounds": 3,
+                           "candidates": "uniform b = 1 (serial) .. 4 micro-batches per SSM"},
             "clocks": clk.summary()}
     if ranks.rank == 0:
         print(json.dumps(line), flush=True)
@@ -524,7 +529,7 @@ def main():
 
     world, rank, local = ranks.world, ranks.rank, ranks.local
     hbm, tflops, peak_src = peaks()
-    rounds_total = 2 * (args.warmup + args.steps) + 4
+    rounds_total = 2 * (args.warmup + args.steps) + 4 + 4 * 5  # + the pipelining probes
     max_ctx = ((PROMPT_HI + (WINDOW + 1) * rounds_total + 8 + 63) // 64) * 64
     eng = Engine(LLAMA_7B, (LLAMA_68M, LLAMA_160M), max_requests=BATCH, max_ctx=max_ctx, window=WINDOW, device=local,
                  pack_width=args.pack_width)
@@ -577,6 +582,14 @@ def main():
     roof["attention"] = {"achieved": a_achieved, "frac": a_achieved / hbm, "us_per_launch": a_us,
                          "alg_bytes_per_launch": a_bytes, "bound": "hbm",
                          "kernel": "packed ragged causal attention + shared-max combine"}
+    # f1: speculation/verification pipelining, tuned on measured throughput
+    # (tune_micro_batches, pipeline.cpp:345-380); the main line above is the serial round
+    chosen, curve = eng.tune_micro_batches(slots, assign, max_micro_batches=4, probe_rounds=4)
+    pipelining = {"candidates": "uniform b = 1 (serial) .. 4 micro-batches per SSM", "probe_rounds": 4,
+                  "curve_tokens_per_s": curve, "chosen_per_ssm": chosen.tolist(),
+                  "note": "b = 1 is the serial round; each further group re-streams the target weights in its own "
+                          "verification (HBM-bound at this batch), so the tuner keeps the serial round unless "
+                          "overlapping the drafts pays for that"}
     t_roof_us, alg_bytes, alg_flops = path_roofline_us(LLAMA_7B, committed - 0, WINDOW, hbm, tflops)
     verify_med = statistics.median(verify_us)
     round_ms = dev_ms_max / args.steps
@@ -588,7 +601,7 @@ def main():
             "verify_roofline_us": t_roof_us, "verify_roofline_frac": t_roof_us / verify_med,
             "verify_alg_bytes": alg_bytes, "verify_alg_flops": alg_flops,
             "mean_accepted_per_request": mean_acc, "per_class_ms_one_round": {k: v[0] for k, v in prof.items()},
-            "per_class_launches": {k: v[2] for k, v in prof.items()}}
+            "per_class_launches": {k: v[2] for k, v in prof.items()}, "pipelining": pipelining}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded random-init weights, planted bigram)",

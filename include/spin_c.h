@@ -177,6 +177,26 @@ spin_status spin_round_prewarm(spin_ctx* ctx, int32_t n, const int32_t* slots, c
 spin_status spin_run_rounds(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
                             int32_t rounds, int64_t* emitted, float* device_ms);
 
+/* Speculation/verification pipelining (pipeline.cpp:160-329): per SSM, its
+ * requests are split into per_ssm[j] micro-batch groups (near-equal, batch order);
+ * with any count above 1, each (SSM, group) drafts on the SSM's stream and is
+ * verified on its own, FIFO in expected arrival order, and in spin_run_rounds the
+ * next slot's draft of a group starts as soon as that group was verified
+ * (causality, pipeline.cpp:236-241) -- drafting overlaps verification. All ones
+ * (the default) is the serial round: every SSM drafts, one packed verification.
+ * Outcomes follow the same greedy semantics either way. */
+spin_status spin_set_micro_batches(spin_ctx* ctx, const int32_t* per_ssm, int32_t n_ssm);
+spin_status spin_get_micro_batches(spin_ctx* ctx, int32_t* per_ssm, int32_t n_ssm);
+/* tune_micro_batches (pipeline.cpp:345-380) on MEASURED throughput: uniform plans
+ * b = 1, 2 .. max_micro_batches (capped by the largest SSM batch), each probed with
+ * probe_rounds device-resident rounds (spin_run_rounds) on the given requests; stops
+ * at the first plan more than `threshold` below the best and keeps the last
+ * non-degraded one (set on the context, copied to chosen[n_ssm]); curve[k] = the
+ * measured accepted tokens/s of candidate k. The probes commit tokens (real rounds). */
+spin_status spin_tune_micro_batches(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
+                                    int32_t max_micro_batches, int32_t probe_rounds, double threshold,
+                                    int32_t* chosen, double* curve, int32_t curve_cap, int32_t* n_curve);
+
 /* Committed token history of one slot (prompt + generated). */
 spin_status spin_read_tokens(spin_ctx* ctx, int32_t slot, int32_t* tokens, int32_t cap, int32_t* len);
 /* fp32 target logits of the last verify ([rows, vocab]); needs debug_logits. */

@@ -126,6 +126,10 @@ _SIGNATURES = {
     "spin_prefill": [C.c_void_p, C.c_int32, P_I32, P_I32, P_I32],
     "spin_round": [C.c_void_p, C.c_int32, P_I32, P_I32, C.POINTER(RoundOut)],
     "spin_round_prewarm": [C.c_void_p, C.c_int32, P_I32, P_I32, P_I32, C.POINTER(RoundOut)],
+    "spin_set_micro_batches": [C.c_void_p, P_I32, C.c_int32],
+    "spin_get_micro_batches": [C.c_void_p, P_I32, C.c_int32],
+    "spin_tune_micro_batches": [C.c_void_p, C.c_int32, P_I32, P_I32, C.c_int32, C.c_int32, C.c_double, P_I32, P_F64,
+                                C.c_int32, P_I32],
     "spin_run_rounds": [C.c_void_p, C.c_int32, P_I32, P_I32, C.c_int32, P_I64, P_F32],
     "spin_read_tokens": [C.c_void_p, C.c_int32, P_I32, C.c_int32, P_I32],
     "spin_read_logits": [C.c_void_p, P_F32, C.c_int64, P_I32],

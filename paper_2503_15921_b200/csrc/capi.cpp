@@ -329,6 +329,32 @@ spin_status spin_round(spin_ctx* ctx, int32_t n, const int32_t* slots, const int
   });
 }
 
+spin_status spin_set_micro_batches(spin_ctx* ctx, const int32_t* per_ssm, int32_t n_ssm) {
+  return guarded([&] {
+    if (!ctx || !per_ssm) fail(SPIN_INPUT_ERROR, "spin_set_micro_batches: null argument");
+    ctx->eng->set_micro_batches(per_ssm, n_ssm);
+  });
+}
+
+spin_status spin_get_micro_batches(spin_ctx* ctx, int32_t* per_ssm, int32_t n_ssm) {
+  return guarded([&] {
+    if (!ctx || !per_ssm) fail(SPIN_INPUT_ERROR, "spin_get_micro_batches: null argument");
+    ctx->eng->get_micro_batches(per_ssm, n_ssm);
+  });
+}
+
+spin_status spin_tune_micro_batches(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
+                                    int32_t max_micro_batches, int32_t probe_rounds, double threshold,
+                                    int32_t* chosen, double* curve, int32_t curve_cap, int32_t* n_curve) {
+  return guarded([&] {
+    if (!ctx || !slots || !ssm_of) fail(SPIN_INPUT_ERROR, "spin_tune_micro_batches: null argument");
+    int nc = 0;
+    ctx->eng->tune_micro_batches(n, slots, ssm_of, max_micro_batches, probe_rounds, threshold, chosen, curve,
+                                 curve_cap, &nc);
+    if (n_curve) *n_curve = nc;
+  });
+}
+
 spin_status spin_round_prewarm(spin_ctx* ctx, int32_t n, const int32_t* slots, const int32_t* ssm_of,
                                const int32_t* prewarm, spin_round_out* out) {
   return guarded([&] {

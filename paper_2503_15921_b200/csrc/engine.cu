@@ -559,12 +559,21 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
   ev_spec_end_.resize(n_ssm);  // per-SSM draft end (timing; the event trace)
   for (auto& e : ev_spec_end_) check_cuda(cudaEventCreate(&e), "event");
   last_spec_ms_.assign(n_ssm, -1.f);
+  mb_.assign(n_ssm, 1);
   sync_sv("init sync");
 }
 
 Engine::~Engine() {
   if (pw_thread_.joinable()) pw_thread_.join();
   cudaDeviceSynchronize();
+  for (auto& kv : pipes_)
+    for (PipeUnit& u : kv.second->units) {
+      if (u.draft) cudaGraphExecDestroy(u.draft);
+      if (u.verify) cudaGraphExecDestroy(u.verify);
+      if (u.gd) cudaGraphDestroy(u.gd);
+      if (u.gv) cudaGraphDestroy(u.gv);
+      for (cudaEvent_t e : {u.ev_d, u.ev_v, u.t_d, u.t_v0, u.t_v1}) cudaEventDestroy(e);
+    }
   for (auto& kv : rounds_) {
     if (kv.second->exec) cudaGraphExecDestroy(kv.second->exec);
     if (kv.second->graph) cudaGraphDestroy(kv.second->graph);
@@ -873,9 +882,75 @@ void Engine::record_timing(cudaEvent_t ev, cudaStream_t s) {
     check_cuda(cudaEventRecord(ev, s), "event");
 }
 
+// The gamma-step draft loop of SSM j over nj requests (device list d_list) on stream sj.
+void Engine::enqueue_draft(int j, const int32_t* d_list, int nj, cudaStream_t sj) {
+  const int W = opts_.window;
+  ModelDev& m = ssm_[j];
+  Lane& ln = slane_[j];
+  const int tiles = (m.V + 127) / 128;
+  MetaArgs a{};
+  a.mode = kMetaDraft0;
+  a.n_req = nj;
+  a.list = d_list;
+  a.ssm = j;
+  a.width = nj;
+  a.chunks = attn_chunks(nj, m.H, num_sms_, 2);
+  a.padded = 1;  // few-query steps: one row per request, whole requests per CTA (no merges)
+  prof_begin(kProfMeta, sj);
+  launch_meta(a, st_, ln.meta, sj);
+  prof_end(sj, 0);
+  forward(m, ln, FwdShape{2 * nj, nj, nj, 2, 1}, sj, 1);
+  int prev_t = 2 * nj, prev_q = 2;
+  for (int k = 1; k <= W; ++k) {
+    MetaArgs b{};
+    b.mode = k < W ? kMetaDraftK : kMetaCollect;
+    b.n_req = nj;
+    b.list = d_list;
+    b.step = k;
+    b.ssm = j;
+    b.width = nj;
+    b.chunks = attn_chunks(nj, m.H, num_sms_, 1);
+    b.padded = 1;
+    b.amax_val = ln.amax_val;
+    b.amax_idx = ln.amax_idx;
+    b.amax_tiles = tiles;
+    b.prev_t = prev_t;
+    b.prev_qlen = prev_q;
+    prof_begin(kProfMeta, sj);
+    launch_meta(b, st_, ln.meta, sj);
+    prof_end(sj, 0);
+    if (k < W) forward(m, ln, FwdShape{nj, nj, nj, 1, 1}, sj, 1);
+    prev_t = nj, prev_q = 1;
+  }
+}
+
+// Pack (device request decomposition), target verify forward and greedy accept of n
+// requests (d_list slots, d_ssm_of their SSMs) on stream s; outcomes to d_out.
+void Engine::enqueue_verify(const int32_t* d_list, const int32_t* d_ssm_of, int n, int32_t* d_out, cudaStream_t s) {
+  const int W = opts_.window;
+  const int T = n * (W + 1);
+  const int width = opts_.pack_width > 0 ? std::min(opts_.pack_width, n) : n;
+  MetaArgs a{};
+  a.mode = kMetaVerify;
+  a.n_req = n;
+  a.list = d_list;
+  a.width = width;
+  a.padded = opts_.packing ? 0 : 1;
+  a.chunks = attn_chunks(a.padded ? n : width, target_.H, num_sms_);
+  prof_begin(kProfMeta, s);
+  launch_meta(a, st_, tlane_.meta, s);
+  prof_end(s, 0);
+  forward(target_, tlane_, FwdShape{T, n, a.padded ? n : width, W + 1, 1}, s, opts_.debug_logits ? 2 : 1);
+  int32_t* o = d_out;
+  prof_begin(kProfMeta, s);
+  launch_accept(tlane_.meta, n, W, d_list, d_ssm_of, tlane_.amax_val, tlane_.amax_idx, (target_.V + 127) / 128, T,
+                st_, o, o + n, o + 2 * n, o + 3 * n, o + 3 * n + n * W, d_emitted_, s);
+  prof_end(s, 0);
+}
+
 // Enqueues one round on sv_ (+ SSM streams); used for capture and direct runs.
 void Engine::capture_round(RoundPlan& p) {
-  const int W = opts_.window, M = static_cast<int>(ssm_.size());
+  const int M = static_cast<int>(ssm_.size());
   const int64_t launches_before = launches_;
   stamp_used_ = 0;
   stamp_tab_.clear();
@@ -886,77 +961,203 @@ void Engine::capture_round(RoundPlan& p) {
   for (int j = 0; j < M; ++j) {
     cudaStream_t sj = ss_[j];
     check_cuda(cudaStreamWaitEvent(sj, ev_fork_, 0), "fork");
-    const int nj = p.n_ssm[j];
-    if (nj > 0) {
-      ModelDev& m = ssm_[j];
-      Lane& ln = slane_[j];
-      const int32_t* list = d_in_ + p.off_ssm_list[j];
-      const int tiles = (m.V + 127) / 128;
-      MetaArgs a{};
-      a.mode = kMetaDraft0;
-      a.n_req = nj;
-      a.list = list;
-      a.ssm = j;
-      a.width = nj;
-      a.chunks = attn_chunks(nj, m.H, num_sms_, 2);
-      a.padded = 1;  // few-query steps: one row per request, whole requests per CTA (no merges)
-      prof_begin(kProfMeta, sj);
-      launch_meta(a, st_, ln.meta, sj);
-      prof_end(sj, 0);
-      forward(m, ln, FwdShape{2 * nj, nj, nj, 2, 1}, sj, 1);
-      int prev_t = 2 * nj, prev_q = 2;
-      for (int k = 1; k <= W; ++k) {
-        MetaArgs b{};
-        b.mode = k < W ? kMetaDraftK : kMetaCollect;
-        b.n_req = nj;
-        b.list = list;
-        b.step = k;
-        b.ssm = j;
-        b.width = nj;
-        b.chunks = attn_chunks(nj, m.H, num_sms_, 1);
-        b.padded = 1;
-        b.amax_val = ln.amax_val;
-        b.amax_idx = ln.amax_idx;
-        b.amax_tiles = tiles;
-        b.prev_t = prev_t;
-        b.prev_qlen = prev_q;
-        prof_begin(kProfMeta, sj);
-        launch_meta(b, st_, ln.meta, sj);
-        prof_end(sj, 0);
-        if (k < W) forward(m, ln, FwdShape{nj, nj, nj, 1, 1}, sj, 1);
-        prev_t = nj, prev_q = 1;
-      }
+    if (p.n_ssm[j] > 0) {
+      enqueue_draft(j, d_in_ + p.off_ssm_list[j], p.n_ssm[j], sj);
+      record_timing(ev_spec_end_[j], sj);
     }
-    if (p.n_ssm[j] > 0) record_timing(ev_spec_end_[j], sj);
     check_cuda(cudaEventRecord(ev_join_[j], sj), "join");
     check_cuda(cudaStreamWaitEvent(s, ev_join_[j], 0), "join");
   }
   record_timing(ev_draft_, s);
   const int n = p.n_act;
   if (n > 0) {
-    const int T = n * (W + 1);
-    const int width = opts_.pack_width > 0 ? std::min(opts_.pack_width, n) : n;
-    MetaArgs a{};
-    a.mode = kMetaVerify;
-    a.n_req = n;
-    a.list = d_in_ + p.off_list;
-    a.width = width;
-    a.padded = opts_.packing ? 0 : 1;
-    a.chunks = attn_chunks(a.padded ? n : width, target_.H, num_sms_);
-    prof_begin(kProfMeta, s);
-    launch_meta(a, st_, tlane_.meta, s);
-    prof_end(s, 0);
-    forward(target_, tlane_, FwdShape{T, n, a.padded ? n : width, W + 1, 1}, s, opts_.debug_logits ? 2 : 1);
-    int32_t* o = d_out_;
-    prof_begin(kProfMeta, s);
-    launch_accept(tlane_.meta, n, W, d_in_ + p.off_list, d_in_ + p.off_ssm_of, tlane_.amax_val, tlane_.amax_idx,
-                  (target_.V + 127) / 128, T, st_, o, o + n, o + 2 * n, o + 3 * n, o + 3 * n + n * W, d_emitted_, s);
-    prof_end(s, 0);
+    enqueue_verify(d_in_ + p.off_list, d_in_ + p.off_ssm_of, n, d_out_, s);
     check_cuda(cudaMemcpyAsync(pin_out_, d_out_, p.out_ints * 4, cudaMemcpyDeviceToHost, s), "d2h outcome");
   }
   record_timing(ev_end_, s);
   check_cuda(cudaGetLastError(), "round launch");
   p.launches = launches_ - launches_before;
+}
+
+// ------------------------------------------------------------------ pipelining
+void Engine::set_micro_batches(const int32_t* per_ssm, int m) {
+  if (m != static_cast<int>(ssm_.size())) fail(SPIN_INPUT_ERROR, "micro_batches: one count per SSM");
+  for (int j = 0; j < m; ++j)
+    if (per_ssm[j] < 1 || per_ssm[j] > 16) fail(SPIN_INPUT_ERROR, "micro_batches: counts must be in 1..16");
+  mb_.assign(per_ssm, per_ssm + m);
+}
+
+void Engine::get_micro_batches(int32_t* per_ssm, int m) const {
+  for (int j = 0; j < m && j < static_cast<int>(mb_.size()); ++j) per_ssm[j] = mb_[j];
+}
+
+// Units of the current micro-batch plan for this assignment shape: SSM j's n_j active
+// requests (batch order) split into min(b_j, n_j) near-equal groups, the remainder to
+// the earlier groups (pipeline.cpp:176-189). Verify order: expected arrival, i.e.
+// group g of SSM j done at (g + 1) / b_j of j's measured draft time (FIFO verifier,
+// pipeline.cpp:265-282).
+Engine::PipePlan& Engine::plan_pipe(int n, const int32_t* ssm_of) {
+  const int M = static_cast<int>(ssm_.size()), W = opts_.window;
+  std::vector<int> cnt(M, 0);
+  for (int i = 0; i < n; ++i)
+    if (ssm_of[i] >= 0) ++cnt[ssm_of[i]];
+  std::vector<int> key = mb_;
+  key.insert(key.end(), cnt.begin(), cnt.end());
+  auto it = pipes_.find(key);
+  if (it != pipes_.end()) return *it->second;
+  auto pp = std::make_unique<PipePlan>();
+  int off = 0, off_out = 0;
+  for (int j = 0; j < M; ++j) {
+    if (cnt[j] == 0) continue;
+    const int b = std::max(1, std::min(mb_[j], cnt[j]));
+    const int base = cnt[j] / b, extra = cnt[j] % b;
+    const double t_j = last_spec_ms_[j] > 0.f ? last_spec_ms_[j] : 0.1 * ssm_[j].L;
+    for (int g = 0; g < b; ++g) {
+      PipeUnit u;
+      u.ssm = j, u.g = g, u.n = base + (g < extra ? 1 : 0);
+      u.off_list = off, u.off_ssm_of = off + u.n, off += 2 * u.n;
+      u.off_out = off_out, off_out += u.n * (3 + 2 * W + 1);
+      u.arrival = t_j * (g + 1) / b;
+      check_cuda(cudaEventCreateWithFlags(&u.ev_d, cudaEventDisableTiming), "event");
+      check_cuda(cudaEventCreateWithFlags(&u.ev_v, cudaEventDisableTiming), "event");
+      check_cuda(cudaEventCreate(&u.t_d), "event");
+      check_cuda(cudaEventCreate(&u.t_v0), "event");
+      check_cuda(cudaEventCreate(&u.t_v1), "event");
+      pp->units.push_back(u);
+      pp->n_act += u.n;
+    }
+  }
+  pp->in_ints = off;
+  pp->out_ints = off_out;
+  pp->vorder.resize(pp->units.size());
+  for (size_t k = 0; k < pp->units.size(); ++k) pp->vorder[k] = static_cast<int>(k);
+  std::stable_sort(pp->vorder.begin(), pp->vorder.end(),
+                   [&](int a, int b) { return pp->units[a].arrival < pp->units[b].arrival; });
+  PipePlan& ref = *pp;
+  pipes_.emplace(key, std::move(pp));
+  return ref;
+}
+
+// Host staging of the unit lists (pinned): unit (j, g) takes SSM j's requests of
+// group g, in batch order.
+void Engine::stage_pipe(PipePlan& pp, int n, const int32_t* slots, const int32_t* ssm_of) {
+  std::vector<std::vector<int>> by_ssm(ssm_.size());
+  for (int i = 0; i < n; ++i)
+    if (ssm_of[i] >= 0) by_ssm[ssm_of[i]].push_back(i);
+  std::vector<size_t> cursor(ssm_.size(), 0);
+  for (PipeUnit& u : pp.units) {
+    for (int k = 0; k < u.n; ++k) {
+      const int i = by_ssm[u.ssm][cursor[u.ssm]++];
+      pin_in_[u.off_list + k] = slots[i];
+      pin_in_[u.off_ssm_of + k] = u.ssm;
+    }
+  }
+}
+
+// One pipelined slot: unit drafts on the SSM streams, unit verifies FIFO on sv_.
+// first: order the SSM streams after sv_ (host-driven slots, the first slot of a
+// device loop); later slots of a device loop only wait for their unit's previous
+// verification, so the next slot's drafting overlaps this slot's verifications.
+void Engine::launch_pipe_slot(PipePlan& pp, bool first, bool host_round) {
+  const bool graphs = opts_.use_graphs != 0;
+  if (first) {
+    check_cuda(cudaEventRecord(ev_start_, sv_), "event");
+    if (host_round)
+      check_cuda(cudaMemcpyAsync(d_in_, pin_in_, pp.in_ints * 4, cudaMemcpyHostToDevice, sv_), "h2d lists");
+    check_cuda(cudaEventRecord(ev_fork_, sv_), "event");
+    for (size_t j = 0; j < ssm_.size(); ++j) check_cuda(cudaStreamWaitEvent(ss_[j], ev_fork_, 0), "fork");
+  }
+  const int64_t before = launches_;
+  for (PipeUnit& u : pp.units) {
+    cudaStream_t sj = ss_[u.ssm];
+    if (!first) check_cuda(cudaStreamWaitEvent(sj, u.ev_v, 0), "unit causality");
+    if (graphs) {
+      if (!u.draft) {
+        check_cuda(cudaStreamBeginCapture(sj, cudaStreamCaptureModeRelaxed), "capture");
+        capturing_ = true;
+        enqueue_draft(u.ssm, d_in_ + u.off_list, u.n, sj);
+        capturing_ = false;
+        check_cuda(cudaStreamEndCapture(sj, &u.gd), "capture");
+        check_cuda(cudaGraphInstantiate(&u.draft, u.gd, 0), "instantiate");
+      }
+      check_cuda(cudaGraphLaunch(u.draft, sj), "graph launch");
+    } else {
+      enqueue_draft(u.ssm, d_in_ + u.off_list, u.n, sj);
+    }
+    check_cuda(cudaEventRecord(u.t_d, sj), "event");
+    check_cuda(cudaEventRecord(u.ev_d, sj), "event");
+  }
+  for (int k : pp.vorder) {
+    PipeUnit& u = pp.units[k];
+    check_cuda(cudaStreamWaitEvent(sv_, u.ev_d, 0), "unit drafted");
+    check_cuda(cudaEventRecord(u.t_v0, sv_), "event");
+    if (graphs) {
+      if (!u.verify) {
+        check_cuda(cudaStreamBeginCapture(sv_, cudaStreamCaptureModeRelaxed), "capture");
+        capturing_ = true;
+        enqueue_verify(d_in_ + u.off_list, d_in_ + u.off_ssm_of, u.n, d_out_ + u.off_out, sv_);
+        capturing_ = false;
+        check_cuda(cudaStreamEndCapture(sv_, &u.gv), "capture");
+        check_cuda(cudaGraphInstantiate(&u.verify, u.gv, 0), "instantiate");
+      }
+      check_cuda(cudaGraphLaunch(u.verify, sv_), "graph launch");
+    } else {
+      enqueue_verify(d_in_ + u.off_list, d_in_ + u.off_ssm_of, u.n, d_out_ + u.off_out, sv_);
+    }
+    check_cuda(cudaEventRecord(u.t_v1, sv_), "event");
+    check_cuda(cudaEventRecord(u.ev_v, sv_), "event");
+  }
+  if (pp.launches == 0 && launches_ > before) pp.launches = launches_ - before;  // counted at capture
+  if (host_round)
+    check_cuda(cudaMemcpyAsync(pin_out_, d_out_, pp.out_ints * 4, cudaMemcpyDeviceToHost, sv_), "d2h outcome");
+  check_cuda(cudaEventRecord(ev_end_, sv_), "event");
+  check_cuda(cudaGetLastError(), "pipelined slot launch");
+}
+
+// tune_micro_batches (pipeline.cpp:345-380) on MEASURED throughput: uniform plans with
+// b = 1 (the serial round) and b = 2 .. max_mb (capped by the largest SSM batch), each
+// probed with `probe_rounds` device-resident rounds on the live requests; the search
+// stops at the first plan more than `threshold` below the best so far and keeps the
+// last non-degraded plan.
+void Engine::tune_micro_batches(int n, const int32_t* slots, const int32_t* ssm_of, int max_mb, int probe_rounds,
+                                double threshold, int32_t* chosen, double* curve, int curve_cap, int* n_curve) {
+  const int M = static_cast<int>(ssm_.size());
+  if (probe_rounds < 1 || max_mb < 1 || !(threshold >= 0.0)) fail(SPIN_INPUT_ERROR, "tune: bad arguments");
+  std::vector<int> sizes(M, 0);
+  int largest = 1;
+  for (int i = 0; i < n; ++i)
+    if (ssm_of[i] >= 0) largest = std::max(largest, ++sizes[ssm_of[i]]);
+  std::vector<int> cand{1};
+  for (int b = 2; b <= std::min(max_mb, largest); ++b) cand.push_back(b);
+  auto uniform = [&](int b) {
+    std::vector<int32_t> p(M);
+    for (int j = 0; j < M; ++j) p[j] = std::max(1, std::min(b, sizes[j]));
+    return p;
+  };
+  std::vector<int32_t> last_good = uniform(1);
+  double best = -1.0;
+  int k = 0;
+  std::vector<int64_t> em(probe_rounds);
+  for (int b : cand) {
+    const std::vector<int32_t> plan = uniform(b);
+    set_micro_batches(plan.data(), M);
+    float ms = 0.f;
+    run_rounds(n, slots, ssm_of, probe_rounds, em.data(), &ms);
+    int64_t tok = 0;
+    for (int64_t e : em) tok += e;
+    const double tput = ms > 0.f ? tok / (ms * 1e-3) : 0.0;
+    if (curve && k < curve_cap) curve[k] = tput;
+    ++k;
+    best = std::max(best, tput);
+    if (tput >= (1.0 - threshold) * best) {
+      last_good = plan;
+    } else {
+      break;  // first clear degradation ends the search
+    }
+  }
+  set_micro_batches(last_good.data(), M);
+  if (chosen) std::copy(last_good.begin(), last_good.end(), chosen);
+  if (n_curve) *n_curve = k;
 }
 
 void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, const int32_t* prewarm, spin_round_out* out) {
@@ -982,48 +1183,85 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, const int
   std::vector<int32_t> sw_tok(n, 0);
   const int64_t sw_total = switch_ssm(n, slots, ssm_of, sw_tok.data());
   check_cuda(cudaEventRecord(ev_r1_, sv_), "event");
-  RoundPlan& p = plan_round(n, slots, ssm_of);
-  // stage the lists
-  std::vector<int> act;
-  for (int i = 0; i < n; ++i)
-    if (ssm_of[i] >= 0) act.push_back(i);
-  for (int a = 0; a < p.n_act; ++a) {
-    pin_in_[p.off_list + a] = slots[act[a]];
-    pin_in_[p.off_ssm_of + a] = ssm_of[act[a]];
-  }
-  std::vector<int> fill(M, 0);
-  for (int i : act) pin_in_[p.off_ssm_list[ssm_of[i]] + fill[ssm_of[i]]++] = slots[i];
-  if (opts_.use_graphs) {
-    if (!p.exec) {
-      check_cuda(cudaStreamBeginCapture(sv_, cudaStreamCaptureModeRelaxed), "capture");
-      capturing_ = true;
-      capture_round(p);
-      capturing_ = false;
-      check_cuda(cudaStreamEndCapture(sv_, &p.graph), "capture");
-      check_cuda(cudaGraphInstantiate(&p.exec, p.graph, 0), "instantiate");
+  // Outcome rows of request i: accepted, bonus, committed, drafts [W], target [W + 1].
+  struct Rows {
+    const int32_t *acc, *bon, *com, *dr, *tg;
+    int a;
+  };
+  std::vector<Rows> rows_of(n, Rows{nullptr, nullptr, nullptr, nullptr, nullptr, -1});
+  float draft_ms = 0.f, total_ms = 0.f, verify_ms = 0.f;
+  if (pipelined()) {
+    PipePlan& pp = plan_pipe(n, ssm_of);
+    stage_pipe(pp, n, slots, ssm_of);
+    launch_pipe_slot(pp, true, true);
+    if (prewarm) enqueue_prewarm(n, slots, prewarm, ssm_of);
+    sync_sv("round");
+    check_cuda(cudaEventElapsedTime(&total_ms, ev_start_, ev_end_), "event timing");
+    for (int j = 0; j < M; ++j) last_spec_ms_[j] = -1.f;
+    for (const PipeUnit& u : pp.units) {
+      float d = 0.f, v = 0.f;
+      check_cuda(cudaEventElapsedTime(&d, ev_start_, u.t_d), "event timing");
+      check_cuda(cudaEventElapsedTime(&v, u.t_v0, u.t_v1), "event timing");
+      draft_ms = std::max(draft_ms, d);
+      verify_ms += v;  // verifier busy time
+      last_spec_ms_[u.ssm] = std::max(last_spec_ms_[u.ssm], d);
     }
-    check_cuda(cudaGraphLaunch(p.exec, sv_), "graph launch");
+    // unit rows back to the requests (stage_pipe order)
+    std::vector<std::vector<int>> by_ssm(M);
+    for (int i = 0; i < n; ++i)
+      if (ssm_of[i] >= 0) by_ssm[ssm_of[i]].push_back(i);
+    std::vector<size_t> cur(M, 0);
+    for (const PipeUnit& u : pp.units) {
+      const int32_t* o = pin_out_ + u.off_out;
+      for (int k = 0; k < u.n; ++k) {
+        const int i = by_ssm[u.ssm][cur[u.ssm]++];
+        rows_of[i] = Rows{o, o + u.n, o + 2 * u.n, o + 3 * u.n, o + 3 * u.n + u.n * W, k};
+      }
+    }
+    last_verify_rows_ = 0;  // the in-situ kernel replays expect a serial round's layout
   } else {
-    capture_round(p);
+    RoundPlan& p = plan_round(n, slots, ssm_of);
+    // stage the lists
+    std::vector<int> act;
+    for (int i = 0; i < n; ++i)
+      if (ssm_of[i] >= 0) act.push_back(i);
+    for (int a = 0; a < p.n_act; ++a) {
+      pin_in_[p.off_list + a] = slots[act[a]];
+      pin_in_[p.off_ssm_of + a] = ssm_of[act[a]];
+    }
+    std::vector<int> fill(M, 0);
+    for (int i : act) pin_in_[p.off_ssm_list[ssm_of[i]] + fill[ssm_of[i]]++] = slots[i];
+    if (opts_.use_graphs) {
+      if (!p.exec) {
+        check_cuda(cudaStreamBeginCapture(sv_, cudaStreamCaptureModeRelaxed), "capture");
+        capturing_ = true;
+        capture_round(p);
+        capturing_ = false;
+        check_cuda(cudaStreamEndCapture(sv_, &p.graph), "capture");
+        check_cuda(cudaGraphInstantiate(&p.exec, p.graph, 0), "instantiate");
+      }
+      check_cuda(cudaGraphLaunch(p.exec, sv_), "graph launch");
+    } else {
+      capture_round(p);
+    }
+    // destinations of future switches recomputed on idle streams while this round runs
+    if (prewarm) enqueue_prewarm(n, slots, prewarm, ssm_of);
+    sync_sv("round");
+    dump_stamps();
+    check_cuda(cudaEventElapsedTime(&draft_ms, ev_start_, ev_draft_), "event timing");
+    check_cuda(cudaEventElapsedTime(&total_ms, ev_start_, ev_end_), "event timing");
+    verify_ms = total_ms - draft_ms;
+    for (int j = 0; j < M; ++j) {
+      last_spec_ms_[j] = -1.f;
+      if (p.n_ssm[j] > 0)
+        check_cuda(cudaEventElapsedTime(&last_spec_ms_[j], ev_start_, ev_spec_end_[j]), "event timing");
+    }
+    const int na = p.n_act;
+    for (int a = 0; a < na; ++a)
+      rows_of[act[a]] = Rows{pin_out_, pin_out_ + na, pin_out_ + 2 * na, pin_out_ + 3 * na,
+                             pin_out_ + 3 * na + na * W, a};
+    last_verify_rows_ = na * (W + 1);
   }
-  // destinations of future switches recomputed on idle streams while this round runs
-  if (prewarm) enqueue_prewarm(n, slots, prewarm, ssm_of);
-  sync_sv("round");
-  dump_stamps();
-  float draft_ms = 0.f, total_ms = 0.f;
-  check_cuda(cudaEventElapsedTime(&draft_ms, ev_start_, ev_draft_), "event timing");
-  check_cuda(cudaEventElapsedTime(&total_ms, ev_start_, ev_end_), "event timing");
-  for (int j = 0; j < M; ++j) {
-    last_spec_ms_[j] = -1.f;
-    if (p.n_ssm[j] > 0) check_cuda(cudaEventElapsedTime(&last_spec_ms_[j], ev_start_, ev_spec_end_[j]), "event timing");
-  }
-  const int na = p.n_act;
-  const int32_t* acc = pin_out_;
-  const int32_t* bon = pin_out_ + na;
-  const int32_t* com = pin_out_ + 2 * na;
-  const int32_t* dr = pin_out_ + 3 * na;
-  const int32_t* tg = pin_out_ + 3 * na + na * W;
-  int a = 0;
   for (int i = 0; i < n; ++i) {
     const int s = slots[i];
     if (ssm_of[i] < 0) {
@@ -1032,34 +1270,33 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, const int
       if (out && out->committed) out->committed[i] = h_committed_[s];
       continue;
     }
+    const Rows& r = rows_of[i];
+    const int a = r.a, acc = r.acc[a], bon = r.bon[a], com = r.com[a];
+    const int32_t* dr = r.dr + static_cast<size_t>(a) * W;
     const int c = h_committed_[s];
     int32_t* hist = h_tokens_.data() + static_cast<size_t>(s) * opts_.max_ctx;
-    for (int k = 0; k < acc[a]; ++k) hist[c + k] = dr[static_cast<size_t>(a) * W + k];
-    hist[c + acc[a]] = bon[a];
-    h_committed_[s] = com[a];
-    for (int j = 0; j < M; ++j) {
-      int32_t& len = h_ssm_len_[static_cast<size_t>(j) * R + s];
-      if (j == ssm_of[i]) len = std::min(c + W - 1, c + acc[a]);
-    }
+    for (int k = 0; k < acc; ++k) hist[c + k] = dr[k];
+    hist[c + acc] = bon;
+    h_committed_[s] = com;
+    int32_t& len = h_ssm_len_[static_cast<size_t>(ssm_of[i]) * R + s];
+    len = std::min(c + W - 1, c + acc);
     if (out) {
-      if (out->accepted) out->accepted[i] = acc[a];
-      if (out->bonus_token) out->bonus_token[i] = bon[a];
-      if (out->committed) out->committed[i] = com[a];
-      if (out->drafts) std::memcpy(out->drafts + static_cast<size_t>(i) * W, dr + static_cast<size_t>(a) * W, W * 4);
+      if (out->accepted) out->accepted[i] = acc;
+      if (out->bonus_token) out->bonus_token[i] = bon;
+      if (out->committed) out->committed[i] = com;
+      if (out->drafts) std::memcpy(out->drafts + static_cast<size_t>(i) * W, dr, W * 4);
       if (out->target_tokens)
-        std::memcpy(out->target_tokens + static_cast<size_t>(i) * (W + 1), tg + static_cast<size_t>(a) * (W + 1),
+        std::memcpy(out->target_tokens + static_cast<size_t>(i) * (W + 1), r.tg + static_cast<size_t>(a) * (W + 1),
                     (W + 1) * 4);
     }
-    ++a;
   }
-  last_verify_rows_ = na * (W + 1);
   float switch_ms = 0.f;
   if (sw_total > 0) check_cuda(cudaEventElapsedTime(&switch_ms, ev_r0_, ev_r1_), "event timing");
   last_switch_ms_ = switch_ms;
   if (out) {
     out->draft_ms = draft_ms;
     out->round_ms = total_ms + switch_ms;
-    out->verify_ms = total_ms - draft_ms;
+    out->verify_ms = verify_ms;
     out->switch_ms = switch_ms;
     out->switch_tokens = static_cast<int32_t>(sw_total);
     for (int j = 0; j < SPIN_MAX_SSM; ++j) out->spec_end_ms[j] = j < M ? last_spec_ms_[j] : -1.f;
@@ -1079,7 +1316,9 @@ void Engine::run_rounds(int n, const int32_t* slots, const int32_t* ssm_of, int 
   // one host-driven round first: validates, switches SSMs, captures the graph
   spin_round_out tmp{};
   round(n, slots, ssm_of, nullptr, &tmp);
-  RoundPlan& p = plan_round(n, slots, ssm_of);
+  const bool pipe = pipelined();
+  RoundPlan* p = pipe ? nullptr : &plan_round(n, slots, ssm_of);
+  PipePlan* pp = pipe ? &plan_pipe(n, ssm_of) : nullptr;
   std::vector<unsigned long long> counts(rounds, 0);
   unsigned long long* d_counts = nullptr;
   check_cuda(cudaMalloc(&d_counts, rounds * 8), "counts");
@@ -1089,10 +1328,12 @@ void Engine::run_rounds(int n, const int32_t* slots, const int32_t* ssm_of, int 
   check_cuda(cudaMemsetAsync(d_emitted_, 0, 8, sv_), "memset");
   check_cuda(cudaEventRecord(a, sv_), "event");
   for (int r = 0; r < rounds; ++r) {
-    if (opts_.use_graphs)
-      check_cuda(cudaGraphLaunch(p.exec, sv_), "graph launch");
+    if (pipe)  // slots overlap: a unit's next draft waits only for that unit's verification
+      launch_pipe_slot(*pp, r == 0, false);
+    else if (opts_.use_graphs)
+      check_cuda(cudaGraphLaunch(p->exec, sv_), "graph launch");
     else
-      capture_round(p);
+      capture_round(*p);
     check_cuda(cudaMemcpyAsync(d_counts + r, d_emitted_, 8, cudaMemcpyDeviceToDevice, sv_), "count");
   }
   check_cuda(cudaEventRecord(b, sv_), "event");
@@ -1344,6 +1585,7 @@ void Engine::last_round_trace(float* spec_end_ms, int cap) const {
 }
 
 int64_t Engine::launches_per_round(int n, const int32_t* slots, const int32_t* ssm_of) {
+  if (pipelined()) return plan_pipe(n, ssm_of).launches;
   return plan_round(n, slots, ssm_of).launches;
 }
 

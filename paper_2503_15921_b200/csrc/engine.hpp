@@ -101,6 +101,44 @@ class Engine {
 
  private:
   struct RoundPlan;
+  // Speculation/verification pipelining (simulate_pipelined,
+  // pipeline.cpp:160-329): each SSM's requests split into micro-batch groups; a unit
+  // (SSM j, group g) drafts on j's stream and is verified on its own, FIFO on sv_; the
+  // next slot's draft of a unit starts as soon as that unit was verified (causality,
+  // pipeline.cpp:236-241), so drafting overlaps the verification of other units.
+  struct PipeUnit {
+    int ssm = 0, g = 0, n = 0;
+    int off_list = 0, off_ssm_of = 0, off_out = 0;
+    double arrival = 0.0;  // expected draft end (verify FIFO order)
+    cudaGraph_t gd = nullptr, gv = nullptr;
+    cudaGraphExec_t draft = nullptr, verify = nullptr;
+    cudaEvent_t ev_d = nullptr, ev_v = nullptr;             // ordering
+    cudaEvent_t t_d = nullptr, t_v0 = nullptr, t_v1 = nullptr;  // timing
+  };
+  struct PipePlan {
+    std::vector<PipeUnit> units;  // SSM-major, groups in order (draft order per stream)
+    std::vector<int> vorder;      // verify order (expected arrival)
+    int in_ints = 0, out_ints = 0, n_act = 0;
+    int64_t launches = 0;
+  };
+  std::vector<int> mb_;  // micro-batches per SSM; all ones = the serial round
+  std::map<std::vector<int>, std::unique_ptr<PipePlan>> pipes_;
+  bool pipelined() const {
+    for (int b : mb_)
+      if (b != 1) return true;
+    return false;
+  }
+  PipePlan& plan_pipe(int n, const int32_t* ssm_of);
+  void stage_pipe(PipePlan& pp, int n, const int32_t* slots, const int32_t* ssm_of);
+  void launch_pipe_slot(PipePlan& pp, bool first, bool host_round);
+
+ public:
+  void set_micro_batches(const int32_t* per_ssm, int m);
+  void get_micro_batches(int32_t* per_ssm, int m) const;
+  void tune_micro_batches(int n, const int32_t* slots, const int32_t* ssm_of, int max_mb, int probe_rounds,
+                          double threshold, int32_t* chosen, double* curve, int curve_cap, int* n_curve);
+
+ private:
   void init_model(ModelDev& m, const spin_model_desc& d, bool draft);
   void init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool logits);
   void forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, int head_mode);
@@ -136,6 +174,8 @@ class Engine {
   cudaEvent_t ev_r0_ = nullptr, ev_r1_ = nullptr;
   RoundPlan& plan_round(int n, const int32_t* slots, const int32_t* ssm_of);
   void capture_round(RoundPlan& p);
+  void enqueue_draft(int j, const int32_t* d_list, int nj, cudaStream_t sj);
+  void enqueue_verify(const int32_t* d_list, const int32_t* d_ssm_of, int n, int32_t* d_out, cudaStream_t s);
   void record_timing(cudaEvent_t ev, cudaStream_t s);
   void prof_begin(int cat, cudaStream_t s);
   void prof_end(cudaStream_t s, double bytes);

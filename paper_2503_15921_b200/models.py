@@ -201,6 +201,28 @@ class Engine:
         return {"us": st.us, "query_rows": st.query_rows, "real_rows": st.real_rows, "kv_tokens": st.kv_tokens,
                 "target": tgt}
 
+    def set_micro_batches(self, per_ssm):
+        """Speculation/verification pipelining plan (spin_set_micro_batches); all ones = serial."""
+        p = np.ascontiguousarray(per_ssm, dtype=np.int32)
+        _lib.check(self.lib.spin_set_micro_batches(self.ctx, _p(p), len(p)))
+
+    def micro_batches(self) -> np.ndarray:
+        p = np.zeros(len(self.ssms), np.int32)
+        _lib.check(self.lib.spin_get_micro_batches(self.ctx, _p(p), len(p)))
+        return p
+
+    def tune_micro_batches(self, slots, ssm_of, max_micro_batches=4, probe_rounds=4, threshold=0.05):
+        """tune_micro_batches on measured throughput; returns (chosen plan, curve of tokens/s)."""
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        ssm_of = np.ascontiguousarray(ssm_of, dtype=np.int32)
+        chosen = np.zeros(len(self.ssms), np.int32)
+        curve = np.zeros(16, np.float64)
+        k = C.c_int32()
+        _lib.check(self.lib.spin_tune_micro_batches(self.ctx, len(slots), _p(slots), _p(ssm_of), max_micro_batches,
+                                                    probe_rounds, threshold, _p(chosen),
+                                                    curve.ctypes.data_as(_lib.P_F64), 16, C.byref(k)))
+        return chosen, curve[: k.value].tolist()
+
     def switch(self, slots, ssm_of):
         slots = np.ascontiguousarray(slots, dtype=np.int32)
         ssm_of = np.ascontiguousarray(ssm_of, dtype=np.int32)
