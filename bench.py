@@ -482,7 +482,7 @@ def gemm_roofline(eng, target, T, hbm, tflops, peak_src):
                 traffic = json.load(f).get("bytes_per_launch_target_gemm")
         except Exception:
             traffic = None
-    tensor = g_flops / g_bytes > hbm * 1e9 / (tflops * 1e12)  # arithmetic intensity above the ridge
+    tensor = g_flops / g_bytes > tflops * 1e12 / (hbm * 1e9)  # arithmetic intensity (flop/B) above the ridge
     if tensor:
         achieved = g_flops / (g_us * 1e-6) / 1e12
         return {"bound": "tensor", "kernel": "tcgen05 weight-streaming GEMM (target projections)",
