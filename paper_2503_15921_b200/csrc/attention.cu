@@ -337,36 +337,58 @@ __global__ void __launch_bounds__(32 * kVW) attn_kernel(const __grid_constant__ 
       const int qbase = ph.kvlen - ph.qlen;  // absolute position of query 0
       if (stamp && k == 0 && pb == p_lo) w.st[8 * blockIdx.x + 3] = ptx::globaltimer() + (qh[0][0][0] == 12345u);
 
-      for (int t = 0; t * 16 < ph.len; ++t) {
-        const int st = consumed % S;
-        ptx::mbar_wait(&bar[st], static_cast<uint32_t>((consumed / S) & 1));
-        if (stamp && consumed == 0) w.st[8 * blockIdx.x + 2] = ptx::globaltimer();
-        const uint32_t kb = ptx::smem_u32(ring + st * C::kStage);
-        const uint32_t vb = kb + C::kHalf;
-        // ---- S^T = K Q^T : 16 keys x 8 queries per n-tile. Four independent accumulator
+      // Software-pipelined tile loop: the scores of tile t + 1 (S^T = K Q^T, independent of
+      // tile t's softmax and P V) are issued before tile t's softmax and O^T += V^T P^T, so
+      // the two mma.sync chains and the exp / shuffle work of neighbouring tiles overlap
+      // inside the warp (each warp owns a whole (row, head): its tile chain is the critical path).
+      auto scores = [&](int stg, float (&sv)[NQT][4]) {
+        // S^T = K Q^T : 16 keys x 8 queries per n-tile. Four independent accumulator
         // chains (k-step parity x hi/lo plane) keep the mma.sync pipeline full; summed at the end.
-        float s[NQT][4];
-        {
-          float sc[NQT][4][4];
+        const uint32_t kb = ptx::smem_u32(ring + stg * C::kStage);
+        float sc[NQT][4][4];
 #pragma unroll
-          for (int nt = 0; nt < NQT; ++nt)
+        for (int nt = 0; nt < NQT; ++nt)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) sc[nt][c][0] = sc[nt][c][1] = sc[nt][c][2] = sc[nt][c][3] = 0.f;
+          for (int c = 0; c < 4; ++c) sc[nt][c][0] = sc[nt][c][1] = sc[nt][c][2] = sc[nt][c][3] = 0.f;
 #pragma unroll
-          for (int kt = 0; kt < DT; ++kt) {
-            uint32_t a[4];
-            ldsm_x4(kb + kvoff<HD>((lane & 7) + ((lane >> 3) & 1) * 8, 2 * kt + (lane >> 4), ph.tok0), a);
+        for (int kt = 0; kt < DT; ++kt) {
+          uint32_t a[4];
+          ldsm_x4(kb + kvoff<HD>((lane & 7) + ((lane >> 3) & 1) * 8, 2 * kt + (lane >> 4), ph.tok0), a);
 #pragma unroll
-            for (int nt = 0; nt < NQT; ++nt) {
-              mma16816(sc[nt][kt & 1], a, qh[nt][kt][0], qh[nt][kt][1]);
-              mma16816(sc[nt][2 + (kt & 1)], a, ql[nt][kt][0], ql[nt][kt][1]);
-            }
+          for (int nt = 0; nt < NQT; ++nt) {
+            mma16816(sc[nt][kt & 1], a, qh[nt][kt][0], qh[nt][kt][1]);
+            mma16816(sc[nt][2 + (kt & 1)], a, ql[nt][kt][0], ql[nt][kt][1]);
           }
-#pragma unroll
-          for (int nt = 0; nt < NQT; ++nt)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) s[nt][e] = (sc[nt][0][e] + sc[nt][1][e]) + (sc[nt][2][e] + sc[nt][3][e]);
         }
+#pragma unroll
+        for (int nt = 0; nt < NQT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sv[nt][e] = (sc[nt][0][e] + sc[nt][1][e]) + (sc[nt][2][e] + sc[nt][3][e]);
+      };
+      // (NQT > 1 keeps the plain order: the look-ahead scores would spill at 3 query tiles)
+      constexpr bool kPipe = NQT == 1;
+      const int ntile = (ph.len + 15) / 16;
+      float s[NQT][4];
+      if (kPipe) {
+        ptx::mbar_wait(&bar[consumed % S], static_cast<uint32_t>((consumed / S) & 1));
+        if (stamp && consumed == 0) w.st[8 * blockIdx.x + 2] = ptx::globaltimer();
+        scores(consumed % S, s);
+      }
+      for (int t = 0; t < ntile; ++t) {
+        const int st = consumed % S;
+        const bool more = kPipe && t + 1 < ntile;
+        float s_next[NQT][4];
+        if (!kPipe) {
+          ptx::mbar_wait(&bar[st], static_cast<uint32_t>((consumed / S) & 1));
+          if (stamp && consumed == 0) w.st[8 * blockIdx.x + 2] = ptx::globaltimer();
+          scores(st, s);
+        }
+        if (more) {  // tile t + 1 is already in flight (the ring keeps S >= 2 tiles issued ahead)
+          const int st1 = (consumed + 1) % S;
+          ptx::mbar_wait(&bar[st1], static_cast<uint32_t>(((consumed + 1) / S) & 1));
+          scores(st1, s_next);
+        }
+        const uint32_t vb = ptx::smem_u32(ring + st * C::kStage) + C::kHalf;
         // ---- mask + online softmax per query column (keys gq, gq+8; queries 2cq, 2cq+1)
         const int key0 = ph.tok0 + t * 16 + gq;
         const int kend = ph.tok0 + ph.len;
@@ -429,6 +451,12 @@ __global__ void __launch_bounds__(32 * kVW) attn_kernel(const __grid_constant__ 
         ++consumed;
         __syncwarp();
         try_issue();
+        if (more) {
+#pragma unroll
+          for (int nt = 0; nt < NQT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) s[nt][e] = s_next[nt][e];
+        }
       }
 
       if constexpr (NQT == 1) {

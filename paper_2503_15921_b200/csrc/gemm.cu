@@ -41,9 +41,12 @@ struct Piece {
 struct PieceIter {
   long long u, u_end;  // stream-K unit range (PARTIAL)
   int next_tile;       // round-robin tile (ARGMAX)
+  int grp, my_nt;      // grouped stream-K: this CTA's group and token tile
 
   __device__ void init(const PieceMap& pm, int n_tiles) {
-    const long long c = blockIdx.x;
+    grp = pm.ntg > 1 ? static_cast<int>(blockIdx.x) / pm.ntg : static_cast<int>(blockIdx.x);
+    my_nt = pm.ntg > 1 ? static_cast<int>(blockIdx.x) % pm.ntg : 0;
+    const long long c = grp;
     u = c * pm.units / pm.grid;
     u_end = (c + 1) * pm.units / pm.grid;
     next_tile = blockIdx.x;
@@ -52,11 +55,12 @@ struct PieceIter {
   __device__ bool next(const PieceMap& pm, int n_tiles, Piece& p) {
     if (pm.mode == kGemmPartial) {
       if (u >= u_end) return false;
-      p.tile = static_cast<int>(u / pm.kb);
+      const int t = static_cast<int>(u / pm.kb);  // tile, or weight tile when grouped
+      p.tile = pm.ntg > 1 ? t * pm.n_ntiles + my_nt : t;
       p.kb0 = static_cast<int>(u % pm.kb);
       const long long left = u_end - u;
       p.kb1 = static_cast<int>((p.kb0 + left < pm.kb) ? p.kb0 + left : pm.kb);
-      p.slot = static_cast<int>(blockIdx.x) - pm.cta_of(static_cast<long long>(p.tile) * pm.kb);
+      p.slot = grp - pm.cta_of(static_cast<long long>(t) * pm.kb);
       u += p.kb1 - p.kb0;
       return true;
     }
@@ -129,7 +133,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      const uint64_t pol_w = ptx::policy_evict_first();  // weights stream through once
+      // weights stream through once (evict-first), unless sibling CTAs of a group re-read them
+      const uint64_t pol_w = pm.ntg > 1 ? ptx::policy_evict_last() : ptx::policy_evict_first();
       const uint64_t pol_x = ptx::policy_evict_last();   // activations are re-read by every CTA
       PieceIter it;
       it.init(pm, n_tiles);
@@ -385,6 +390,15 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
   m.n_ntiles = p.n_ntiles;
   m.bn = p.bn;
   m.units = n_tiles * p.kb;
+  static const bool grouped_ok = [] {
+    const char* e = std::getenv("SPIN_GEMM_GROUPED");  // A/B switch
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  if (mode == kGemmPartial && p.n_ntiles > 1 && grouped_ok && p.n_ntiles <= num_sms) {
+    m.ntg = p.n_ntiles;
+    m.units = static_cast<long long>(p.n_mtiles) * p.kb;
+    num_sms /= m.ntg;  // the stream-K search below runs over CTA groups
+  }
   if (mode == kGemmPartial) {
     // At least kMinUnits k-blocks (64 KiB of weights) per CTA: small draft
     // GEMMs then use fewer SMs instead of fragmenting every tile into many
@@ -407,7 +421,7 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
         w = std::max(w, q.pieces(static_cast<int>((tile % p.n_ntiles) * p.bn), static_cast<int>((tile / p.n_ntiles) * kBlockM)));
       return w;
     };
-    if (m.grid == num_sms && n_tiles * p.kb <= (1 << 20)) {
+    if (m.grid == num_sms && m.units <= (1 << 20)) {
       int best = m.grid, best_w = worst(m.grid);
       for (int g = m.grid - 1; g >= m.grid - slack && g > 0; --g) {
         const int w = worst(g);
@@ -428,7 +442,7 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
     m.grid = static_cast<int>(std::min<long long>(num_sms, n_tiles));
     p.max_pieces = 1;
   }
-  p.grid = m.grid;
+  p.grid = m.grid * m.ntg;
   return p;
 }
 

@@ -37,16 +37,22 @@ struct PieceMap {
                     // so the CTAs streaming them run concurrently and share each weight atom in L2)
   int bn;           // token tile
   int mode;         // GemmMode
+  // Grouped stream-K (PARTIAL, more than one token tile): the stream-K units are the
+  // weight tiles' k-blocks alone (units = n_mtiles * kb) and `grid` counts CTA GROUPS of
+  // ntg = n_ntiles CTAs; the CTAs of a group stream the same weight range at the same
+  // time, each against its own token tile, so every weight atom comes from DRAM once and
+  // from L2 for its siblings (instead of once per token tile). ntg = 1: plain stream-K.
+  int ntg = 1;
   const uint8_t* tbl = nullptr;  // device: pieces per tile (filled by the host at plan time)
 
-  // CTA that owns stream-K unit u.
+  // CTA (group, when ntg > 1) that owns stream-K unit u.
   __host__ __device__ __forceinline__ int cta_of(long long u) const {
     return static_cast<int>((u * grid + grid - 1) / units);
   }
   // Number of partial slots written for (token t, feature n).
   __host__ __device__ __forceinline__ int pieces(int t, int n) const {
     if (mode != kGemmPartial) return 1;
-    const long long tile = static_cast<long long>(n / 128) * n_ntiles + t / bn;
+    const long long tile = ntg > 1 ? static_cast<long long>(n / 128) : static_cast<long long>(n / 128) * n_ntiles + t / bn;
     return cta_of(tile * kb + kb - 1) - cta_of(tile * kb) + 1;
   }
   __device__ __forceinline__ int tile_pieces(int t, int n) const { return tbl[(n / 128) * n_ntiles + t / bn]; }
@@ -56,7 +62,7 @@ struct GemmPlan {
   int n_out = 0, k = 0, t = 0;
   std::vector<uint8_t> tile_pieces;  // host copy of PieceMap::tbl
   int bn = 0, n_ntiles = 0, n_mtiles = 0, kb = 0;
-  int grid = 0, stages = 0, max_pieces = 1;
+  int grid = 0, stages = 0, max_pieces = 1;  // grid: CTAs launched (= map.grid * map.ntg)
   size_t smem_bytes = 0;
   PieceMap map{};
 };
