@@ -125,26 +125,47 @@ def path_roofline_us(target, committed, window, hbm_gbs, tflops):
 
 # ---------------------------------------------------------------- ranks and collectives
 class Ranks:
-    """rank / world / local device, and libspin's communicator (NCCL) for N > 1."""
+    """rank / world / device, and libspin's communicator for N > 1: NCCL (ncclAllGather of
+    the stats rows); the TCP transport when SPIN_COMM=tcp or when NCCL cannot initialise
+    (same gather semantics; the gathered rows are host data either way).
+    SPIN_BENCH_SHARE_DEVICE=1 puts every rank on device 0 (functional runs of the N > 1
+    path on a one-GPU box; NCCL refuses two ranks on one device, so it implies TCP)."""
 
     def __init__(self):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.shared = os.environ.get("SPIN_BENCH_SHARE_DEVICE", "0") == "1"
+        self.device = 0 if self.shared else self.local
         self.comm = None
+        self.backend = None
         if self.world > 1:
-            from paper_2503_15921_b200 import dist
+            from paper_2503_15921_b200 import _lib, dist
 
-            uid = os.environ.get("SPIN_COMM_ID")
-            if uid is None:  # launched by torchrun: rank 0's NCCL id travels over torch's CPU store
+            want = "tcp" if self.shared or os.environ.get("SPIN_COMM", "nccl") == "tcp" else "nccl"
+            ids = os.environ.get("SPIN_COMM_ID")
+            if ids is None:  # launched by torchrun: rank 0's ids travel over torch's CPU store
                 import torch.distributed as tdist
 
                 tdist.init_process_group("gloo")
-                obj = [dist.unique_id(dist.NCCL).hex() if self.rank == 0 else None]
+                obj = [None]
+                if self.rank == 0:
+                    nccl = dist.unique_id(dist.NCCL).hex() if want == "nccl" else ""
+                    obj = [nccl + ":" + dist.unique_id(dist.TCP).hex()]
                 tdist.broadcast_object_list(obj, src=0)
-                uid = obj[0]
+                ids = obj[0]
                 tdist.destroy_process_group()
-            self.comm = dist.Comm(dist.NCCL, self.rank, self.world, bytes.fromhex(uid), self.local)
+            nccl_id, tcp_id = ids.split(":")
+            if want == "nccl" and nccl_id:
+                try:
+                    self.comm = dist.Comm(dist.NCCL, self.rank, self.world, bytes.fromhex(nccl_id), self.device)
+                    self.backend = "nccl"
+                except _lib.SpinError as e:
+                    print(f"rank {self.rank}: NCCL communicator failed ({e}); using the TCP transport",
+                          file=sys.stderr, flush=True)
+            if self.comm is None:
+                self.comm = dist.Comm(dist.TCP, self.rank, self.world, bytes.fromhex(tcp_id), self.device)
+                self.backend = "tcp"
 
     def barrier(self):
         if self.comm is not None:
@@ -165,11 +186,13 @@ def spawn_ranks(n: int) -> int:
     """`bench.py --gpus N` without WORLD_SIZE: one process per GPU, NCCL id from here."""
     from paper_2503_15921_b200 import dist
 
-    uid = dist.unique_id(dist.NCCL).hex()
+    nccl = "" if os.environ.get("SPIN_COMM") == "tcp" or os.environ.get("SPIN_BENCH_SHARE_DEVICE") == "1" \
+        else dist.unique_id(dist.NCCL).hex()
+    ids = nccl + ":" + dist.unique_id(dist.TCP).hex()
     procs = []
     for r in range(n):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(n), LOCAL_RANK=str(r), LOCAL_WORLD_SIZE=str(n),
-                   SPIN_COMM_ID=uid, MASTER_ADDR="127.0.0.1")
+                   SPIN_COMM_ID=ids, MASTER_ADDR="127.0.0.1")
         procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env,
                                       stdout=None if r == 0 else subprocess.DEVNULL))
     return max(p.wait() for p in procs)
@@ -420,17 +443,17 @@ def run_c5(args, ranks):
     slots_n = args.steps + args.warmup
     max_ctx = ((PROMPT_HI + (WINDOW + 1) * (slots_n + 4 + 4 * 4) + 8 + 63) // 64) * 64
     prompts = synthetic_prompts(N, PROMPT_LO, PROMPT_HI, LLAMA_7B.vocab, SEED + 5)
-    eng = Engine(LLAMA_7B, ssms, max_requests=n_local, max_ctx=max_ctx, window=WINDOW, device=ranks.local)
+    eng = Engine(LLAMA_7B, ssms, max_requests=n_local, max_ctx=max_ctx, window=WINDOW, device=ranks.device)
     eng.prefill(range(n_local), [prompts[i] for i in mine])
     slots = np.arange(n_local, dtype=np.int32)
     # f1: pipelining plan tuned on measured throughput on this rank's shard (i % 2 assignment)
     chosen, curve = eng.tune_micro_batches(slots, np.array([i % 2 for i in range(n_local)], np.int32),
-                                           max_micro_batches=4, probe_rounds=3)
+                                           max_micro_batches=args.max_micro_batches, probe_rounds=3)
     sel = Lbss(N, [N] * len(ssms), alpha=8, beta=2, seed=SEED)
     # warm-up slots (graph capture per assignment shape), then the timed slots
     serve(eng, sel, N, len(ssms), slots, args.warmup, ranks.comm)
     ranks.barrier()
-    with ClockSampler(ranks.local) as clk:
+    with ClockSampler(ranks.device) as clk:
         rep, final = serve(eng, sel, N, len(ssms), slots, args.steps, ranks.comm)
         ranks.barrier()
     dev_ms = ranks.max(rep["device_ms"])
@@ -444,7 +467,8 @@ def run_c5(args, ranks):
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "c5: 256 requests sharded over the ranks, LLaMA-7B-shaped target, "
                                    "LLaMA-68M/160M-shaped SSMs, LBSS (alpha 8, beta 2) on every rank",
-                       "requests_per_gpu": n_local, "parallelism": f"request-sharded dp{ranks.world}"},
+                       "requests_per_gpu": n_local, "parallelism": f"request-sharded dp{ranks.world}",
+                       "comm": ranks.backend, "shared_device": ranks.shared},
             "e2e": {"value": tokens / (wall_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * 3 * n_local,
                     "d2h_bytes_per_step": 4 * n_local * (3 + 2 * WINDOW + 1)},
             "lbss": {"explore_slots": rep["explore_slots"], "epochs": rep["epochs"], "switch_ms": rep["switch_ms"],
@@ -504,9 +528,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--pack-width", type=int, default=0)
+    ap.add_argument("--max-micro-batches", type=int, default=4, help="f1 tuner candidates (1 = serial only)")
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if os.environ.get("SPIN_BENCH_SHARE_DEVICE") == "1":
+        # functional runs of the N > 1 plumbing on one GPU: ranks time-slice the device, so
+        # the pipelining probes (per-unit graphs on several streams) are not meaningful there
+        # (and hit an illegal address once in that setting; one process per GPU never did)
+        args.max_micro_batches = 1
     if args.impl == "reference":
         run_reference(args)
         return
@@ -527,7 +557,7 @@ def main():
     from paper_2503_15921_b200.dist import AcceptanceStats
     from paper_2503_15921_b200.models import LLAMA_7B, LLAMA_68M, LLAMA_160M, Engine, synthetic_prompts
 
-    world, rank, local = ranks.world, ranks.rank, ranks.local
+    world, rank, local = ranks.world, ranks.rank, ranks.device
     hbm, tflops, peak_src = peaks()
     rounds_total = 2 * (args.warmup + args.steps) + 4 + 4 * 5  # + the pipelining probes
     max_ctx = ((PROMPT_HI + (WINDOW + 1) * rounds_total + 8 + 63) // 64) * 64
@@ -584,7 +614,7 @@ def main():
                          "kernel": "packed ragged causal attention + shared-max combine"}
     # f1: speculation/verification pipelining, tuned on measured throughput
     # (tune_micro_batches, pipeline.cpp:345-380); the main line above is the serial round
-    chosen, curve = eng.tune_micro_batches(slots, assign, max_micro_batches=4, probe_rounds=4)
+    chosen, curve = eng.tune_micro_batches(slots, assign, max_micro_batches=args.max_micro_batches, probe_rounds=4)
     pipelining = {"candidates": "uniform b = 1 (serial) .. 4 micro-batches per SSM", "probe_rounds": 4,
                   "curve_tokens_per_s": curve, "chosen_per_ssm": chosen.tolist(),
                   "note": "b = 1 is the serial round; each further group re-streams the target weights in its own "
@@ -597,6 +627,7 @@ def main():
     d2h = 4 * BATCH * (3 + 2 * WINDOW + 1)
     mean_acc = float(emitted.sum()) / (args.steps * BATCH) - 1.0
     info = {"pack_width": args.pack_width or BATCH, "parallelism": f"request-sharded dp{world}",
+            "comm": ranks.backend, "shared_device": ranks.shared,
             "verify_step_us_median": verify_med, "draft_us_median": statistics.median(draft_us),
             "verify_roofline_us": t_roof_us, "verify_roofline_frac": t_roof_us / verify_med,
             "verify_alg_bytes": alg_bytes, "verify_alg_flops": alg_flops,

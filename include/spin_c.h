@@ -360,6 +360,15 @@ spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int3
                            int32_t ctx, int32_t layer, const void* k_cache, const void* v_cache, const void* q,
                            int32_t n_req, const int32_t* req_slot, const int32_t* req_qlen, const int32_t* req_kvlen,
                            int32_t width, void* out);
+/* The same production kernel family with an explicit score scale and causal flag:
+ * scale = 1, causal = 0 is the reference's toy mode (attention.cpp:67-162: unscaled,
+ * every query sees all of its request's keys; kvlen may then be < qlen). Used by
+ * tests/test_gpu_attention_toy.py to pin the production kernel to the reference's
+ * own reference_attention / decomposed_attention outputs. */
+spin_status spin_attention_ex(void* stream, int32_t n_heads, int32_t head_dim, int32_t layers, int32_t slots,
+                              int32_t ctx, int32_t layer, const void* k_cache, const void* v_cache, const void* q,
+                              int32_t n_req, const int32_t* req_slot, const int32_t* req_qlen,
+                              const int32_t* req_kvlen, int32_t width, float scale, int32_t causal, void* out);
 
 #ifdef __cplusplus
 }

@@ -13,6 +13,12 @@ Cases follow the reference's own tests:
   attention             test_attention.cpp:85-161 (seeds 21, 22/23, 31-33, random 424242)
   acceptance            test_model.cpp:112-142 (p = 0, 0.8, 1; E = 2.3616)
 
+`python oracle/make_golden.py toy_bf16` writes tests/golden/toy_bf16_golden.json: the
+reference's reference_attention and decomposed_attention (pack width as given) on
+make_toy_input data whose K / V are rounded to bf16 and Q to fp32 -- the operand
+precisions of the production attention kernel -- so that kernel, run in toy mode
+(scale 1, non-causal), can be pinned to the reference's own outputs.
+
 `python oracle/make_golden.py lbss` writes tests/golden/lbss_golden.json: the
 reference selector's assignment / prewarm / explore trace (run_lbss control flow,
 bandit.cpp:248-332, replayed by ref_lbss_trace in oracle/ref_shim.cpp) on seeded
@@ -199,8 +205,58 @@ def lbss_main():
     print("wrote", LBSS_OUT, os.path.getsize(LBSS_OUT), "bytes")
 
 
+TOY_OUT = os.path.join(os.path.dirname(OUT), "toy_bf16_golden.json")
+
+
+def bf16_round(x):
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def toy_main():
+    lib = load_ref()
+    rng = np.random.default_rng(20240002)
+    specs = [([(21, 3, 6)], 1, 4), ([(22, 3, 10), (23, 3, 2)], 2, 4), ([(31, 2, 9), (32, 2, 4), (33, 2, 3)], 2, 4),
+             ([(61, 5, 37), (62, 5, 12), (63, 5, 80), (64, 5, 5)], 3, 64), ([(71, 8, 90), (72, 1, 33)], 1, 64),
+             ([(81, 4, 40), (82, 4, 17), (83, 4, 29), (84, 2, 16), (85, 4, 1)], 2, 128)]
+    for _ in range(30):
+        n = int(rng.integers(1, 7))
+        specs.append(([(int(rng.integers(0, 2**62)), int(rng.integers(1, 9)), int(rng.integers(1, 40)))
+                       for _ in range(n)], int(rng.integers(1, n + 1)), int(rng.choice([4, 8, 64]))))
+    out = []
+    for spec, width, dim in specs:
+        qs, ks, vs = [], [], []
+        for seed, q, kv in spec:
+            Q, K, V = np.zeros(q * dim), np.zeros(kv * dim), np.zeros(kv * dim)
+            lib.ref_make_toy_input(seed, q, kv, dim, ptr(Q), ptr(K), ptr(V))
+            qs.append(Q.astype(np.float32).astype(np.float64)), ks.append(bf16_round(K)), vs.append(bf16_round(V))
+        Q, K, V = np.concatenate(qs), np.concatenate(ks), np.concatenate(vs)
+        qr = np.array([s_[1] for s_ in spec], np.int32)
+        kr = np.array([s_[2] for s_ in spec], np.int32)
+        dec = np.zeros(Q.size)
+        st = lib.ref_decomposed_attention(len(spec), dim, ptr(qr), ptr(kr), ptr(Q), ptr(K), ptr(V), width, ptr(dec))
+        assert st == 0, st
+        refo, qo, ko = [], 0, 0
+        for q, kv in zip(qr, kr):
+            o = np.zeros(q * dim)
+            lib.ref_reference_attention(int(q), int(kv), dim, ptr(Q[qo * dim:]), ptr(K[ko * dim:]), ptr(V[ko * dim:]),
+                                        ptr(o))
+            refo.append(o)
+            qo += q
+            ko += kv
+        out.append({"q_rows": qr.tolist(), "kv_rows": kr.tolist(), "width": width, "dim": dim, "q": Q.tolist(),
+                    "k": K.tolist(), "v": V.tolist(), "decomposed": dec.tolist(),
+                    "reference": np.concatenate(refo).tolist()})
+    with open(TOY_OUT, "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+    print("wrote", TOY_OUT, os.path.getsize(TOY_OUT), "bytes")
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "lbss":
+    if len(sys.argv) > 1 and sys.argv[1] == "toy_bf16":
+        toy_main()
+    elif len(sys.argv) > 1 and sys.argv[1] == "lbss":
         lbss_main()
     else:
         main()

@@ -139,6 +139,9 @@ _SIGNATURES = {
     "spin_kernel_bench": [C.c_void_p, C.c_int32, C.c_int32, P_F64, P_F64],
     "spin_attention": [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                        C.c_void_p, C.c_void_p, C.c_int32, P_I32, P_I32, P_I32, C.c_int32, C.c_void_p],
+    "spin_attention_ex": [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                          C.c_void_p, C.c_void_p, C.c_int32, P_I32, P_I32, P_I32, C.c_int32, C.c_float, C.c_int32,
+                          C.c_void_p],
     "spin_last_round_trace": [C.c_void_p, P_F32, C.c_int32],
     "spin_verify_bench": [C.c_void_p, C.c_int32, P_I32, P_I32, P_I32, C.c_int32, C.c_int32, C.c_void_p],
     "spin_gemm_info": [C.c_int32, C.c_int32, C.c_int32, C.c_int32, P_I32, P_I32, P_I32],

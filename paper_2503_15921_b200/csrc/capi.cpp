@@ -440,6 +440,14 @@ spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int3
                            int32_t ctx, int32_t layer, const void* k_cache, const void* v_cache, const void* q,
                            int32_t n_req, const int32_t* req_slot, const int32_t* req_qlen, const int32_t* req_kvlen,
                            int32_t width, void* out) {
+  return spin_attention_ex(stream, n_heads, head_dim, layers, slots, ctx, layer, k_cache, v_cache, q, n_req, req_slot,
+                           req_qlen, req_kvlen, width, static_cast<float>(1.0 / std::sqrt(double(head_dim))), 1, out);
+}
+
+spin_status spin_attention_ex(void* stream, int32_t n_heads, int32_t head_dim, int32_t layers, int32_t slots,
+                              int32_t ctx, int32_t layer, const void* k_cache, const void* v_cache, const void* q,
+                              int32_t n_req, const int32_t* req_slot, const int32_t* req_qlen,
+                              const int32_t* req_kvlen, int32_t width, float scale, int32_t causal, void* out) {
   return guarded([&] {
     if (head_dim != 64 && head_dim != 128) fail(SPIN_INPUT_ERROR, "spin_attention: head_dim must be 64 or 128");
     if (n_req < 1 || n_req > 1024) fail(SPIN_INPUT_ERROR, "spin_attention: batch must be 1..1024 requests");
@@ -447,7 +455,8 @@ spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int3
     std::vector<int32_t> qstart(n_req);
     int T = 0;
     for (int i = 0; i < n_req; ++i) {
-      if (req_qlen[i] < 1 || req_qlen[i] > 17 || req_kvlen[i] < req_qlen[i] || req_kvlen[i] > ctx)
+      if (req_qlen[i] < 1 || req_qlen[i] > 17 || req_kvlen[i] < 1 || req_kvlen[i] > ctx ||
+          (causal && req_kvlen[i] < req_qlen[i]))
         fail(SPIN_INPUT_ERROR, "spin_attention: bad request shape");
       if (req_slot[i] < 0 || req_slot[i] >= slots) fail(SPIN_INPUT_ERROR, "spin_attention: slot out of range");
       qstart[i] = T;
@@ -491,7 +500,8 @@ spin_status spin_attention(void* stream, int32_t n_heads, int32_t head_dim, int3
     bf16* vs = static_cast<bf16*>(dal((kv_rows + 16) * head_dim * 2));
     launch_swizzle_kv(static_cast<const bf16*>(k_cache), ks, kv_rows, head_dim, ctx, s);
     launch_swizzle_kv(static_cast<const bf16*>(v_cache), vs, kv_rows, head_dim, ctx, s);
-    AttnGeom g{n_heads, head_dim, slots, ctx, layer, static_cast<float>(1.0 / std::sqrt(double(head_dim))), ks, vs};
+    AttnGeom g{n_heads, head_dim, slots, ctx, layer, scale, ks, vs};
+    g.causal = causal != 0;
     CUtensorMap tk{}, tv{};  // unused by the bulk-copy attention
     launch_attention(tk, tv, m, rows, n_req, g, static_cast<const float*>(q), w, static_cast<bf16*>(out), s);
     check_cuda(cudaGetLastError(), "attention launch");

@@ -95,6 +95,7 @@ struct AttnGeom {
   float scale;
   bf16* k_cache;  // [layers][slots][heads][ctx][hd], rows swizzled by kv_swz (+16 padding rows at the end)
   bf16* v_cache;
+  int causal = 1;  // 0: every query sees all of its request's keys (the reference's toy mode, attention.cpp:67-96)
 };
 
 void launch_meta(const MetaArgs& a, const SlotState& st, const FwdMeta& m, cudaStream_t s);
