@@ -43,6 +43,7 @@ constexpr int kThreads = 32 * kNW;
 #endif
 constexpr int kVW = SPIN_ATTN_VW;
 constexpr int kMaxPieces = 16;           // piece records staged per warp per pass
+constexpr int kDecStages = 2;            // few-query ring depth per warp (launch_decode)
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
@@ -83,10 +84,10 @@ __device__ __forceinline__ uint32_t kvoff(int row, int chunk, int base) {
   return static_cast<uint32_t>(row * (HD * 2) + (chunk >> 3) * 128 + (((chunk & 7) ^ ((row + base) & 7)) << 4));
 }
 
-template <int HD, int NQT, int NW = kNW>
+template <int HD, int NQT, int NW = kNW, int ST = 0>
 struct Cfg {
   static constexpr int kWarps = NW;
-  static constexpr int kStages = HD == 128 ? 3 : 4;     // per-warp ring depth
+  static constexpr int kStages = ST > 0 ? ST : (HD == 128 ? 3 : 4);  // per-warp ring depth
   static constexpr uint32_t kHalf = 16 * HD * 2;        // K or V of one 16-key tile
   static constexpr uint32_t kStage = 2 * kHalf;
   static constexpr uint32_t kRing = NW * kStages * kStage;
@@ -790,9 +791,9 @@ __global__ void __launch_bounds__(64) attn_ws_kernel(FwdMeta m, AttnGeom g, cons
 // warps' partials of each piece are merged in shared memory (fixed warp order), and
 // pieces of multi-piece requests go through the same global last-arriver merge as
 // attn_kernel. NQT = 1 (<= 8 queries per request).
-template <int HD>
+template <int HD, int ST>
 struct DecCfg {
-  using C = Cfg<HD, 1>;
+  using C = Cfg<HD, 1, kNW, ST>;
   static constexpr int kQ = kDecodeQ;                // queries per request (<= 2)
   static constexpr int kMergeFloats = kQ * (2 + HD);  // per slot: m[kQ], l[kQ], o[kQ][HD]
   static constexpr int kCluster = 2;                 // CTAs per item (tiles round robin over 2 x 4 warps)
@@ -800,11 +801,11 @@ struct DecCfg {
                                    (kNW + kCluster) * kMergeFloats * 4;  // warp slots + cluster receive slots
 };
 
-template <int HD>
+template <int HD, int ST>
 __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGeom g, const float* __restrict__ q,
                                                                AttnWork w, bf16* __restrict__ out, int n_items) {
-  using C = Cfg<HD, 1>;
-  using DC = DecCfg<HD>;
+  using DC = DecCfg<HD, ST>;
+  using C = typename DC::C;
   constexpr int CS = DC::kCluster;
   constexpr int S = C::kStages, DT = C::kDT, NR = C::kNR, QP = C::kQP;
   extern __shared__ uint8_t smem_raw[];
@@ -1075,11 +1076,11 @@ __global__ void __launch_bounds__(kThreads) attn_decode_kernel(FwdMeta m, AttnGe
 
 }
 
-template <int HD>
-void launch_decode(const FwdMeta& m, int n_rows, const AttnGeom& g, const float* q, const AttnWork& w, bf16* out,
-                   cudaStream_t s) {
-  using DC = DecCfg<HD>;
-  ensure_smem_optin(reinterpret_cast<const void*>(attn_decode_kernel<HD>), DC::kTotal);
+template <int HD, int ST>
+void launch_decode_st(const FwdMeta& m, int n_rows, const AttnGeom& g, const float* q, const AttnWork& w, bf16* out,
+                      cudaStream_t s) {
+  using DC = DecCfg<HD, ST>;
+  ensure_smem_optin(reinterpret_cast<const void*>(attn_decode_kernel<HD, ST>), DC::kTotal);
   const int n_items = n_rows * std::max(1, w.chunks);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -1099,7 +1100,22 @@ void launch_decode(const FwdMeta& m, int n_rows, const AttnGeom& g, const float*
   cfg.gridDim = dim3(n_items * g.n_heads * DC::kCluster);  // one cluster per (row, chunk, head)
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = DC::kTotal;
-  cudaLaunchKernelEx(&cfg, attn_decode_kernel<HD>, m, g, q, w, out, n_items);
+  cudaLaunchKernelEx(&cfg, attn_decode_kernel<HD, ST>, m, g, q, w, out, n_items);
+}
+
+// Ring depth of the few-query kernel: a draft-step item is a whole (request, head) over
+// 2 x 4 warps, a few 16-key tiles per warp, so a shallow ring keeps the CTA small enough
+// for every item of a launch to be resident at once (one wave).
+template <int HD>
+void launch_decode(const FwdMeta& m, int n_rows, const AttnGeom& g, const float* q, const AttnWork& w, bf16* out,
+                   cudaStream_t s) {
+  static const int st = [] {
+    const char* e = std::getenv("SPIN_ATTN_DEC_STAGES");  // tuning
+    return e ? std::atoi(e) : kDecStages;
+  }();
+  if (st <= 2) return launch_decode_st<HD, 2>(m, n_rows, g, q, w, out, s);
+  if (st == 3) return launch_decode_st<HD, 3>(m, n_rows, g, q, w, out, s);
+  return launch_decode_st<HD, 4>(m, n_rows, g, q, w, out, s);
 }
 
 template <int HD, int NQT>

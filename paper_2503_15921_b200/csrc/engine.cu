@@ -314,7 +314,8 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     prof_end(s, gemm_bytes(3 * D, D));
     if (!(skip & 1)) {
       prof_begin(base + 3, s);
-      launch_qkv_epilogue(ln.part, pq.map, ln.meta, T, g, m.rcos, m.rsin, ln.q, s);
+      launch_qkv_epilogue(ln.part, pq.map, ln.meta, T, g, m.rcos, m.rsin, ln.q, s,
+                          stamp_layer ? stamp_slot(16, qkv_epilogue_blocks(T, m.H * m.hd)) : nullptr);
       prof_end(s, 0);
     }
     prof_begin(base + 2, s);
@@ -329,7 +330,7 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     prof_end(s, gemm_bytes(D, D));
     if (!(skip & 2)) {
       prof_begin(base + 3, s);
-      launch_resid_norm(ln.part, po.map, T, D, eps, ln.h, ln.xn, s);
+      launch_resid_norm(ln.part, po.map, T, D, eps, ln.h, ln.xn, s, stamp_layer ? stamp_slot(17, T) : nullptr);
       prof_end(s, 0);
     }
     const GemmPlan& pg = plan(2 * F, D, T, kGemmPartial);
@@ -339,7 +340,7 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     prof_end(s, gemm_bytes(2 * F, D));
     if (!(skip & 4)) {
       prof_begin(base + 3, s);
-      launch_swiglu(ln.part, pg.map, T, F, ln.act, s);
+      launch_swiglu(ln.part, pg.map, T, F, ln.act, s, stamp_layer ? stamp_slot(18, swiglu_blocks(T, F)) : nullptr);
       prof_end(s, 0);
     }
     const GemmPlan& pd = plan(D, F, T, kGemmPartial);
@@ -350,7 +351,7 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     prof_end(s, gemm_bytes(D, F));
     if (!(skip & 2)) {
       prof_begin(base + 3, s);
-      launch_resid_norm(ln.part, pd.map, T, D, eps, ln.h, ln.xn, s);
+      launch_resid_norm(ln.part, pd.map, T, D, eps, ln.h, ln.xn, s, stamp_layer ? stamp_slot(19, T) : nullptr);
       prof_end(s, 0);
     }
   }

@@ -2,6 +2,7 @@
 // embedding/RMSNorm, split-K reductions fused with RoPE + KV append, residual +
 // RMSNorm and SwiGLU, greedy acceptance with KV rollback, synthetic weights,
 // and the fp64 toy-mode packed attention operator.
+#include <algorithm>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -18,6 +19,12 @@ constexpr unsigned kFull = 0xffffffffu;
 // The first kUnrollPieces partial loads are predicated rather than looped so that a
 // caller summing several groups has all of their loads in flight at once.
 constexpr int kUnrollPieces = 2;
+
+// SPIN_STAMPS: per-block globaltimer stamps (start, dependency released, -, end) of the
+// epilogue kernels of target layer 1 (engine.cu stamp_slot kinds 16-18)
+__device__ __forceinline__ void stamp(unsigned long long* st, int j) {
+  if (st != nullptr && threadIdx.x == 0) st[4 * (blockIdx.y * gridDim.x + blockIdx.x) + j] = ptx::globaltimer();
+}
 __device__ __forceinline__ float4 sum_pieces4(const float* __restrict__ part, const PieceMap& pm, int T, int n_out,
                                               int t, int n) {
   const int np = pm.tile_pieces(t, n);
@@ -44,6 +51,50 @@ __device__ __forceinline__ float4 sum_pieces4(const float* __restrict__ part, co
     acc.w = __fadd_rn(acc.w, w.w);
   }
   return acc;
+}
+
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+
+// sum_pieces4 split in two so that a kernel looks its piece counts up BEFORE the PDL
+// dependency wait (the table is constant) and issues every slot load right after it:
+// set() (pre-wait), issue() (post-wait), sum() -- same fixed slot order as sum_pieces4.
+struct Pieces4 {
+  const float* p;
+  int np;
+  float4 v[kUnrollPieces];
+  __device__ __forceinline__ void set(const float* part, const PieceMap& pm, int T, int n_out, int t, int n) {
+    np = pm.tile_pieces(t, n);
+    p = part + static_cast<size_t>(t) * n_out + n;
+  }
+  __device__ __forceinline__ void issue(size_t stride) {
+#pragma unroll
+    for (int s = 0; s < kUnrollPieces; ++s)
+      if (s < np) v[s] = __ldg(reinterpret_cast<const float4*>(p + s * stride));
+  }
+  __device__ __forceinline__ float4 sum(size_t stride) const {
+    float4 acc = v[0];
+#pragma unroll
+    for (int s = 1; s < kUnrollPieces; ++s)
+      if (s < np) acc = add4(acc, v[s]);
+    for (int s = kUnrollPieces; s < np; ++s) acc = add4(acc, __ldg(reinterpret_cast<const float4*>(p + s * stride)));
+    return acc;
+  }
+};
+
+// SMs of the current device (grid sizing of the one-wave epilogue kernels).
+int device_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n;
+  }
+  return cache[dev];
 }
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
@@ -407,10 +458,9 @@ __global__ void __launch_bounds__(kRowThreads) embed_norm_kernel(const bf16* __r
 template <int NV, int PB>
 __global__ void __launch_bounds__(kRowThreads, 2) resid_norm_kernel(const float* __restrict__ part, PieceMap pm, int T,
                                                                  int D, float eps, float* __restrict__ h,
-                                                                 bf16* __restrict__ xn) {
+                                                                 bf16* __restrict__ xn, unsigned long long* st) {
   __shared__ float red[32];
-  ptx::grid_dep_wait();
-  ptx::grid_dep_launch();  // dependents (the next GEMM) may start their weight prefetch now
+  stamp(st, 0);
   const int t = blockIdx.x;
   const size_t stride = static_cast<size_t>(T) * D;
   const float* prow = part + static_cast<size_t>(t) * D;
@@ -418,15 +468,23 @@ __global__ void __launch_bounds__(kRowThreads, 2) resid_norm_kernel(const float*
   float4 v[NV], y[NV];
   int np[NV];
   int maxp = 0;
+  // Before the dependency wait: the piece counts (constant table) and the residual row
+  // (last written by the previous residual kernel, two launches back: final once the
+  // projection that precedes us has passed its own wait and triggered).
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const int i = 4 * (threadIdx.x + k * kRowThreads);
     np[k] = i < D ? pm.tile_pieces(t, i) : 0;
     maxp = max(maxp, np[k]);
-    if (i < D) {
-      v[k] = hrow[i >> 2];
-      y[k] = __ldg(reinterpret_cast<const float4*>(prow + i));
-    }
+    if (i < D) v[k] = __ldcg(hrow + (i >> 2));
+  }
+  ptx::grid_dep_wait();
+  ptx::grid_dep_launch();  // dependents (the next GEMM) may start their weight prefetch now
+  stamp(st, 1);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int i = 4 * (threadIdx.x + k * kRowThreads);
+    if (i < D) y[k] = __ldg(reinterpret_cast<const float4*>(prow + i));
   }
   for (int s0 = 1; s0 < maxp; s0 += PB) {
     float4 z[PB][NV];
@@ -467,71 +525,114 @@ __global__ void __launch_bounds__(kRowThreads, 2) resid_norm_kernel(const float*
     u.y = *reinterpret_cast<uint32_t*>(&b);
     *reinterpret_cast<uint2*>(xrow + 4 * (threadIdx.x + k * kRowThreads)) = u;
   }
+  stamp(st, 3);
 }
 
-// grid (T, ceil(F / 1024)): 4 SwiGLU outputs per thread.
-// grid (T, ceil(F / (4 * kSwiVec * 256))): kSwiVec groups of 4 SwiGLU outputs per thread
-// (1024 features apart). Measured: 4 groups per thread (one wave of fat threads) cost
-// 1.8x the time of 1 group per thread (several waves of short threads).
-constexpr int kSwiVec = 1;
-__global__ void __launch_bounds__(kRowThreads) swiglu_kernel(const float* __restrict__ part, PieceMap pm, int T, int F,
-                                                             bf16* act) {
+// SwiGLU of the gate|up split-K partials: one wave of 2 x SMs blocks (small enough that
+// the next GEMM's CTA stays co-resident and prefetches its weights meanwhile), each thread
+// kSwiG groups of 4 features per pass with every slot load of the pass in flight; the
+// first pass's piece counts are looked up before the dependency wait.
+constexpr int kSwiG = 2;
+__device__ __forceinline__ void swiglu_store(float4 g, float4 u, bf16* dst) {
+  const float gs[4] = {g.x, g.y, g.z, g.w}, us[4] = {u.x, u.y, u.z, u.w};
+  float r[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r[i] = __fmul_rn(__fdiv_rn(gs[i], __fadd_rn(1.0f, expf(-gs[i]))), us[i]);
+  __nv_bfloat162 a = __floats2bfloat162_rn(r[0], r[1]), b = __floats2bfloat162_rn(r[2], r[3]);
+  uint2 o;
+  o.x = *reinterpret_cast<uint32_t*>(&a);
+  o.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(dst) = o;
+}
+
+__global__ void __launch_bounds__(kRowThreads, 2) swiglu_kernel(const float* __restrict__ part, PieceMap pm, int T,
+                                                                int F, bf16* act, unsigned long long* st) {
+  stamp(st, 0);
+  const int per_row = F / 4;
+  const int items = T * per_row;
+  const int nthr = gridDim.x * blockDim.x;
+  const size_t stride = static_cast<size_t>(T) * 2 * F;
+  Pieces4 g[kSwiG], u[kSwiG];
+  int it0 = blockIdx.x * blockDim.x + threadIdx.x;
+  auto set = [&](int base) {
+#pragma unroll
+    for (int k = 0; k < kSwiG; ++k) {
+      const int it = base + k * nthr;
+      const int t = it / per_row, f = 4 * (it % per_row);
+      if (it < items) {
+        g[k].set(part, pm, T, 2 * F, t, f);
+        u[k].set(part, pm, T, 2 * F, t, F + f);
+      } else {
+        g[k].np = u[k].np = 0;
+      }
+    }
+  };
+  set(it0);
   ptx::grid_dep_wait();
   ptx::grid_dep_launch();  // dependents (the next GEMM) may start their weight prefetch now
-  const int t = blockIdx.x;
-  float4 g[kSwiVec], u[kSwiVec];
+  stamp(st, 1);
+  for (; it0 < items; it0 += kSwiG * nthr) {
+    if (it0 != static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x)) set(it0);
 #pragma unroll
-  for (int k = 0; k < kSwiVec; ++k) {
-    const int f = 4 * ((blockIdx.y * kSwiVec + k) * kRowThreads + threadIdx.x);
-    if (f < F) {
-      g[k] = sum_pieces4(part, pm, T, 2 * F, t, f);
-      u[k] = sum_pieces4(part, pm, T, 2 * F, t, F + f);
+    for (int k = 0; k < kSwiG; ++k) g[k].issue(stride), u[k].issue(stride);
+#pragma unroll
+    for (int k = 0; k < kSwiG; ++k) {
+      const int it = it0 + k * nthr;
+      if (it >= items) continue;
+      const int t = it / per_row, f = 4 * (it % per_row);
+      swiglu_store(g[k].sum(stride), u[k].sum(stride), act + static_cast<size_t>(t) * F + f);
     }
   }
-#pragma unroll
-  for (int k = 0; k < kSwiVec; ++k) {
-    const int f = 4 * ((blockIdx.y * kSwiVec + k) * kRowThreads + threadIdx.x);
-    if (f >= F) continue;
-    const float gs[4] = {g[k].x, g[k].y, g[k].z, g[k].w}, us[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
-    float r[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) r[i] = __fmul_rn(__fdiv_rn(gs[i], __fadd_rn(1.0f, expf(-gs[i]))), us[i]);
-    __nv_bfloat162 a = __floats2bfloat162_rn(r[0], r[1]), b = __floats2bfloat162_rn(r[2], r[3]);
-    uint2 o;
-    o.x = *reinterpret_cast<uint32_t*>(&a);
-    o.y = *reinterpret_cast<uint32_t*>(&b);
-    *reinterpret_cast<uint2*>(act + static_cast<size_t>(t) * F + f) = o;
-  }
+  stamp(st, 3);
 }
+
+// Split-K reduce of the QKV partials + RoPE on q and k + KV append: items of 4 rotary pairs
+// of one token (q, k, v sections: 12 partial float4 loads), grid-stride over one wave of
+// 2 x SMs blocks; the first item's row metadata, RoPE factors and piece counts are read
+// before the dependency wait.
+struct QkvItem {
+  int t, nq, hh, i, slot, pos;
+  float4 c, s;
+  Pieces4 pc[6];  // q lo, q hi, k lo, k hi, v lo, v hi
+};
 
 __global__ void __launch_bounds__(kRowThreads, 2) qkv_epilogue_kernel(const float* __restrict__ part, PieceMap pm,
                                                                    FwdMeta m, int T, AttnGeom g,
                                                                    const float* __restrict__ rcos,
-                                                                   const float* __restrict__ rsin, float* q) {
-  const int t = blockIdx.x;
+                                                                   const float* __restrict__ rsin, float* q,
+                                                                   unsigned long long* st) {
+  stamp(st, 0);
   const int H = g.n_heads, hd = g.head_dim, half = hd / 2, D = H * hd, N = 3 * D;
-  const int p4 = 4 * (blockIdx.y * kRowThreads + threadIdx.x);  // first of 4 rotary pairs
-  const bool active = p4 < H * half;
-  const int hh = p4 / half, i = p4 % half;
-  // The row metadata (meta_kernel, complete before the projection that precedes us
-  // triggered) and the RoPE tables are read before the dependency wait.
-  int slot = -1, pos = 0;
-  float4 c = make_float4(0.f, 0.f, 0.f, 0.f), s = c;
-  if (active) {
-    slot = m.row_slot[t], pos = m.row_pos[t];
-    c = *reinterpret_cast<const float4*>(rcos + static_cast<size_t>(pos) * half + i);
-    s = *reinterpret_cast<const float4*>(rsin + static_cast<size_t>(pos) * half + i);
-  }
+  const int per_row = H * half / 4;
+  const int items = T * per_row;
+  const size_t stride = static_cast<size_t>(T) * N;
+  QkvItem x;
+  auto set = [&](int it) {
+    x.t = it / per_row;
+    const int p4 = 4 * (it % per_row);
+    x.hh = p4 / half, x.i = p4 % half;
+    x.nq = x.hh * hd + x.i;
+    x.slot = m.row_slot[x.t], x.pos = m.row_pos[x.t];
+    x.c = *reinterpret_cast<const float4*>(rcos + static_cast<size_t>(x.pos) * half + x.i);
+    x.s = *reinterpret_cast<const float4*>(rsin + static_cast<size_t>(x.pos) * half + x.i);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) x.pc[j].set(part, pm, T, N, x.t, (j >> 1) * D + x.nq + (j & 1) * half);
+  };
+  int it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it < items) set(it);
   ptx::grid_dep_wait();
   ptx::grid_dep_launch();  // dependents (attention) may stage their work list now
-  if (active) {
-    const int nq = hh * hd + i;
-    const float4 q0 = sum_pieces4(part, pm, T, N, t, nq), q1 = sum_pieces4(part, pm, T, N, t, nq + half);
-    const float4 k0 = sum_pieces4(part, pm, T, N, t, D + nq), k1 = sum_pieces4(part, pm, T, N, t, D + nq + half);
-    const float4 v0 = sum_pieces4(part, pm, T, N, t, 2 * D + nq), v1 = sum_pieces4(part, pm, T, N, t, 2 * D + nq + half);
+  stamp(st, 1);
+  for (bool first = true; it < items; it += gridDim.x * blockDim.x, first = false) {
+    if (!first) set(it);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) x.pc[j].issue(stride);
+    const float4 q0 = x.pc[0].sum(stride), q1 = x.pc[1].sum(stride);
+    const float4 k0 = x.pc[2].sum(stride), k1 = x.pc[3].sum(stride);
+    const float4 v0 = x.pc[4].sum(stride), v1 = x.pc[5].sum(stride);
     const float qa[4] = {q0.x, q0.y, q0.z, q0.w}, qb[4] = {q1.x, q1.y, q1.z, q1.w};
     const float ka[4] = {k0.x, k0.y, k0.z, k0.w}, kb[4] = {k1.x, k1.y, k1.z, k1.w};
-    const float cs[4] = {c.x, c.y, c.z, c.w}, sn[4] = {s.x, s.y, s.z, s.w};
+    const float cs[4] = {x.c.x, x.c.y, x.c.z, x.c.w}, sn[4] = {x.s.x, x.s.y, x.s.z, x.s.w};
     float qo0[4], qo1[4], ko0[4], ko1[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -540,25 +641,26 @@ __global__ void __launch_bounds__(kRowThreads, 2) qkv_epilogue_kernel(const floa
       ko0[e] = __fsub_rn(__fmul_rn(ka[e], cs[e]), __fmul_rn(kb[e], sn[e]));
       ko1[e] = __fadd_rn(__fmul_rn(kb[e], cs[e]), __fmul_rn(ka[e], sn[e]));
     }
-    float* qo = q + static_cast<size_t>(t) * D + nq;
+    float* qo = q + static_cast<size_t>(x.t) * D + x.nq;
     *reinterpret_cast<float4*>(qo) = make_float4(qo0[0], qo0[1], qo0[2], qo0[3]);
     *reinterpret_cast<float4*>(qo + half) = make_float4(qo1[0], qo1[1], qo1[2], qo1[3]);
-    if (slot >= 0) {
-      const size_t kv = ((((static_cast<size_t>(g.layer) * g.slots + slot) * H + hh) * g.ctx) + pos) * hd;
+    if (x.slot >= 0) {
+      const size_t kv = ((((static_cast<size_t>(g.layer) * g.slots + x.slot) * H + x.hh) * g.ctx) + x.pos) * hd;
       auto put4 = [](bf16* dst, float a, float b, float c2, float d) {
-        __nv_bfloat162 x = __floats2bfloat162_rn(a, b), y = __floats2bfloat162_rn(c2, d);
-        uint2 u;
-        u.x = *reinterpret_cast<uint32_t*>(&x);
-        u.y = *reinterpret_cast<uint32_t*>(&y);
-        *reinterpret_cast<uint2*>(dst) = u;
+        __nv_bfloat162 u = __floats2bfloat162_rn(a, b), w = __floats2bfloat162_rn(c2, d);
+        uint2 o;
+        o.x = *reinterpret_cast<uint32_t*>(&u);
+        o.y = *reinterpret_cast<uint32_t*>(&w);
+        *reinterpret_cast<uint2*>(dst) = o;
       };
       // 4 consecutive dims stay inside one 16-B chunk: swizzle the chunk (kv_swz)
-      put4(g.k_cache + kv + kv_swz(pos, i), ko0[0], ko0[1], ko0[2], ko0[3]);
-      put4(g.k_cache + kv + kv_swz(pos, i + half), ko1[0], ko1[1], ko1[2], ko1[3]);
-      put4(g.v_cache + kv + kv_swz(pos, i), v0.x, v0.y, v0.z, v0.w);
-      put4(g.v_cache + kv + kv_swz(pos, i + half), v1.x, v1.y, v1.z, v1.w);
+      put4(g.k_cache + kv + kv_swz(x.pos, x.i), ko0[0], ko0[1], ko0[2], ko0[3]);
+      put4(g.k_cache + kv + kv_swz(x.pos, x.i + half), ko1[0], ko1[1], ko1[2], ko1[3]);
+      put4(g.v_cache + kv + kv_swz(x.pos, x.i), v0.x, v0.y, v0.z, v0.w);
+      put4(g.v_cache + kv + kv_swz(x.pos, x.i + half), v1.x, v1.y, v1.z, v1.w);
     }
   }
+  stamp(st, 3);
 }
 
 // ------------------------------------------------------------------ accept
@@ -782,24 +884,32 @@ void launch_embed_norm(const bf16* emb, const FwdMeta& m, int T, int D, float ep
              static_cast<const int32_t*>(m.row_tok), D, eps, h, xn);
 }
 
+int qkv_epilogue_blocks(int T, int D) {
+  return std::min((T * (D / 8) + kRowThreads - 1) / kRowThreads, 2 * device_sms());
+}
+
+int swiglu_blocks(int T, int F) {
+  return std::min((T * (F / 4) + kSwiG * kRowThreads - 1) / (kSwiG * kRowThreads), 2 * device_sms());
+}
+
 void launch_qkv_epilogue(const float* part, const PieceMap& pm, const FwdMeta& m, int T, const AttnGeom& g,
-                         const float* rcos, const float* rsin, float* q, cudaStream_t s) {
-  const int pairs = g.n_heads * g.head_dim / 2;
-  launch_pdl(qkv_epilogue_kernel, dim3(T, (pairs + 4 * kRowThreads - 1) / (4 * kRowThreads)), dim3(kRowThreads), 0, s,
-             part, pm, m, T, g, rcos, rsin, q);
+                         const float* rcos, const float* rsin, float* q, cudaStream_t s, unsigned long long* st) {
+  const int blocks = qkv_epilogue_blocks(T, g.n_heads * g.head_dim);
+  launch_pdl(qkv_epilogue_kernel, dim3(blocks), dim3(kRowThreads), 0, s, part, pm, m, T, g, rcos, rsin, q, st);
 }
 
 void launch_resid_norm(const float* part, const PieceMap& pm, int T, int D, float eps, float* h, bf16* xn,
-                       cudaStream_t s) {
+                       cudaStream_t s, unsigned long long* st) {
   if (D <= 4 * 4 * kRowThreads)
-    launch_pdl(resid_norm_kernel<4, 4>, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, D, eps, h, xn);
+    launch_pdl(resid_norm_kernel<4, 4>, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, D, eps, h, xn, st);
   else
-    launch_pdl(resid_norm_kernel<8, 1>, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, D, eps, h, xn);
+    launch_pdl(resid_norm_kernel<8, 1>, dim3(T), dim3(kRowThreads), 0, s, part, pm, T, D, eps, h, xn, st);
 }
 
-void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* act, cudaStream_t s) {
-  const int per_block = 4 * kSwiVec * kRowThreads;
-  launch_pdl(swiglu_kernel, dim3(T, (F + per_block - 1) / per_block), dim3(kRowThreads), 0, s, part, pm, T, F, act);
+void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* act, cudaStream_t s,
+                   unsigned long long* st) {
+  const int blocks = swiglu_blocks(T, F);
+  launch_pdl(swiglu_kernel, dim3(blocks), dim3(kRowThreads), 0, s, part, pm, T, F, act, st);
 }
 
 void launch_accept(const FwdMeta& m, int n_req, int window, const int32_t* list, const int32_t* ssm_of_req,

@@ -101,11 +101,16 @@ struct AttnGeom {
 void launch_meta(const MetaArgs& a, const SlotState& st, const FwdMeta& m, cudaStream_t s);
 void launch_embed_norm(const bf16* emb, const FwdMeta& m, int T, int D, float eps, float* h, bf16* xn,
                        cudaStream_t s);
+// one-wave grids of the epilogue kernels (SPIN_STAMPS slot sizes)
+int qkv_epilogue_blocks(int T, int D);
+int swiglu_blocks(int T, int F);
 void launch_qkv_epilogue(const float* part, const PieceMap& pm, const FwdMeta& m, int T, const AttnGeom& g,
-                         const float* rcos, const float* rsin, float* q, cudaStream_t s);
+                         const float* rcos, const float* rsin, float* q, cudaStream_t s,
+                         unsigned long long* st = nullptr);
 void launch_resid_norm(const float* part, const PieceMap& pm, int T, int D, float eps, float* h, bf16* xn,
-                       cudaStream_t s);
-void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* act, cudaStream_t s);
+                       cudaStream_t s, unsigned long long* st = nullptr);
+void launch_swiglu(const float* part, const PieceMap& pm, int T, int F, bf16* act, cudaStream_t s,
+                   unsigned long long* st = nullptr);
 
 // Fused projections of the draft step (draft.cu): one CTA per 16/32 output rows over
 // the full K, epilogue in the projection, RMSNorm folded into the consumers through

@@ -5,7 +5,7 @@ from collections import defaultdict
 
 import numpy as np
 
-KIND = {0: "qkv", 1: "attn", 2: "o", 3: "gate_up", 4: "down"}
+KIND = defaultdict(lambda: "?", {0: "qkv", 1: "attn", 2: "o", 3: "gate_up", 4: "down", 10: "T.qkv", 11: "T.o", 12: "T.gu", 13: "T.down", 14: "T.attn", 15: "lm_head", 16: "T.qkvepi", 17: "T.rn_o", 18: "T.swiglu", 19: "T.rn_dn"})
 rows = defaultdict(list)
 kinds = {}
 with open(sys.argv[1]) as f:
