@@ -351,6 +351,12 @@ spin_status spin_gemm_info(int32_t n_out, int32_t k, int32_t t, int32_t mode, in
  * mode 1: amax_val/amax_idx [ceil(n_out/128)][t], logits [t][n_out] optional. Synchronous. */
 spin_status spin_gemm(void* stream, const void* w, const void* x, int32_t n_out, int32_t k, int32_t t,
                       int32_t mode, float* part, float* amax_val, int32_t* amax_idx, float* logits);
+/* Device time of the projection GEMM alone: seeded synthetic weights (tiled layout) and
+ * tokens allocated internally, `iters` back-to-back launches of the production plan
+ * (PDL, one CUDA graph) timed with CUDA events after one warm replay; *us_per_launch =
+ * graph time / iters. mode as spin_gemm. Synchronous; for probes and the bench. */
+spin_status spin_gemm_bench(int32_t n_out, int32_t k, int32_t t, int32_t mode, int32_t iters,
+                            double* us_per_launch);
 
 /* Packed ragged causal attention over a KV cache [layers][slots][heads][ctx][hd]
  * (bf16, device). q: [sum(qlen)][heads*hd] fp32 rows, request i owning qlen[i]

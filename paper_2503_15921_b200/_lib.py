@@ -145,6 +145,7 @@ _SIGNATURES = {
     "spin_last_round_trace": [C.c_void_p, P_F32, C.c_int32],
     "spin_verify_bench": [C.c_void_p, C.c_int32, P_I32, P_I32, P_I32, C.c_int32, C.c_int32, C.c_void_p],
     "spin_gemm_info": [C.c_int32, C.c_int32, C.c_int32, C.c_int32, P_I32, P_I32, P_I32],
+    "spin_gemm_bench": [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)],
     "spin_pack_device": [P_I32, C.c_int32, C.c_int32, P_I32, P_I32, C.POINTER(Segment), C.c_int32, P_I32, P_I64,
                          P_I32],
     "spin_device_count": [P_I32],

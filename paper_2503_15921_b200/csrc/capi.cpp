@@ -155,6 +155,66 @@ spin_status spin_gemm(void* stream, const void* w, const void* x, int32_t n_out,
 }
 
 
+spin_status spin_gemm_bench(int32_t n_out, int32_t k, int32_t t, int32_t mode, int32_t iters,
+                            double* us_per_launch) {
+  return guarded([&] {
+    if (n_out < 1 || k < 1 || t < 1 || iters < 1) fail(SPIN_INPUT_ERROR, "spin_gemm_bench: empty shape");
+    if (k % 8 != 0) fail(SPIN_INPUT_ERROR, "spin_gemm_bench: K must be a multiple of 8 (16-B rows)");
+    if (us_per_launch == nullptr) fail(SPIN_INPUT_ERROR, "spin_gemm_bench: null output");
+    const GemmPlan p = gemm_plan(n_out, k, t, mode, num_sms_cached());
+    bf16 *w = nullptr, *x = nullptr;
+    float *out = nullptr, *logits = nullptr;
+    int32_t* idx = nullptr;
+    const size_t out_elems = mode == kGemmPartial ? static_cast<size_t>(p.max_pieces) * t * n_out
+                                                  : static_cast<size_t>(p.n_mtiles) * t;
+    cudaStream_t st = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    auto cleanup = [&] {
+      if (ge) cudaGraphExecDestroy(ge);
+      if (g) cudaGraphDestroy(g);
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+      if (st) cudaStreamDestroy(st);
+      cudaFree(w), cudaFree(x), cudaFree(out), cudaFree(idx), cudaFree(logits);
+    };
+    try {
+      check_cuda(cudaMalloc(&w, tiled_weight_elems(n_out, k) * 2), "malloc");
+      check_cuda(cudaMalloc(&x, static_cast<size_t>(t) * k * 2), "malloc");
+      check_cuda(cudaMalloc(&out, out_elems * 4), "malloc");
+      check_cuda(cudaMalloc(&idx, out_elems * 4), "malloc");
+      check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+      // tiled layout of seeded weights is still a weight matrix (values do not matter for timing)
+      launch_init_weights(w, n_out, k, 0x5350494eull, 0.05f, nullptr, 0.f, 0, 0, 0, 1, st);
+      launch_init_weights(x, t, k, 0x58ull, 1.f, nullptr, 0.f, 0, 0, 0, 0, st);
+      GemmEpilogue e;
+      e.mode = mode;
+      e.part = out;
+      e.amax_val = out;
+      e.amax_idx = idx;
+      check_cuda(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+      for (int i = 0; i < iters; ++i) check_cuda(gemm_launch(p, w, x, e, st, true), "gemm launch");
+      check_cuda(cudaStreamEndCapture(st, &g), "capture");
+      check_cuda(cudaGraphInstantiate(&ge, g, 0), "instantiate");
+      check_cuda(cudaEventCreate(&a), "event");
+      check_cuda(cudaEventCreate(&b), "event");
+      check_cuda(cudaGraphLaunch(ge, st), "graph");
+      check_cuda(cudaEventRecord(a, st), "event");
+      check_cuda(cudaGraphLaunch(ge, st), "graph");
+      check_cuda(cudaEventRecord(b, st), "event");
+      check_cuda(cudaEventSynchronize(b), "gemm bench");
+      float ms = 0.f;
+      check_cuda(cudaEventElapsedTime(&ms, a, b), "event");
+      *us_per_launch = 1e3 * ms / iters;
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
 // ---------------------------------------------------------------- attention operator
 spin_status spin_reference_attention(int32_t q_rows, int32_t kv_rows, int32_t dim, const double* q, const double* k,
                                      const double* v, double* out) {

@@ -43,9 +43,13 @@ struct PieceIter {
   int next_tile;       // round-robin tile (ARGMAX)
   int grp, my_nt;      // grouped stream-K: this CTA's group and token tile
 
+  int rank;            // CTA pairs: this CTA's weight tile within the pair's super tile
+
   __device__ void init(const PieceMap& pm, int n_tiles) {
-    grp = pm.ntg > 1 ? static_cast<int>(blockIdx.x) / pm.ntg : static_cast<int>(blockIdx.x);
-    my_nt = pm.ntg > 1 ? static_cast<int>(blockIdx.x) % pm.ntg : 0;
+    const int id = static_cast<int>(blockIdx.x) / pm.pair;  // both CTAs of a pair: same schedule
+    rank = static_cast<int>(blockIdx.x) % pm.pair;
+    grp = pm.ntg > 1 ? id / pm.ntg : id;
+    my_nt = pm.ntg > 1 ? id % pm.ntg : 0;
     const long long c = grp;
     u = c * pm.units / pm.grid;
     u_end = (c + 1) * pm.units / pm.grid;
@@ -55,8 +59,13 @@ struct PieceIter {
   __device__ bool next(const PieceMap& pm, int n_tiles, Piece& p) {
     if (pm.mode == kGemmPartial) {
       if (u >= u_end) return false;
-      const int t = static_cast<int>(u / pm.kb);  // tile, or weight tile when grouped
-      p.tile = pm.ntg > 1 ? t * pm.n_ntiles + my_nt : t;
+      const int t = static_cast<int>(u / pm.kb);  // tile, or weight tile when grouped (super tiles when paired)
+      if (pm.pair == 1) {
+        p.tile = pm.ntg > 1 ? t * pm.n_ntiles + my_nt : t;
+      } else {
+        const int smt = pm.ntg > 1 ? t : t / pm.n_ntiles, nt = pm.ntg > 1 ? my_nt : t % pm.n_ntiles;
+        p.tile = (smt * pm.pair + rank) * pm.n_ntiles + nt;
+      }
       p.kb0 = static_cast<int>(u % pm.kb);
       const long long left = u_end - u;
       p.kb1 = static_cast<int>((p.kb0 + left < pm.kb) ? p.kb0 + left : pm.kb);
@@ -81,16 +90,25 @@ __device__ __forceinline__ void argmax_merge(float& v, int& i, float ov, int oi)
   }
 }
 
+// P2 = CTA pair (cta_group::2): the two CTAs of a cluster own the weight tiles 2s and 2s + 1
+// of a 256-row super tile; the leader issues one tcgen05.mma M = 256 per k step that reads
+// A from both CTAs (128 rows each) and the token tile B split across them (bn / 2 tokens
+// each), and writes each CTA's 128 x bn accumulator into that CTA's TMEM. Every SM then
+// ingests 16 KB of weights + bn * 64 B of tokens per stage instead of 16 KB + bn * 128 B:
+// the single-CTA k-loop was bound by the L2 -> SM operand stream at T > 256.
+template <bool P2>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __nv_bfloat16* __restrict__ w_tiled, const __grid_constant__ CUtensorMap tm_x,
-                   const __grid_constant__ CUtensorMap tm_part, PieceMap pm, GemmEpilogue epi, int n_out, int t_total,
-                   int stages) {
+                   const __grid_constant__ CUtensorMap tm_part, const __grid_constant__ CUtensorMap tm_w, PieceMap pm,
+                   GemmEpilogue epi, int n_out, int t_total, int stages) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
 
   const int bn = pm.bn;
-  const uint32_t tile_b_bytes = static_cast<uint32_t>(bn) * kBlockK * 2;
+  // token rows held (and loaded) per CTA and stage: all bn, or this CTA's half in a pair
+  const int bn_cta = P2 ? bn / 2 : bn;
+  const uint32_t tile_b_bytes = static_cast<uint32_t>(bn_cta) * kBlockK * 2;
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + static_cast<size_t>(stages) * kTileABytes;
   uint8_t* smem_red = smem_b + static_cast<size_t>(stages) * tile_b_bytes;  // ARGMAX scratch | PARTIAL staging
@@ -104,6 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const bool leader = !P2 || (blockIdx.x & 1) == 0;  // cluster rank 0 issues the pair's MMAs
   // stamps [CTA][8]: start, producer wait release, first stage ready (MMA), last MMA issued,
   // first epilogue start, last epilogue done, end
   unsigned long long* st = epi.st ? epi.st + 8 * blockIdx.x : nullptr;
@@ -112,7 +131,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(2 * bn)) tmem_cols <<= 1;
 
-  if (warp == 0 && lane == 0) ptx::tma_prefetch_desc(&tm_x);
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_x);
+    if (P2) ptx::tma_prefetch_desc(&tm_w);
+  }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
@@ -120,13 +142,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull_bar[s], 1);
-      ptx::mbar_init(&tempty_bar[s], 4);
+      ptx::mbar_init(&tempty_bar[s], P2 ? 8 : 4);  // pair: both CTAs' epilogue warps drain the leader's MMA
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_slot, tmem_cols);
+  if (warp == 2) {
+    if (P2)
+      ptx::tmem_alloc_2sm(tmem_slot, tmem_cols);
+    else
+      ptx::tmem_alloc(tmem_slot, tmem_cols);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (P2) {  // the peer signals our barriers and its MMAs write our TMEM
+    ptx::cluster_arrive();
+    ptx::cluster_wait();
+  } else {
+    __syncthreads();
+  }
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -136,12 +168,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       // weights stream through once (evict-first), unless sibling CTAs of a group re-read them
       const uint64_t pol_w = pm.ntg > 1 ? ptx::policy_evict_last() : ptx::policy_evict_first();
       const uint64_t pol_x = ptx::policy_evict_last();   // activations are re-read by every CTA
+      // every stage completes on the leader's full barrier (pair: both CTAs' loads)
+      const uint32_t stage_bytes = (kTileABytes + tile_b_bytes) * (P2 ? 2 : 1);
+      auto load_a = [&](int s, int mt, int kb) {
+        if (P2)
+          ptx::tma_load_2d_2sm(smem_a + static_cast<size_t>(s) * kTileABytes, &tm_w,
+                               ptx::mapa(ptx::smem_u32(&full_bar[s]), 0), 0, (mt * pm.kb + kb) * kBlockM, pol_w);
+        else
+          ptx::bulk_load(smem_a + static_cast<size_t>(s) * kTileABytes,
+                         w_tiled + (static_cast<size_t>(mt) * pm.kb + kb) * (kBlockM * kBlockK), kTileABytes,
+                         &full_bar[s], pol_w);
+      };
       PieceIter it;
       it.init(pm, n_tiles);
       Piece p;
       int stage = 0;
       uint32_t phase = 0;
-      bool waited = false;
       int prefetched = 0;  // stages whose W half was issued before the dependency wait
       // Issue the weight halves of the first stages before waiting on the
       // producer kernel (PDL): weights never depend on the previous kernel.
@@ -152,16 +194,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (s < stages && pre.next(pm, n_tiles, q)) {
           const int mt = q.tile / pm.n_ntiles;
           for (int kb = q.kb0; kb < q.kb1 && s < stages; ++kb, ++s) {
-            ptx::mbar_arrive_expect_tx(&full_bar[s], kTileABytes + tile_b_bytes);
-            ptx::bulk_load(smem_a + static_cast<size_t>(s) * kTileABytes,
-                           w_tiled + (static_cast<size_t>(mt) * pm.kb + kb) * (kBlockM * kBlockK), kTileABytes,
-                           &full_bar[s], pol_w);
+            if (leader) ptx::mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+            load_a(s, mt, kb);
           }
         }
         prefetched = s;
       }
       ptx::grid_dep_wait();
-      waited = true;
       if (st) st[1] = ptx::globaltimer();
       int issued = 0;
       while (it.next(pm, n_tiles, p)) {
@@ -170,13 +209,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = p.kb0; kb < p.kb1; ++kb) {
           if (issued >= prefetched) {
             ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-            ptx::mbar_arrive_expect_tx(&full_bar[stage], kTileABytes + tile_b_bytes);
-            ptx::bulk_load(smem_a + static_cast<size_t>(stage) * kTileABytes,
-                           w_tiled + (static_cast<size_t>(mt) * pm.kb + kb) * (kBlockM * kBlockK), kTileABytes,
-                           &full_bar[stage], pol_w);
+            if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
+            load_a(stage, mt, kb);
           }
-          ptx::tma_load_2d(smem_b + static_cast<size_t>(stage) * tile_b_bytes, &tm_x, &full_bar[stage],
-                           kb * kBlockK, nt * bn, pol_x);
+          if (P2)  // this CTA's half of the token tile
+            ptx::tma_load_2d_2sm(smem_b + static_cast<size_t>(stage) * tile_b_bytes, &tm_x,
+                                 ptx::mapa(ptx::smem_u32(&full_bar[stage]), 0), kb * kBlockK,
+                                 nt * bn + it.rank * bn_cta, pol_x);
+          else
+            ptx::tma_load_2d(smem_b + static_cast<size_t>(stage) * tile_b_bytes, &tm_x, &full_bar[stage],
+                             kb * kBlockK, nt * bn, pol_x);
           ++issued;
           if (++stage == stages) {
             stage = 0;
@@ -184,46 +226,72 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      (void)waited;
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc = ptx::idesc_bf16_m128(static_cast<uint32_t>(bn));
-    PieceIter it;
-    it.init(pm, n_tiles);
-    Piece p;
-    int stage = 0;
-    uint32_t phase = 0;
-    int iter = 0;
-    while (it.next(pm, n_tiles, p)) {
-      const int acc = iter & 1;
-      ptx::mbar_wait(&tempty_bar[acc], ((iter >> 1) & 1) ^ 1);
-      ptx::tc_fence_after();
-      const uint32_t d_addr = tmem_base + static_cast<uint32_t>(acc * bn);
-      for (int kb = p.kb0; kb < p.kb1; ++kb) {
-        ptx::mbar_wait(&full_bar[stage], phase);
-        ptx::tc_fence_after();
-        if (st && lane == 0 && iter == 0 && kb == p.kb0) st[2] = ptx::globaltimer();
-        if (lane == 0) {
-          const uint64_t da = ptx::smem_desc_sw128(smem_a + static_cast<size_t>(stage) * kTileABytes);
-          const uint64_t db = ptx::smem_desc_sw128(smem_b + static_cast<size_t>(stage) * tile_b_bytes);
-#pragma unroll
-          for (int k = 0; k < kBlockK / 16; ++k) {
-            // +32 bytes per 16-element K step inside the 128-B swizzle atom.
-            ptx::umma_bf16(d_addr, da + 2 * k, db + 2 * k, idesc, (kb > p.kb0 || k > 0) ? 1u : 0u);
+      if (P2) {
+        // producer tail: every stage released by the leader's MMAs, so none of its commits is
+        // still in flight towards our barriers when the CTAs leave
+        for (int i = 0; i < stages; ++i) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (++stage == stages) {
+            stage = 0;
+            phase ^= 1;
           }
-          ptx::umma_commit(&empty_bar[stage]);
-          if (kb + 1 == p.kb1) ptx::umma_commit(&tfull_bar[acc]);
-        }
-        __syncwarp();
-        if (++stage == stages) {
-          stage = 0;
-          phase ^= 1;
         }
       }
-      ++iter;
     }
-    if (st && lane == 0) st[3] = ptx::globaltimer();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (pair: leader only)
+    if (leader) {
+      const uint32_t idesc = ptx::idesc_bf16(P2 ? 256u : 128u, static_cast<uint32_t>(bn));
+      PieceIter it;
+      it.init(pm, n_tiles);
+      Piece p;
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      while (it.next(pm, n_tiles, p)) {
+        const int acc = iter & 1;
+        ptx::mbar_wait(&tempty_bar[acc], ((iter >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_addr = tmem_base + static_cast<uint32_t>(acc * bn);
+        for (int kb = p.kb0; kb < p.kb1; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          if (st && lane == 0 && iter == 0 && kb == p.kb0) st[2] = ptx::globaltimer();
+          if (lane == 0) {
+            const uint64_t da = ptx::smem_desc_sw128(smem_a + static_cast<size_t>(stage) * kTileABytes);
+            const uint64_t db = ptx::smem_desc_sw128(smem_b + static_cast<size_t>(stage) * tile_b_bytes);
+#pragma unroll
+            for (int k = 0; k < kBlockK / 16; ++k) {
+              // +32 bytes per 16-element K step inside the 128-B swizzle atom.
+              const uint32_t accum = (kb > p.kb0 || k > 0) ? 1u : 0u;
+              if (P2)
+                ptx::umma_bf16_2sm(d_addr, da + 2 * k, db + 2 * k, idesc, accum);
+              else
+                ptx::umma_bf16(d_addr, da + 2 * k, db + 2 * k, idesc, accum);
+            }
+            if (P2) {  // the stage spans both CTAs: release it in both; the accumulator is in both
+              ptx::umma_commit_2sm(&empty_bar[stage], 0x3);
+              if (kb + 1 == p.kb1) ptx::umma_commit_2sm(&tfull_bar[acc], 0x3);
+            } else {
+              ptx::umma_commit(&empty_bar[stage]);
+              if (kb + 1 == p.kb1) ptx::umma_commit(&tfull_bar[acc]);
+            }
+          }
+          __syncwarp();
+          if (++stage == stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ++iter;
+      }
+      if (P2) {
+        // accumulator tail: both CTAs' epilogues have drained every accumulator (their
+        // remote arrivals on our tempty barriers have landed) before the pair leaves
+        for (int i = 0; i < 2; ++i, ++iter) ptx::mbar_wait(&tempty_bar[iter & 1], ((iter >> 1) & 1) ^ 1);
+      }
+      if (st && lane == 0) st[3] = ptx::globaltimer();
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;  // TMEM lane quadrant (warp % 4)
@@ -234,6 +302,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     it.init(pm, n_tiles);
     Piece p;
     int iter = 0, chunk = 0;
+    // accumulator release: our own tempty, or the pair leader's
+    auto release_acc = [&](int acc) {
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (P2)
+          ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty_bar[acc]), 0));
+        else
+          ptx::mbar_arrive(&tempty_bar[acc]);
+      }
+    };
     while (it.next(pm, n_tiles, p)) {
       const int acc = iter & 1;
       const int mt = p.tile / pm.n_ntiles;
@@ -245,9 +324,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n = mt * kBlockM + row;
       const bool n_ok = n < n_out;
       const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * bn);
-      PieceIter ahead = it;
-      Piece pn;
-      const bool last_piece = !ahead.next(pm, n_tiles, pn);
       if (epi.mode == kGemmPartial) {
         // 16-token chunks through the staging slots; a slot is rewritten only after the
         // store issued kStgSlots chunks earlier has finished reading it
@@ -269,10 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::bulk_commit();
           }
         }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
-        (void)last_piece;
+        release_acc(acc);
         (void)n_ok;
       } else {
         for (int c0 = 0; c0 < bn; c0 += 16) {
@@ -296,9 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+        release_acc(acc);
         asm volatile("bar.sync 1, 128;" ::: "memory");
         for (int c = ew * 32 + lane; c < bn; c += 128) {
           const int t = nt * bn + c;
@@ -321,9 +392,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   ptx::grid_dep_launch();
   ptx::tc_fence_before();
-  __syncthreads();
+  if (P2) {  // neither CTA frees its TMEM / shared memory while the peer may still touch it
+    ptx::cluster_arrive();
+    ptx::cluster_wait();
+  } else {
+    __syncthreads();
+  }
   ptx::tc_fence_after();
-  if (warp == 2) ptx::tmem_dealloc(tmem_base, tmem_cols);
+  if (warp == 2) {
+    if (P2)
+      ptx::tmem_dealloc_2sm(tmem_base, tmem_cols);
+    else
+      ptx::tmem_dealloc(tmem_base, tmem_cols);
+  }
   if (st && threadIdx.x == 0) st[6] = ptx::globaltimer();
 }
 
@@ -368,7 +449,18 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
   p.n_mtiles = (n_out + kBlockM - 1) / kBlockM;
   p.kb = (k + kBlockK - 1) / kBlockK;
   const long long n_tiles = static_cast<long long>(p.n_mtiles) * p.n_ntiles;
-  const size_t stage_bytes = kTileABytes + static_cast<size_t>(p.bn) * kBlockK * 2;
+  // CTA pairs (cta_group::2, PieceMap::pair) from this many token rows (0 = never): above one
+  // token tile (compute-bound); at T = 160 the weight stream bounds the k-loop and a pair's
+  // coarser stream-K units cost more than the halved token operand saves
+  // (tools/gemm_time_probe.py: T = 1280 QKV 105.3 -> 100.4 us, gate_up 184.9 -> 175.4;
+  // T = 160 QKV 23.2 -> 24.6)
+  static const int pair_min_t = [] {
+    const char* e = std::getenv("SPIN_GEMM_PAIR_MIN_T");
+    return e ? std::atoi(e) : 257;
+  }();
+  const bool paired = mode == kGemmPartial && pair_min_t > 0 && t >= pair_min_t && p.n_mtiles % 2 == 0 &&
+                      p.bn % 32 == 0;
+  const size_t stage_bytes = kTileABytes + static_cast<size_t>(paired ? p.bn / 2 : p.bn) * kBlockK * 2;
   const size_t budget = 227 * 1024 - 1024 - (mode == kGemmPartial ? kStgBytes : kRedBytes) - kBarBytes;
   static const int cap = [] {
     const char* e = std::getenv("SPIN_GEMM_STAGES");  // experiments only
@@ -394,9 +486,14 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
     const char* e = std::getenv("SPIN_GEMM_GROUPED");  // A/B switch
     return e ? std::atoi(e) != 0 : true;
   }();
+  if (paired) {
+    m.pair = 2;
+    m.units /= 2;
+    num_sms /= 2;  // the stream-K search below runs over CTA pairs
+  }
   if (mode == kGemmPartial && p.n_ntiles > 1 && grouped_ok && p.n_ntiles <= num_sms) {
     m.ntg = p.n_ntiles;
-    m.units = static_cast<long long>(p.n_mtiles) * p.kb;
+    m.units = static_cast<long long>(p.n_mtiles / m.pair) * p.kb;
     num_sms /= m.ntg;  // the stream-K search below runs over CTA groups
   }
   if (mode == kGemmPartial) {
@@ -421,9 +518,13 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
         w = std::max(w, q.pieces(static_cast<int>((tile % p.n_ntiles) * p.bn), static_cast<int>((tile / p.n_ntiles) * kBlockM)));
       return w;
     };
+    // The slack counts SMs: with CTA groups of ntg token tiles, one group fewer already idles
+    // ntg SMs (T = 1280: 24 instead of 29 groups of 5 left 25 SMs idle for 1 piece per tile,
+    // 113 -> 105.6 us for the 7B QKV at 29 groups, tools/gemm_time_probe.py).
+    const int gslack = slack / m.ntg;
     if (m.grid == num_sms && m.units <= (1 << 20)) {
       int best = m.grid, best_w = worst(m.grid);
-      for (int g = m.grid - 1; g >= m.grid - slack && g > 0; --g) {
+      for (int g = m.grid - 1; g >= m.grid - gslack && g > 0; --g) {
         const int w = worst(g);
         if (w < best_w) best = g, best_w = w;
       }
@@ -442,14 +543,22 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
     m.grid = static_cast<int>(std::min<long long>(num_sms, n_tiles));
     p.max_pieces = 1;
   }
-  p.grid = m.grid * m.ntg;
+  p.grid = m.grid * m.ntg * m.pair;
   return p;
 }
 
 cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, const GemmEpilogue& epi,
                         cudaStream_t stream, bool pdl) {
   CUtensorMap tm_x, tm_part{};
-  if (!encode_tmap_bf16(&tm_x, X, plan.t, plan.k, plan.bn, kBlockK, true)) return cudaErrorInvalidValue;
+  // paired CTAs each load half of the token tile; their weight atoms come through a 2-D
+  // view of the tiled layout ([atoms * 128 rows][64], unswizzled: the atoms already are
+  // the swizzled shared-memory images) so that the copy can signal the leader's barrier
+  CUtensorMap tm_w{};
+  if (!encode_tmap_bf16(&tm_x, X, plan.t, plan.k, plan.bn / plan.map.pair, kBlockK, true)) return cudaErrorInvalidValue;
+  if (plan.map.pair > 1 &&
+      !encode_tmap_bf16(&tm_w, W, static_cast<uint64_t>(plan.n_mtiles) * plan.kb * kBlockM, kBlockK, kBlockM, kBlockK,
+                        false))
+    return cudaErrorInvalidValue;
   if (epi.mode == kGemmPartial) {
     // part[slot][t][n_out] fp32 as a 3-D tensor (clips rows t >= T and features n >= n_out)
     auto fn = get_encode_fn();
@@ -464,20 +573,33 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  ensure_smem_optin(reinterpret_cast<const void*>(gemm_tc_kernel), 227 * 1024);
+  const bool p2 = plan.map.pair > 1;
+  ensure_smem_optin(p2 ? reinterpret_cast<const void*>(gemm_tc_kernel<true>)
+                       : reinterpret_cast<const void*>(gemm_tc_kernel<false>),
+                    227 * 1024);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(plan.grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = plan.smem_bytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (plan.map.pair > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = plan.map.pair;
+    attr[na].val.clusterDim.y = 1;
+    attr[na++].val.clusterDim.z = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   GemmEpilogue e = epi;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel, static_cast<const __nv_bfloat16*>(W), tm_x, tm_part, plan.map, e,
-                            plan.n_out, plan.t, plan.stages);
+  return cudaLaunchKernelEx(&cfg, p2 ? gemm_tc_kernel<true> : gemm_tc_kernel<false>,
+                            static_cast<const __nv_bfloat16*>(W), tm_x, tm_part, tm_w, plan.map, e, plan.n_out, plan.t,
+                            plan.stages);
 }
 
 }  // namespace spin

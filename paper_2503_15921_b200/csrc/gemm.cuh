@@ -43,6 +43,11 @@ struct PieceMap {
   // time, each against its own token tile, so every weight atom comes from DRAM once and
   // from L2 for its siblings (instead of once per token tile). ntg = 1: plain stream-K.
   int ntg = 1;
+  // CTA pairs (PARTIAL): the two CTAs of a 2-CTA cluster own adjacent weight tiles
+  // (2s, 2s + 1) over the same token tile and k-range; each TMA-loads half of the token
+  // tile and multicasts it to both, so the L2 serves every token tile once per pair. The
+  // stream-K units are then the PAIRS' k-blocks (a unit is a 256-row weight super tile).
+  int pair = 1;
   const uint8_t* tbl = nullptr;  // device: pieces per tile (filled by the host at plan time)
 
   // CTA (group, when ntg > 1) that owns stream-K unit u.
@@ -52,7 +57,8 @@ struct PieceMap {
   // Number of partial slots written for (token t, feature n).
   __host__ __device__ __forceinline__ int pieces(int t, int n) const {
     if (mode != kGemmPartial) return 1;
-    const long long tile = ntg > 1 ? static_cast<long long>(n / 128) : static_cast<long long>(n / 128) * n_ntiles + t / bn;
+    const long long sm = n / (128 * pair);
+    const long long tile = ntg > 1 ? sm : sm * n_ntiles + t / bn;
     return cta_of(tile * kb + kb - 1) - cta_of(tile * kb) + 1;
   }
   __device__ __forceinline__ int tile_pieces(int t, int n) const { return tbl[(n / 128) * n_ntiles + t / bn]; }
@@ -62,7 +68,7 @@ struct GemmPlan {
   int n_out = 0, k = 0, t = 0;
   std::vector<uint8_t> tile_pieces;  // host copy of PieceMap::tbl
   int bn = 0, n_ntiles = 0, n_mtiles = 0, kb = 0;
-  int grid = 0, stages = 0, max_pieces = 1;  // grid: CTAs launched (= map.grid * map.ntg)
+  int grid = 0, stages = 0, max_pieces = 1;  // grid: CTAs launched (= map.grid * map.ntg * map.pair)
   size_t smem_bytes = 0;
   PieceMap map{};
 };
