@@ -25,7 +25,8 @@ def _rand_bf16(shape, seed, scale=1.0):
 @pytest.mark.parametrize(
     "n_out,k,t",
     [(256, 256, 16), (1376, 256, 40), (768, 688, 8), (4096, 4096, 160), (12288, 4096, 160), (4096, 11008, 160),
-     (22016, 4096, 160), (2304, 768, 32), (1024, 512, 600), (12288, 4096, 645), (4096, 4096, 1280)],
+     (22016, 4096, 160), (2304, 768, 32), (1024, 512, 600), (12288, 4096, 645), (4096, 4096, 1280),
+     (2048, 1024, 512), (5120, 13824, 1280)],  # T > 256 with an even tile count: CTA pairs (cta_group::2)
 )
 def test_gemm_partial_matches_fp32(n_out, k, t):
     lib = _lib.load()
