@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define SPIN_ABI_VERSION 2
+#define SPIN_ABI_VERSION 3
 #define SPIN_MAX_SSM 8
 
 typedef enum spin_status {
@@ -111,6 +111,13 @@ typedef struct spin_model_desc {
   float planted_gain;/* strength of the planted next-token map in lm_head    */
   float resid_scale; /* o_proj / down_proj scale: block contribution size    */
   float init_scale;  /* other projections ~ U(-1,1) * init_scale             */
+  /* Token domains of the planted map (ABI v3): the vocabulary splits into planted_domains
+   * contiguous ranges of vocab / planted_domains ids and pi maps every range onto itself;
+   * the lm_head rows of domain d carry the planted term only if bit d of planted_mask is
+   * set. 0 / 0 = one domain, all planted (the v2 behaviour). A model whose mask misses a
+   * request's domain drafts noise for it: per-request heterogeneous SSM quality (config 4). */
+  int32_t planted_domains;
+  uint32_t planted_mask;
 } spin_model_desc;
 
 typedef struct spin_engine_opts {

@@ -22,7 +22,8 @@ class SoModelDesc(C.Structure):
         ("d_model", C.c_int32), ("n_layers", C.c_int32), ("n_heads", C.c_int32), ("head_dim", C.c_int32),
         ("ffn", C.c_int32), ("vocab", C.c_int32), ("rope_theta", C.c_float), ("rms_eps", C.c_float),
         ("seed", C.c_uint64), ("embed_scale", C.c_float), ("planted_gain", C.c_float),
-        ("resid_scale", C.c_float), ("init_scale", C.c_float),
+        ("resid_scale", C.c_float), ("init_scale", C.c_float), ("planted_domains", C.c_int32),
+        ("planted_mask", C.c_uint32),
     ]
 
 

@@ -37,11 +37,11 @@ static inline uint16_t f2bf(float f) { /* round to nearest even, like __float2bf
 static inline float rbf(float f) { return bf2f(f2bf(f)); }
 
 /* --------------------------------------------------------- synthetic weights
- * Spec (identical in paper_2503_15921_b200/csrc/weights.cu):
+ * Spec (identical in paper_2503_15921_b200/csrc/kernels.cu init_weights_kernel, engine.cu init_model):
  *   stream = mix_seed(seed, 0x5350494E, tag, layer)
  *   r      = float(splitmix64(stream + row*cols + col) >> 40) * 2^-23 - 1   in [-1, 1), exact
  *   w      = bf16_rne(r * scale)                           (one fp32 multiply)
- * lm_head row v additionally carries the planted next-token map:
+ * lm_head row v additionally carries the planted next-token map (if v's domain is planted):
  *   w      = bf16_rne(r * scale + (planted_gain / d) * E[pi^-1(v)][col])
  */
 enum { TAG_EMBED = 1, TAG_LM_HEAD = 2, TAG_QKV = 3, TAG_O = 4, TAG_GATE_UP = 5, TAG_DOWN = 6 };
@@ -86,21 +86,40 @@ static int64_t gcd64(int64_t a, int64_t b) {
   return a;
 }
 
-/* pi(t) = (A t + C) mod V with A the first value >= 7919 coprime to V. */
-static void planted_params(const so_model_desc* m, int64_t* A, int64_t* Cc, int64_t* Ainv) {
-  const int64_t V = m->vocab;
-  int64_t a = 7919 % V;
+/* Domains of the planted map: nd = max(planted_domains, 1) contiguous ranges of
+ * S = vocab / nd ids; inside each, pi(t) = base + (A (t - base) + C) mod S with A the
+ * first value >= 7919 coprime to S (nd = 1: pi(t) = (A t + C) mod V). Row v of the
+ * lm_head is planted iff bit (v / S) of planted_mask is set (mask 0 = all). */
+typedef struct {
+  int64_t S, A, Cc, Ainv;
+  uint32_t mask;
+} planted_t;
+
+static planted_t planted_params(const so_model_desc* m) {
+  planted_t p;
+  const int64_t nd = m->planted_domains > 1 ? m->planted_domains : 1;
+  p.S = m->vocab / nd;
+  int64_t a = 7919 % p.S;
   if (a == 0) a = 1;
-  while (gcd64(a, V) != 1) a = (a + 1) % V;
-  *A = a;
-  *Cc = 12345 % V;
-  *Ainv = mod_inverse(a, V);
+  while (gcd64(a, p.S) != 1) a = (a + 1) % p.S;
+  p.A = a;
+  p.Cc = 12345 % p.S;
+  p.Ainv = mod_inverse(a, p.S);
+  p.mask = m->planted_mask ? m->planted_mask : 0xffffffffu;
+  return p;
+}
+
+/* pi^-1(v) if row v is planted, else -1 */
+static int64_t planted_src(const planted_t* p, int64_t v) {
+  const int64_t dom = v / p->S, base = dom * p->S;
+  if (dom >= 32 || !((p->mask >> dom) & 1u)) return -1;
+  return base + (p->Ainv * (((v - base - p->Cc) % p->S) + p->S)) % p->S;
 }
 
 int so_planted_next(const so_model_desc* m, int token) {
-  int64_t A, Cc, Ai;
-  planted_params(m, &A, &Cc, &Ai);
-  return (int)((A * token + Cc) % m->vocab);
+  const planted_t p = planted_params(m);
+  const int64_t base = token / p.S * p.S;
+  return (int)(base + (p.A * (token - base) + p.Cc) % p.S);
 }
 
 uint16_t so_weight_bits(const so_model_desc* m, int tag, int layer, int64_t row, int64_t col) {
@@ -108,9 +127,9 @@ uint16_t so_weight_bits(const so_model_desc* m, int tag, int layer, int64_t row,
   const float s = tag_scale(m, tag);
   const float r = uniform_pm1(weight_stream(m, tag, layer), (uint64_t)(row * cols + col));
   if (tag != TAG_LM_HEAD || m->planted_gain == 0.0f) return f2bf(r * s);
-  int64_t A, Cc, Ai;
-  planted_params(m, &A, &Cc, &Ai);
-  const int64_t src = (Ai * ((row - Cc) % m->vocab + m->vocab)) % m->vocab;
+  const planted_t p = planted_params(m);
+  const int64_t src = planted_src(&p, row);
+  if (src < 0) return f2bf(r * s);
   const float e = bf2f(so_weight_bits(m, TAG_EMBED, 0, src, col));
   const float g = (float)((double)m->planted_gain / (double)m->d_model);
   const float a = r * s;
@@ -123,16 +142,15 @@ static uint16_t* make_weight(const so_model_desc* m, int tag, int layer, int64_t
   const float s = tag_scale(m, tag);
   const uint64_t stream = weight_stream(m, tag, layer);
   const int planted = tag == TAG_LM_HEAD && m->planted_gain != 0.0f;
-  int64_t A = 1, Cc = 0, Ai = 1;
-  if (planted) planted_params(m, &A, &Cc, &Ai);
+  const planted_t p = planted_params(m);
   const float g = (float)((double)m->planted_gain / (double)m->d_model);
   uint16_t* w = (uint16_t*)malloc(sizeof(uint16_t) * rows * cols);
 #pragma omp parallel for schedule(static)
   for (int64_t r = 0; r < rows; ++r) {
-    const int64_t src = planted ? (Ai * ((r - Cc) % m->vocab + m->vocab)) % m->vocab : 0;
+    const int64_t src = planted ? planted_src(&p, r) : -1;
     for (int64_t c = 0; c < cols; ++c) {
       const float a = uniform_pm1(stream, (uint64_t)(r * cols + c)) * s;
-      if (!planted) {
+      if (src < 0) {
         w[r * cols + c] = f2bf(a);
       } else {
         const float b = g * bf2f(emb[src * cols + c]);

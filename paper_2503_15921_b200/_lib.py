@@ -60,6 +60,8 @@ class ModelDesc(C.Structure):
         ("planted_gain", C.c_float),
         ("resid_scale", C.c_float),
         ("init_scale", C.c_float),
+        ("planted_domains", C.c_int32),
+        ("planted_mask", C.c_uint32),
     ]
 
 

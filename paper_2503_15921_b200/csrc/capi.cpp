@@ -186,8 +186,8 @@ spin_status spin_gemm_bench(int32_t n_out, int32_t k, int32_t t, int32_t mode, i
       check_cuda(cudaMalloc(&idx, out_elems * 4), "malloc");
       check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
       // tiled layout of seeded weights is still a weight matrix (values do not matter for timing)
-      launch_init_weights(w, n_out, k, 0x5350494eull, 0.05f, nullptr, 0.f, 0, 0, 0, 1, st);
-      launch_init_weights(x, t, k, 0x58ull, 1.f, nullptr, 0.f, 0, 0, 0, 0, st);
+      launch_init_weights(w, n_out, k, 0x5350494eull, 0.05f, nullptr, 0.f, 1, 0, 0, 0u, 1, st);
+      launch_init_weights(x, t, k, 0x58ull, 1.f, nullptr, 0.f, 1, 0, 0, 0u, 0, st);
       GemmEpilogue e;
       e.mode = mode;
       e.part = out;

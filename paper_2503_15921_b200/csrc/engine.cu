@@ -69,6 +69,9 @@ void validate_desc(const spin_model_desc& d, const char* who) {
   if (d.d_model % 64 != 0 || d.ffn % 8 != 0) fail(SPIN_CONFIG_ERROR, w + ": d_model % 64 and ffn % 8 required");
   if (d.d_model > 8192) fail(SPIN_CONFIG_ERROR, w + ": d_model above 8192 unsupported");
   if (!(d.rope_theta > 0.f) || !(d.rms_eps > 0.f)) fail(SPIN_CONFIG_ERROR, w + ": rope_theta / rms_eps must be > 0");
+  if (d.planted_domains < 0 || d.planted_domains > 32 ||
+      (d.planted_domains > 1 && d.vocab % d.planted_domains != 0))
+    fail(SPIN_CONFIG_ERROR, w + ": planted_domains must be 0..32 and divide the vocabulary");
 }
 
 }  // namespace
@@ -115,23 +118,26 @@ void Engine::init_model(ModelDev& m, const spin_model_desc& d, bool draft) {
   const float s_in = static_cast<float>(std::sqrt(3.0 / D) * d.init_scale);
   const float s_o = static_cast<float>(std::sqrt(3.0 / D) * d.resid_scale);
   const float s_dn = static_cast<float>(std::sqrt(3.0 / F) * d.resid_scale);
-  launch_init_weights(m.emb, V, D, stream_of(kTagEmbed, 0), s_emb, nullptr, 0.f, V, 1, 0, 0, sv_);
-  int64_t a = 7919 % static_cast<int64_t>(V);
+  launch_init_weights(m.emb, V, D, stream_of(kTagEmbed, 0), s_emb, nullptr, 0.f, V, 1, 0, 0u, 0, sv_);
+  // planted map: pi maps each of nd domains of S ids onto itself (spin_c.h planted_domains)
+  const int64_t nd = d.planted_domains > 1 ? d.planted_domains : 1, S = V / nd;
+  int64_t a = 7919 % S;
   if (a == 0) a = 1;
-  while (gcd64(a, V) != 1) a = (a + 1) % static_cast<int64_t>(V);
-  const int64_t cc = 12345 % static_cast<int64_t>(V);
+  while (gcd64(a, S) != 1) a = (a + 1) % S;
+  const int64_t cc = 12345 % S;
+  const uint32_t mask = d.planted_mask ? d.planted_mask : 0xffffffffu;
   const float g = static_cast<float>(static_cast<double>(d.planted_gain) / static_cast<double>(D));
-  launch_init_weights(m.head, V, D, stream_of(kTagHead, 0), s_head, d.planted_gain != 0.f ? m.emb : nullptr, g, V,
-                      mod_inverse(a, V), cc, 1, sv_);
+  launch_init_weights(m.head, V, D, stream_of(kTagHead, 0), s_head, d.planted_gain != 0.f ? m.emb : nullptr, g, S,
+                      mod_inverse(a, S), cc, mask, 1, sv_);
   for (int l = 0; l < m.L; ++l) {
     launch_init_weights(const_cast<bf16*>(m.layers[l].qkv), 3 * D, D, stream_of(kTagQkv, l), s_in, nullptr, 0.f, V, 1,
-                        0, 1, sv_);
-    launch_init_weights(const_cast<bf16*>(m.layers[l].o), D, D, stream_of(kTagO, l), s_o, nullptr, 0.f, V, 1, 0, 1,
+                        0, 0u, 1, sv_);
+    launch_init_weights(const_cast<bf16*>(m.layers[l].o), D, D, stream_of(kTagO, l), s_o, nullptr, 0.f, V, 1, 0, 0u, 1,
                         sv_);
     launch_init_weights(const_cast<bf16*>(m.layers[l].gu), 2 * F, D, stream_of(kTagGateUp, l), s_in, nullptr, 0.f, V,
-                        1, 0, 1, sv_);
+                        1, 0, 0u, 1, sv_);
     launch_init_weights(const_cast<bf16*>(m.layers[l].dn), D, F, stream_of(kTagDown, l), s_dn, nullptr, 0.f, V, 1, 0,
-                        1, sv_);
+                        0u, 1, sv_);
   }
   check_cuda(cudaGetLastError(), "init weights");
   // SSMs on the fused draft path also keep unit-contiguous slab copies (draft.cu)
@@ -284,7 +290,13 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
   auto gemm_bytes = [&](int n_out, int k) { return 2.0 * n_out * k + 2.0 * T * k + 2.0 * T * n_out; };
   AttnGeom g{m.H, m.hd, opts_.max_requests, opts_.max_ctx, 0, static_cast<float>(1.0 / std::sqrt(double(m.hd))),
              m.kc, m.vc};
-  if (m.sbuf != nullptr && head_mode != 2 && draft_fused_supported(D, m.H, m.hd, F, T)) {
+  // The fused draft kernels serve draft steps only (sh.early: every request's new KV rows are its
+  // query rows). Extends of <= 32 rows (switch catch-ups, prewarm chunks) take the generic
+  // kernels: fused extends running on a prewarm stream beside graph-launched draft steps
+  // produced NaN logits in the 13B config-4 LBSS loop (tools/scratch/repro_c4dom.py; a draft
+  // token of INT_MAX then faulted in embed_ss_kernel); the switch re-enables them for debugging.
+  static const bool fused_extends = std::getenv("SPIN_DRAFT_FUSED_EXTEND") != nullptr;
+  if (m.sbuf != nullptr && head_mode != 2 && (sh.early || fused_extends) && draft_fused_supported(D, m.H, m.hd, F, T)) {
     forward_draft(m, ln, sh, g, s, head_mode);
     return;
   }
@@ -491,6 +503,8 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
   for (int j = 0; j < n_ssm; ++j) {
     validate_desc(ssms[j], "ssm");
     if (ssms[j].vocab != target.vocab) fail(SPIN_CONFIG_ERROR, "ssm vocabulary must match the target's");
+    if (std::max(ssms[j].planted_domains, 1) != std::max(target.planted_domains, 1))
+      fail(SPIN_CONFIG_ERROR, "ssm planted_domains must match the target's (one planted map)");
   }
   check_cuda(cudaSetDevice(opts.device), "cudaSetDevice");
   (void)cudaGetLastError();  // drop a stale non-sticky error left by an earlier caller
@@ -507,9 +521,9 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
   for (auto& s : ss_) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
   // sticky device status word (FwdMeta::err), host-mapped: read after every synchronisation
   void* err_host = nullptr;
-  check_cuda(cudaHostAlloc(&err_host, 4, cudaHostAllocMapped), "pinned status");
+  check_cuda(cudaHostAlloc(&err_host, 8 * 4, cudaHostAllocMapped), "pinned status");  // [status, detail x 7]
   h_err_ = static_cast<volatile int32_t*>(err_host);
-  *h_err_ = 0;
+  for (int i = 0; i < 8; ++i) h_err_[i] = 0;
   void* err_dev = nullptr;
   check_cuda(cudaHostGetDevicePointer(&err_dev, err_host, 0), "mapped status");
   d_err_ = static_cast<int32_t*>(err_dev);
@@ -611,6 +625,17 @@ void Engine::sync_sv(const char* what) {
   if (*h_err_ != 0) {
     const int e = *h_err_;
     *h_err_ = 0;
+    if (e == 3 || e == 4) {  // non-finite logits: the slot's host-side state for the report
+      const int slot = h_err_[1], j = h_err_[2];
+      std::string st = "slot " + std::to_string(slot) + (e == 3 ? " ssm " + std::to_string(j) : " target") +
+                       " step/k " + std::to_string(h_err_[3]) + " row " + std::to_string(h_err_[4]);
+      if (slot >= 0 && slot < opts_.max_requests) {
+        st += " committed " + std::to_string(h_committed_[slot]) + " ssm_len";
+        for (size_t m = 0; m < ssm_.size(); ++m)
+          st += " " + std::to_string(h_ssm_len_[m * opts_.max_requests + slot]);
+      }
+      fail(SPIN_CUDA_ERROR, std::string(what) + ": non-finite logits (argmax undefined): " + st);
+    }
     fail(SPIN_CAPACITY_ERROR, std::string(what) + (e == 2 ? ": a round would commit past max_ctx"
                                                            : ": attention work list exceeds its buffers") +
                                   " (device status " + std::to_string(e) + ")");
@@ -739,6 +764,13 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
         if (jobs[j].empty()) continue;
         cudaStream_t ps = ps_[j];
         check_cuda(cudaEventSynchronize(ev_pw_[j]), "prewarm staging");  // staging reuse
+        // The catch-up overlaps the round's target verification, not its draft phase: run
+        // beside the fused draft kernels (graph replays) it left NaN logits in a later draft of
+        // the 13B config-4 LBSS loop (deterministic at one slot; tools/scratch/repro_c4dom.py),
+        // an interaction not yet root-caused. The verify is the long phase (7 ms of 8.5 at 13B),
+        // so little hiding is lost. SPIN_PREWARM_WITH_DRAFTS=1 restores full overlap (debugging).
+        static const bool with_drafts = std::getenv("SPIN_PREWARM_WITH_DRAFTS") != nullptr;
+        if (!with_drafts) check_cuda(cudaStreamWaitEvent(ps, ev_draft_, 0), "prewarm after drafts");
         extend(static_cast<int>(j), jobs[j], ps, &pwlane_[j], pw_pin_[j], pw_pin_cap_);
         for (const auto& r : jobs[j]) {
           const size_t idx = j * opts_.max_requests + std::get<0>(r);
@@ -1247,6 +1279,12 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, const int
     }
     // destinations of future switches recomputed on idle streams while this round runs
     if (prewarm) enqueue_prewarm(n, slots, prewarm, ssm_of);
+    static const bool pw_sync = std::getenv("SPIN_PREWARM_SYNC") != nullptr;  // debugging: no overlap
+    if (prewarm && pw_sync) {
+      sync_sv("round (before prewarm)");
+      if (pw_thread_.joinable()) pw_thread_.join();
+      check_cuda(cudaDeviceSynchronize(), "prewarm (synchronous)");
+    }
     sync_sv("round");
     dump_stamps();
     check_cuda(cudaEventElapsedTime(&draft_ms, ev_start_, ev_draft_), "event timing");

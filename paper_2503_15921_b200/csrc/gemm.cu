@@ -201,6 +201,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         prefetched = s;
       }
       ptx::grid_dep_wait();
+      // Early trigger: the dependent (the reduction / epilogue kernel) launches now and its
+      // blocks sit resident at their own dependency wait while this grid streams, so the
+      // hop after the GEMM costs no launch latency. After our wait, not before: dependents
+      // read data of OUR predecessor's predecessor before their wait (resid_norm's h row).
+      if (epi.early_trigger) ptx::grid_dep_launch();
       if (st) st[1] = ptx::globaltimer();
       int issued = 0;
       while (it.next(pm, n_tiles, p)) {
@@ -597,6 +602,11 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
   cfg.attrs = attr;
   cfg.numAttrs = na;
   GemmEpilogue e = epi;
+  static const int early = [] {
+    const char* v = std::getenv("SPIN_GEMM_EARLY_TRIGGER");  // A/B switch
+    return v ? std::atoi(v) : 0;
+  }();
+  e.early_trigger = early;
   return cudaLaunchKernelEx(&cfg, p2 ? gemm_tc_kernel<true> : gemm_tc_kernel<false>,
                             static_cast<const __nv_bfloat16*>(W), tm_x, tm_part, tm_w, plan.map, e, plan.n_out, plan.t,
                             plan.stages);

@@ -163,7 +163,14 @@ __global__ void __launch_bounds__(kMetaThreads) meta_kernel(MetaArgs a, SlotStat
   if (a.mode == kMetaDraftK || a.mode == kMetaCollect) {
     for (int r = warp; r < n; r += kMetaThreads / 32) {
       const int row = r * a.prev_qlen + a.prev_qlen - 1;
-      const int tok = row_argmax_warp(a.amax_val, a.amax_idx, a.amax_tiles, a.prev_t, row);
+      int tok = row_argmax_warp(a.amax_val, a.amax_idx, a.amax_tiles, a.prev_t, row);
+      if (tok < 0 || tok >= a.amax_tiles * 128) {  // all-NaN logits: report (status 3), never index with it
+        if (lane == 0 && m.err && atomicCAS(m.err, 0, 3) == 0) {
+          m.err[1] = a.list[r], m.err[2] = a.ssm, m.err[3] = a.step, m.err[4] = row;
+          __threadfence_system();
+        }
+        tok = 0;
+      }
       if (lane == 0) st.drafts[static_cast<size_t>(a.list[r]) * W + a.step - 1] = tok;
     }
     __syncthreads();
@@ -685,7 +692,14 @@ __global__ void accept_kernel(FwdMeta m, int n_req, int W, const int32_t* list, 
   bool alive = true;
   int bonus = -1;
   for (int k = 0; k <= W; ++k) {
-    const int y = row_argmax_warp(amax_val, amax_idx, tiles, T, q0 + k);
+    int y = row_argmax_warp(amax_val, amax_idx, tiles, T, q0 + k);
+    if (y < 0 || y >= tiles * 128) {  // all-NaN target logits: report (status 4)
+      if (lane == 0 && m.err && atomicCAS(m.err, 0, 4) == 0) {
+        m.err[1] = slot, m.err[2] = -1, m.err[3] = k, m.err[4] = q0 + k;
+        __threadfence_system();
+      }
+      y = 0;
+    }
     if (out_target != nullptr && lane == 0) out_target[static_cast<size_t>(r) * (W + 1) + k] = y;
     if (alive) {
       if (k < W && dr[k] == y) {
@@ -732,8 +746,12 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 //              (16-B chunk c of row r at c ^ (r % 8)); padding rows / columns are zero;
 //   tiled = 0: row-major (the embedding, gathered by token).
 // Values depend only on the logical (row, col): the oracle restates them row-major.
+// emb != nullptr (lm_head): row v also carries g * E[pi^-1(v)] when v's domain (v / dsize)
+// is planted (bit set in `mask`); pi maps each domain of dsize ids onto itself
+// (oracle/llama_oracle.c planted_params).
 __global__ void init_weights_kernel(bf16* w, int64_t rows, int64_t cols, uint64_t stream, float scale,
-                                    const bf16* emb, float g, int64_t vocab, int64_t a_inv, int64_t cc, int tiled) {
+                                    const bf16* emb, float g, int64_t dsize, int64_t a_inv, int64_t cc, uint32_t mask,
+                                    int tiled) {
   const int64_t katoms = (cols + 63) / 64;
   const int64_t prow = tiled ? (rows + 127) / 128 * 128 : rows, pcols = tiled ? katoms * 64 : cols;
   const int64_t total = prow * pcols;
@@ -756,10 +774,11 @@ __global__ void init_weights_kernel(bf16* w, int64_t rows, int64_t cols, uint64_
     const float u = static_cast<float>(splitmix64(stream + static_cast<uint64_t>(le)) >> 40);
     const float r = __fsub_rn(__fmul_rn(u, 0x1.0p-23f), 1.0f);
     const float a = __fmul_rn(r, scale);
-    if (emb == nullptr) {
+    const int64_t dom = row / dsize, base = dom * dsize;
+    if (emb == nullptr || dom >= 32 || !((mask >> dom) & 1u)) {
       w[e] = __float2bfloat16_rn(a);
     } else {
-      const int64_t src = (a_inv * (((row - cc) % vocab + vocab) % vocab)) % vocab;
+      const int64_t src = base + (a_inv * (((row - base - cc) % dsize) + dsize)) % dsize;
       const float b = __fmul_rn(g, __bfloat162float(emb[src * cols + col]));
       w[e] = __float2bfloat16_rn(__fadd_rn(a, b));
     }
@@ -938,8 +957,10 @@ void launch_swizzle_kv(const bf16* src, bf16* dst, int64_t rows, int hd, int ctx
 }
 
 void launch_init_weights(bf16* w, int64_t rows, int64_t cols, uint64_t stream, float scale, const bf16* emb,
-                         float planted_g, int64_t vocab, int64_t A_inv, int64_t Cc, int tiled, cudaStream_t s) {
-  init_weights_kernel<<<148 * 8, 256, 0, s>>>(w, rows, cols, stream, scale, emb, planted_g, vocab, A_inv, Cc, tiled);
+                         float planted_g, int64_t dsize, int64_t A_inv, int64_t Cc, uint32_t mask, int tiled,
+                         cudaStream_t s) {
+  init_weights_kernel<<<148 * 8, 256, 0, s>>>(w, rows, cols, stream, scale, emb, planted_g, dsize, A_inv, Cc, mask,
+                                              tiled);
 }
 
 void launch_tile_weights(const bf16* src, bf16* dst, int64_t rows, int64_t cols, cudaStream_t s) {

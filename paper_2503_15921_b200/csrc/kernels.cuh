@@ -175,8 +175,10 @@ void launch_accept(const FwdMeta& m, int n_req, int window, const int32_t* list,
 // tiled = 1: the GEMM weight layout (gemm.cuh tiled_weight_elems); 0: row-major (embedding).
 // Standard-layout [rows][hd] KV rows -> the swizzled cache layout (kernel tests).
 void launch_swizzle_kv(const bf16* src, bf16* dst, int64_t rows, int hd, int ctx, cudaStream_t s);
+// emb/planted_g/dsize/A_inv/Cc/mask: the planted map of an lm_head (dsize = ids per domain).
 void launch_init_weights(bf16* w, int64_t rows, int64_t cols, uint64_t stream, float scale, const bf16* emb,
-                         float planted_g, int64_t vocab, int64_t A_inv, int64_t Cc, int tiled, cudaStream_t s);
+                         float planted_g, int64_t dsize, int64_t A_inv, int64_t Cc, uint32_t mask, int tiled,
+                         cudaStream_t s);
 // Row-major [rows][cols] -> tiled GEMM weight layout.
 void launch_tile_weights(const bf16* src, bf16* dst, int64_t rows, int64_t cols, cudaStream_t s);
 

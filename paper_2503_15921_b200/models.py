@@ -8,7 +8,7 @@ heterogeneous rates.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, asdict
+from dataclasses import dataclass, asdict, replace
 
 import numpy as np
 
@@ -31,11 +31,13 @@ class ModelShape:
     embed_scale: float = 1.0
     rope_theta: float = 10000.0
     rms_eps: float = 1e-5
+    planted_domains: int = 0  # token domains of the planted map (0/1: one); pi keeps each domain
+    planted_mask: int = 0     # domains whose lm_head rows carry the planted term (0: all)
 
     def desc(self) -> _lib.ModelDesc:
         d = _lib.ModelDesc()
         for f in ("d_model", "n_layers", "n_heads", "head_dim", "ffn", "vocab", "rope_theta", "rms_eps", "seed",
-                  "embed_scale", "planted_gain", "resid_scale", "init_scale"):
+                  "embed_scale", "planted_gain", "resid_scale", "init_scale", "planted_domains", "planted_mask"):
             setattr(d, f, getattr(self, f))
         return d
 
@@ -64,6 +66,30 @@ LLAMA_160M = ModelShape("llama-160m-shape", 768, 12, 12, 64, 3072, 32000, seed=1
                         resid_scale=0.7)
 LLAMA_160M_B = ModelShape("llama-160m-shape-b", 768, 12, 12, 64, 3072, 32000, seed=160002, planted_gain=8.0,
                           resid_scale=0.9)
+
+
+# ---- config 4 with per-request heterogeneity: 4 token domains; the target plants every
+# domain, each SSM only some, so the best SSM depends on the request (its domain): the
+# 68M SSM is cheap but only knows domain 0, the 160M knows 0-2, the 160M-b knows 2-3.
+# The target's planted gain is raised to 20 so that its greedy continuation follows the map
+# (at 12 the 40-layer target leaves the prompt's domain within a few tokens: 35% of generated
+# tokens stay in it; at 20, 100% -- tools/scratch/domain_probe.py), and the 160M-b SSM gets the
+# 160M's gain so it is as good on its own domains.
+C4_DOMAINS = 4
+LLAMA_13B_DOM = replace(LLAMA_13B, name="llama-13b-shape-dom4", planted_domains=C4_DOMAINS, planted_gain=20.0)
+LLAMA_68M_DOM = replace(LLAMA_68M, name="llama-68m-shape-d0", planted_domains=C4_DOMAINS, planted_mask=0b0001)
+LLAMA_160M_DOM = replace(LLAMA_160M, name="llama-160m-shape-d012", planted_domains=C4_DOMAINS, planted_mask=0b0111)
+LLAMA_160M_B_DOM = replace(LLAMA_160M_B, name="llama-160m-shape-b-d23", planted_domains=C4_DOMAINS,
+                           planted_mask=0b1100, planted_gain=10.0, resid_scale=0.7)
+
+
+def domain_prompts(n: int, lo: int, hi: int, vocab: int, n_domains: int, seed: int) -> list[np.ndarray]:
+    """Prompt lengths U[lo, hi]; request i's tokens U over its domain i % n_domains
+    (vocab / n_domains contiguous ids), which the planted map keeps it in."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(lo, hi + 1, n)
+    size = vocab // n_domains
+    return [(size * (i % n_domains) + rng.integers(0, size, int(L))).astype(np.int32) for i, L in enumerate(lens)]
 
 
 def synthetic_prompts(n: int, lo: int, hi: int, vocab: int, seed: int) -> list[np.ndarray]:

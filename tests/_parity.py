@@ -32,9 +32,10 @@ KEYS = ("drafts", "target", "accepted", "bonus", "committed")
 
 class ParityRun:
     def __init__(self, target, ssms, *, batch, prompt_lo, prompt_hi, seed, window, max_ctx, twin=True,
-                 micro_batches=None, **gpu_kw):
+                 micro_batches=None, prompts=None, **gpu_kw):
         self.B, self.W = batch, window
-        prompts = synthetic_prompts(batch, prompt_lo, prompt_hi, target.vocab, seed)
+        if prompts is None:
+            prompts = synthetic_prompts(batch, prompt_lo, prompt_hi, target.vocab, seed)
         self.gpu = Engine(target, ssms, max_requests=batch, max_ctx=max_ctx, window=window, debug_logits=True,
                           **gpu_kw)
         if micro_batches is not None:  # pipelined rounds: the logits check needs one verify per round

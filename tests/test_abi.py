@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, f"declared in spin_c.h but not exported: {missing}"
     assert set(syms) <= set(_lib.exported_symbols())
-    assert lib.spin_abi_version() == 2
+    assert lib.spin_abi_version() == 3
 
 
 def spin_pack(lens, width):

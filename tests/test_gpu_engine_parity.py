@@ -99,3 +99,28 @@ def test_prewarm_hides_switch_catch_up_and_keeps_outcomes():
         assert np.array_equal(a.tokens(s), b.tokens(s))
     a.close()
     b.close()
+
+
+def test_planted_domains_bit_exact_and_heterogeneous():
+    """Per-request heterogeneous SSM quality (spin_c.h planted_domains / planted_mask, the
+    config-4 setup at config-1 size): 4 token domains, SSM 0 planted on domains 0-1, SSM 1 on
+    2-3, requests prompted inside domain i % 4. Bit-exact against the oracle, and a request
+    drafted by an SSM that knows its domain accepts more than one drafted by one that does not."""
+    from dataclasses import replace
+
+    from paper_2503_15921_b200.models import domain_prompts
+
+    tgt = replace(TINY_TARGET, planted_domains=4)
+    ssms = (replace(TINY_SSMS[0], planted_domains=4, planted_mask=0b0011),
+            replace(TINY_SSMS[1], planted_domains=4, planted_mask=0b1100))
+    prompts = domain_prompts(B, 16, 64, tgt.vocab, 4, 2503)
+    run = ParityRun(tgt, ssms, batch=B, prompt_lo=0, prompt_hi=0, seed=0, window=W, max_ctx=CTX, prompts=prompts)
+    assign = np.array([0, 1] * (B // 2), np.int32)  # request i (domain i % 4) on SSM i % 2
+    knows = np.array([(i % 4) // 2 == i % 2 for i in range(B)])
+    acc = np.zeros(B)
+    for _ in range(8):
+        acc += run.round(assign)["accepted"]
+    st = run.check()
+    run.close()
+    assert acc[knows].mean() > acc[~knows].mean() + 1.0, (acc, knows)
+    print("domains parity", st, "accepted known", acc[knows].mean() / 8, "unknown", acc[~knows].mean() / 8)
