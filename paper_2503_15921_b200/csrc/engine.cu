@@ -185,12 +185,13 @@ void Engine::init_model(ModelDev& m, const spin_model_desc& d, bool draft) {
   check_cuda(cudaMemcpy(m.rsin, s.data(), s.size() * 4, cudaMemcpyHostToDevice), "rope");
 }
 
-const GemmPlan& Engine::plan(int n_out, int k, int t, int mode) {
+const GemmPlan& Engine::plan(int n_out, int k, int t, int mode, int sms) {
   std::lock_guard<std::mutex> lock(plan_mu_);  // std::map references stay valid across inserts
-  const auto key = std::make_tuple(n_out, k, t, mode);
+  if (sms <= 0 || sms > num_sms_) sms = num_sms_;
+  const auto key = std::make_tuple(n_out, k, t, mode, sms);
   auto it = plans_.find(key);
   if (it == plans_.end()) {
-    GemmPlan p = gemm_plan(n_out, k, t, mode, num_sms_);
+    GemmPlan p = gemm_plan(n_out, k, t, mode, sms);
     if (!p.tile_pieces.empty()) {  // device copy of the stream-K piece table (consumer kernels)
       void* d = nullptr;
       check_cuda(cudaMalloc(&d, p.tile_pieces.size()), "piece table");
@@ -459,7 +460,7 @@ void Engine::forward_draft(ModelDev& m, Lane& ln, const FwdShape& sh, AttnGeom g
     eh.amax_val = ln.amax_val;
     eh.amax_idx = ln.amax_idx;
     prof_begin(base + 1, s);
-    const GemmPlan& ph = plan(m.V, D, T, kGemmArgmax);
+    const GemmPlan& ph = plan(m.V, D, T, kGemmArgmax, ln.head_sms);
     eh.st = stamp_slot(15, 2 * ph.grid);
     check_cuda(gemm_launch(ph, m.head, ln.xn, eh, s, opts_.use_pdl != 0), "gemm lm_head");
     prof_end(s, wbytes(m.V, D));
@@ -991,6 +992,17 @@ void Engine::capture_round(RoundPlan& p) {
   record_timing(ev_start_, s);
   check_cuda(cudaMemcpyAsync(d_in_, pin_in_, p.in_ints * 4, cudaMemcpyHostToDevice, s), "h2d lists");
   check_cuda(cudaEventRecord(ev_fork_, s), "event");
+  // The deepest active SSM's step chain bounds the draft phase; the others run beside it and
+  // their lm_head (a 49-MB weight stream over every SM) stalls its latency-bound kernels, so
+  // theirs may be held to fewer SMs (SPIN_MINOR_HEAD_SMS; 0 = all).
+  static const int minor_head_sms = [] {
+    const char* e = std::getenv("SPIN_MINOR_HEAD_SMS");
+    return e ? std::atoi(e) : 0;
+  }();
+  int crit = -1;
+  for (int j = 0; j < M; ++j)
+    if (p.n_ssm[j] > 0 && (crit < 0 || ssm_[j].L > ssm_[crit].L)) crit = j;
+  for (int j = 0; j < M; ++j) slane_[j].head_sms = (j == crit) ? 0 : minor_head_sms;
   for (int j = 0; j < M; ++j) {
     cudaStream_t sj = ss_[j];
     check_cuda(cudaStreamWaitEvent(sj, ev_fork_, 0), "fork");

@@ -50,6 +50,7 @@ struct Lane {
   float* amax_val = nullptr;
   int32_t* amax_idx = nullptr;
   float* logits = nullptr;
+  int head_sms = 0;  // SMs the lm_head GEMM may use (0 = all): off the critical chain, fewer
   std::vector<void*> allocs;
 };
 
@@ -203,8 +204,8 @@ class Engine {
   SlotState st_{};
   cudaStream_t sv_ = nullptr;
   std::vector<cudaStream_t> ss_;
-  std::map<std::tuple<int, int, int, int>, GemmPlan> plans_;
-  const GemmPlan& plan(int n_out, int k, int t, int mode);
+  std::map<std::tuple<int, int, int, int, int>, GemmPlan> plans_;
+  const GemmPlan& plan(int n_out, int k, int t, int mode, int sms = 0);  // sms: SMs the plan may use (0 = all)
   std::vector<void*> plan_tables_;
 
   // host mirror of the per-slot state

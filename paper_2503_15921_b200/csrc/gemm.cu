@@ -508,6 +508,7 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
     // on the config-2 draft loop).
     constexpr long long kMinUnits = 4;
     m.grid = static_cast<int>(std::min<long long>(num_sms, std::max<long long>(1, (m.units + kMinUnits - 1) / kMinUnits)));
+
     // A few SMs fewer can cut the worst-case pieces per tile (e.g. 144 CTAs split every
     // 64-k-block QKV tile into exactly 2 pieces where 148 leave some with 3): the consumer
     // re-reads max_pieces partials per element. Search down to grid - kGridSlack.
