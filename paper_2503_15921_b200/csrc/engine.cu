@@ -635,6 +635,31 @@ void Engine::sync_sv(const char* what) {
         for (size_t m = 0; m < ssm_.size(); ++m)
           st += " " + std::to_string(h_ssm_len_[m * opts_.max_requests + slot]);
       }
+      // diagnostics: non-finite K/V entries of the slot in that model's cache, per layer
+      if (slot >= 0 && slot < opts_.max_requests && cudaDeviceSynchronize() == cudaSuccess) {
+        ModelDev& md = (e == 3 && j >= 0 && j < static_cast<int>(ssm_.size())) ? ssm_[j] : target_;
+        const int c = h_committed_[slot];
+        const size_t rowel = static_cast<size_t>(md.hd);
+        std::vector<uint16_t> buf(static_cast<size_t>(c) * rowel);
+        for (int l = 0; l < md.L; ++l) {
+          int bad_k = 0, bad_v = 0, first = -1;
+          for (int h = 0; h < md.H; ++h) {
+            const size_t off = (((static_cast<size_t>(l) * opts_.max_requests + slot) * md.H + h) * opts_.max_ctx) * rowel;
+            for (int kv = 0; kv < 2; ++kv) {
+              cudaMemcpy(buf.data(), (kv ? md.vc : md.kc) + off, buf.size() * 2, cudaMemcpyDeviceToHost);
+              for (size_t i = 0; i < buf.size(); ++i)
+                if ((buf[i] & 0x7f80) == 0x7f80) {
+                  (kv ? bad_v : bad_k)++;
+                  const int pos = static_cast<int>(i / rowel);
+                  if (first < 0 || pos < first) first = pos;
+                }
+            }
+          }
+          if (bad_k || bad_v)
+            st += " | layer " + std::to_string(l) + ": non-finite K " + std::to_string(bad_k) + " V " +
+                  std::to_string(bad_v) + " first pos " + std::to_string(first);
+        }
+      }
       fail(SPIN_CUDA_ERROR, std::string(what) + ": non-finite logits (argmax undefined): " + st);
     }
     fail(SPIN_CAPACITY_ERROR, std::string(what) + (e == 2 ? ": a round would commit past max_ctx"
