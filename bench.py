@@ -609,7 +609,12 @@ def main():
         dev_ms_max = ranks.max(dev_ms)
         tokens_total = ranks.sum(float(emitted.sum()))
         value = tokens_total / (dev_ms_max / 1e3)
-        # ---- e2e: public per-slot call with host buffers + per-step stats gather
+        # ---- e2e: public per-slot call with host buffers + per-step stats gather, over the SAME
+        # rounds as `value` (re-prefilled, same warm-up: greedy decoding repeats them token for
+        # token), so the two differ only by the host path, not by longer contexts
+        eng.prefill(range(BATCH), prompts)
+        for _ in range(args.warmup):
+            eng.round(slots, assign)
         verify_us, draft_us, committed = [], [], None
         ranks.barrier()
         t0 = time.perf_counter()
