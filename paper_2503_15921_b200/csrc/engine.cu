@@ -303,6 +303,7 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
   }
   prof_begin(base + 3, s);
   launch_embed_norm(m.emb, ln.meta, T, D, eps, ln.h, ln.xn, s);
+  if (ln.serial) check_cuda(cudaStreamSynchronize(s), "serial: embed");
   prof_end(s, 0);
   GemmEpilogue ep;
   ep.mode = kGemmPartial;
@@ -324,11 +325,13 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     const bool stamp_layer = &m == &target_ && l == 1;
     ep.st = stamp_layer ? stamp_slot(10, 2 * pq.grid) : nullptr;
     check_cuda(gemm_launch(pq, w.qkv, ln.xn, ep, s, pdl), "gemm qkv");
+    if (ln.serial) check_cuda(cudaStreamSynchronize(s), "serial: gemm qkv");
     prof_end(s, gemm_bytes(3 * D, D));
     if (!(skip & 1)) {
       prof_begin(base + 3, s);
       launch_qkv_epilogue(ln.part, pq.map, ln.meta, T, g, m.rcos, m.rsin, ln.q, s,
                           stamp_layer ? stamp_slot(16, qkv_epilogue_blocks(T, m.H * m.hd)) : nullptr);
+      if (ln.serial) check_cuda(cudaStreamSynchronize(s), "serial: qkv epilogue");
       prof_end(s, 0);
     }
     prof_begin(base + 2, s);
@@ -798,6 +801,37 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
         static const bool with_drafts = std::getenv("SPIN_PREWARM_WITH_DRAFTS") != nullptr;
         if (!with_drafts) check_cuda(cudaStreamWaitEvent(ps, ev_draft_, 0), "prewarm after drafts");
         extend(static_cast<int>(j), jobs[j], ps, &pwlane_[j], pw_pin_[j], pw_pin_cap_);
+        static const bool pw_check = std::getenv("SPIN_PREWARM_CHECK") != nullptr;  // debugging
+        if (pw_check) {  // the recomputed rows, right after the catch-up completes
+          check_cuda(cudaStreamSynchronize(ps), "prewarm check");
+          ModelDev& md = ssm_[j];
+          std::vector<uint16_t> row(md.hd);
+          for (const auto& [slot, from, to] : jobs[j])
+            for (int l = 0; l < md.L; ++l)
+              for (int kv = 0; kv < 2; ++kv) {
+                int bad = 0, first = -1;
+                for (int h = 0; h < md.H; ++h)
+                  for (int p = from; p < to; ++p) {
+                    const size_t off = ((((static_cast<size_t>(l) * opts_.max_requests + slot) * md.H + h) *
+                                         opts_.max_ctx) + p) * md.hd;
+                    cudaMemcpy(row.data(), (kv ? md.vc : md.kc) + off, md.hd * 2, cudaMemcpyDeviceToHost);
+                    for (int i = 0; i < md.hd; ++i)
+                      if ((row[i] & 0x7f80) == 0x7f80) {
+                        if (bad == 0) {
+                          std::fprintf(stderr, "prewarm check: first bad row ssm %zu slot %d layer %d %s head %d pos %d:",
+                                       j, slot, l, kv ? "V" : "K", h, p);
+                          for (int q = 0; q < md.hd; ++q) std::fprintf(stderr, " %04x", row[q]);
+                          std::fprintf(stderr, "\n");
+                        }
+                        ++bad;
+                        if (first < 0 || p < first) first = p;
+                      }
+                  }
+                if (bad)
+                  std::fprintf(stderr, "prewarm check: ssm %zu slot %d [%d,%d) layer %d %s non-finite %d first %d\n", j,
+                               slot, from, to, l, kv ? "V" : "K", bad, first);
+              }
+        }
         for (const auto& r : jobs[j]) {
           const size_t idx = j * opts_.max_requests + std::get<0>(r);
           pw_len_pin_[j][std::get<0>(r)] = std::get<2>(r);
@@ -822,6 +856,7 @@ void Engine::init_prewarm() {
   pw_len_pin_.assign(M, nullptr);
   for (int j = 0; j < M; ++j) {
     init_lane(pwlane_[j], ssm_[j], kExtendRows, kExtendRows, false);
+    pwlane_[j].serial = std::getenv("SPIN_PREWARM_SERIAL") != nullptr;  // debugging
     check_cuda(cudaMallocHost(&pw_pin_[j], pw_pin_cap_ * 4), "prewarm staging");
     check_cuda(cudaMallocHost(&pw_len_pin_[j], static_cast<size_t>(R) * 4), "prewarm staging");
   }
@@ -1291,6 +1326,8 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, const int
     last_verify_rows_ = 0;  // the in-situ kernel replays expect a serial round's layout
   } else {
     RoundPlan& p = plan_round(n, slots, ssm_of);
+    static const bool pw_first = std::getenv("SPIN_PREWARM_FIRST") != nullptr;  // debugging
+    if (prewarm && pw_first) enqueue_prewarm(n, slots, prewarm, ssm_of);
     // stage the lists
     std::vector<int> act;
     for (int i = 0; i < n; ++i)
@@ -1315,7 +1352,7 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, const int
       capture_round(p);
     }
     // destinations of future switches recomputed on idle streams while this round runs
-    if (prewarm) enqueue_prewarm(n, slots, prewarm, ssm_of);
+    if (prewarm && !pw_first) enqueue_prewarm(n, slots, prewarm, ssm_of);
     static const bool pw_sync = std::getenv("SPIN_PREWARM_SYNC") != nullptr;  // debugging: no overlap
     if (prewarm && pw_sync) {
       sync_sv("round (before prewarm)");

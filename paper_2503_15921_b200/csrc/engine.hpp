@@ -51,6 +51,7 @@ struct Lane {
   int32_t* amax_idx = nullptr;
   float* logits = nullptr;
   int head_sms = 0;  // SMs the lm_head GEMM may use (0 = all): off the critical chain, fewer
+  bool serial = false;  // debugging: synchronise the stream after every launch of this lane
   std::vector<void*> allocs;
 };
 

@@ -231,9 +231,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (P2) {
-        // producer tail: every stage released by the leader's MMAs, so none of its commits is
-        // still in flight towards our barriers when the CTAs leave
+      {
+        // producer tail: every stage released by the MMAs (the leader's, in a pair), so no
+        // tcgen05.commit arrival is still in flight towards our barriers when the CTA leaves --
+        // a late arrival would land in the shared memory of the next CTA on this SM
         for (int i = 0; i < stages; ++i) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           if (++stage == stages) {
@@ -454,16 +455,15 @@ GemmPlan gemm_plan(int n_out, int k, int t, int mode, int num_sms) {
   p.n_mtiles = (n_out + kBlockM - 1) / kBlockM;
   p.kb = (k + kBlockK - 1) / kBlockK;
   const long long n_tiles = static_cast<long long>(p.n_mtiles) * p.n_ntiles;
-  // CTA pairs (cta_group::2, PieceMap::pair) from this many token rows (0 = never). Worth it above
-  // one token tile (tools/gemm_time_probe.py: T = 1280 QKV 105.3 -> 100.4 us, gate_up 184.9 ->
-  // 175.4; at T = 160 QKV 23.2 -> 24.6), and parity-green alone (tests/test_gpu_gemm.py) and in
-  // every engine test -- but OFF by default: pair GEMMs of a prewarm catch-up running beside the
-  // SSM draft kernels left garbage in some partial tiles (NaN V rows of a 68M layer, config 4
-  // with SPIN_PREWARM_WITH_DRAFTS=1; clean with pairs off), not yet root-caused.
-  // SPIN_GEMM_PAIR_MIN_T=257 opts in.
+  // CTA pairs (cta_group::2, PieceMap::pair) from this many token rows (0 = never): above one
+  // token tile (tools/gemm_time_probe.py: T = 1280 QKV 105.3 -> 100.4 us, gate_up 184.9 ->
+  // 175.4); at T = 160 the weight stream bounds the k-loop and a pair's coarser stream-K units
+  // cost more than the halved token operand saves (QKV 23.2 -> 24.6 us). (A config-4 failure
+  // first blamed on pairs was the prewarm race of DESIGN.md section 8: it reproduces with pairs
+  // off and not with pairs on once the catch-up waits for the drafts.)
   static const int pair_min_t = [] {
     const char* e = std::getenv("SPIN_GEMM_PAIR_MIN_T");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 257;
   }();
   const bool paired = mode == kGemmPartial && pair_min_t > 0 && t >= pair_min_t && p.n_mtiles % 2 == 0 &&
                       p.bn % 32 == 0;
