@@ -801,8 +801,49 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
         static const bool with_drafts = std::getenv("SPIN_PREWARM_WITH_DRAFTS") != nullptr;
         if (!with_drafts) check_cuda(cudaStreamWaitEvent(ps, ev_draft_, 0), "prewarm after drafts");
         extend(static_cast<int>(j), jobs[j], ps, &pwlane_[j], pw_pin_[j], pw_pin_cap_);
-        static const bool pw_check = std::getenv("SPIN_PREWARM_CHECK") != nullptr;  // debugging
-        if (pw_check) {  // the recomputed rows, right after the catch-up completes
+        static const int pw_check = [] {
+          const char* e = std::getenv("SPIN_PREWARM_CHECK");  // debugging: 1 non-finite scan, 2 + redo and diff
+          return e ? std::atoi(e) : 0;
+        }();
+        if (pw_check == 2) {  // snapshot the rows, recompute them once the round is over, diff
+          check_cuda(cudaStreamSynchronize(ps), "prewarm check");
+          ModelDev& md = ssm_[j];
+          auto snap = [&](std::vector<uint16_t>& out) {
+            out.clear();
+            std::vector<uint16_t> row(md.hd);
+            for (const auto& [slot, from, to] : jobs[j])
+              for (int l = 0; l < md.L; ++l)
+                for (int kv = 0; kv < 2; ++kv)
+                  for (int h = 0; h < md.H; ++h)
+                    for (int p = from; p < to; ++p) {
+                      const size_t off = ((((static_cast<size_t>(l) * opts_.max_requests + slot) * md.H + h) *
+                                           opts_.max_ctx) + p) * md.hd;
+                      cudaMemcpy(row.data(), (kv ? md.vc : md.kc) + off, md.hd * 2, cudaMemcpyDeviceToHost);
+                      out.insert(out.end(), row.begin(), row.end());
+                    }
+          };
+          std::vector<uint16_t> a, b;
+          snap(a);
+          check_cuda(cudaEventSynchronize(ev_end_), "prewarm check: round end");
+          extend(static_cast<int>(j), jobs[j], ps, &pwlane_[j], pw_pin_[j], pw_pin_cap_);
+          check_cuda(cudaStreamSynchronize(ps), "prewarm check redo");
+          snap(b);
+          size_t idx = 0;
+          for (const auto& [slot, from, to] : jobs[j])
+            for (int l = 0; l < md.L; ++l)
+              for (int kv = 0; kv < 2; ++kv) {
+                int diff_rows = 0, first_h = -1, first_p = -1;
+                for (int h = 0; h < md.H; ++h)
+                  for (int p = from; p < to; ++p, idx += md.hd)
+                    if (std::memcmp(a.data() + idx, b.data() + idx, md.hd * 2) != 0) {
+                      if (diff_rows++ == 0) first_h = h, first_p = p;
+                    }
+                if (diff_rows)
+                  std::fprintf(stderr, "prewarm diff: ssm %zu slot %d [%d,%d) layer %d %s rows %d of %d, first head %d pos %d\n",
+                               j, slot, from, to, l, kv ? "V" : "K", diff_rows, md.H * (to - from), first_h, first_p);
+              }
+        }
+        if (pw_check == 1) {  // the recomputed rows, right after the catch-up completes
           check_cuda(cudaStreamSynchronize(ps), "prewarm check");
           ModelDev& md = ssm_[j];
           std::vector<uint16_t> row(md.hd);

@@ -13,7 +13,7 @@ tgt = LLAMA_13B_DOM if os.environ.get("TGT") == "13b" else replace(LLAMA_7B, pla
 ssms = (LLAMA_68M_DOM, LLAMA_160M_DOM, LLAMA_160M_B_DOM)
 eng = Engine(tgt, ssms, max_requests=B, max_ctx=1024, window=W, use_graphs=os.environ.get("GRAPHS", "1") == "1", use_pdl=os.environ.get("PDL", "1") == "1")
 eng.prefill(range(B), domain_prompts(B, 128, 512, tgt.vocab, 4, 7))
-rng = np.random.default_rng(11)
+rng = np.random.default_rng(int(os.environ.get("SEED", "11")))
 mode = os.environ.get("PLAN", "random")
 if mode == "random":
     plans = [rng.integers(0, 3, B).astype(np.int32) for _ in range(R + 1)]
