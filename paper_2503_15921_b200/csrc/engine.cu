@@ -710,6 +710,8 @@ void Engine::extend(int model, const std::vector<std::tuple<int, int, int>>& ran
       }
       check_cuda(cudaMemcpyAsync(dst[k], from, cnt[k] * 4, cudaMemcpyHostToDevice, s), "h2d");
     }
+    static const bool sync_copy = std::getenv("SPIN_EXTEND_SYNC_COPY") != nullptr;  // debugging
+    if (sync_copy) check_cuda(cudaStreamSynchronize(s), "extend: row metadata copied");
     MetaArgs a{};
     a.mode = kMetaExtend;
     a.n_req = R;
@@ -786,7 +788,9 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
   // never touches; join_prewarm() joins it before anything else is enqueued.
   int dev = 0;
   check_cuda(cudaGetDevice(&dev), "device");
-  pw_thread_ = std::thread([this, dev, jobs = std::move(jobs)]() {
+  std::vector<int> drafting_on(R, -1);  // debugging (SPIN_PREWARM_CHECK=3): this round's SSM per slot
+  for (int i = 0; i < n; ++i) drafting_on[slots[i]] = ssm_of ? ssm_of[i] : -1;
+  pw_thread_ = std::thread([this, dev, jobs = std::move(jobs), drafting_on]() {
     try {
       check_cuda(cudaSetDevice(dev), "cudaSetDevice");
       for (size_t j = 0; j < jobs.size(); ++j) {
@@ -800,7 +804,40 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
         // so little hiding is lost. SPIN_PREWARM_WITH_DRAFTS=1 restores full overlap (debugging).
         static const bool with_drafts = std::getenv("SPIN_PREWARM_WITH_DRAFTS") != nullptr;
         if (!with_drafts) check_cuda(cudaStreamWaitEvent(ps, ev_draft_, 0), "prewarm after drafts");
+        static const bool whole_check = [] {
+          const char* e = std::getenv("SPIN_PREWARM_CHECK");
+          return e && std::atoi(e) == 3;
+        }();
+        ModelDev& mdw = ssm_[j];
+        const size_t kv_elems = static_cast<size_t>(mdw.L) * opts_.max_requests * mdw.H * opts_.max_ctx * mdw.hd;
+        const std::vector<uint16_t>& before = dbg_kv_before_[j];  // taken by round() before its launch
         extend(static_cast<int>(j), jobs[j], ps, &pwlane_[j], pw_pin_[j], pw_pin_cap_);
+        if (whole_check && before.size() == 2 * kv_elems) {
+          check_cuda(cudaDeviceSynchronize(), "whole check");  // catch-up and round both done
+          std::vector<uint16_t> after(2 * kv_elems);
+          check_cuda(cudaMemcpy(after.data(), mdw.kc, kv_elems * 2, cudaMemcpyDeviceToHost), "snap k");
+          check_cuda(cudaMemcpy(after.data() + kv_elems, mdw.vc, kv_elems * 2, cudaMemcpyDeviceToHost), "snap v");
+          std::vector<int> job_from(opts_.max_requests, -1), job_to(opts_.max_requests, -1);
+          for (const auto& [slot, from, to] : jobs[j]) job_from[slot] = from, job_to[slot] = to;
+          int unexpected = 0;
+          for (size_t e = 0; e < 2 * kv_elems; e += mdw.hd) {
+            if (std::memcmp(before.data() + e, after.data() + e, mdw.hd * 2) == 0) continue;
+            size_t r = (e % kv_elems) / mdw.hd;
+            const int pos = static_cast<int>(r % opts_.max_ctx);
+            r /= opts_.max_ctx;
+            const int head = static_cast<int>(r % mdw.H);
+            r /= mdw.H;
+            const int slot = static_cast<int>(r % opts_.max_requests), layer = static_cast<int>(r / opts_.max_requests);
+            const bool in_job = pos >= job_from[slot] && pos < job_to[slot];
+            const bool draft = drafting_on[slot] == static_cast<int>(j) && pos >= h_committed_[slot] - 2 - 8;
+            if (!in_job && !draft && unexpected++ < 6)
+              std::fprintf(stderr, "prewarm whole check: ssm %zu unexpected change %s layer %d slot %d head %d pos %d "
+                                   "(slot drafts on %d, committed %d)\n",
+                           j, e < kv_elems ? "K" : "V", layer, slot, head, pos, drafting_on[slot],
+                           h_committed_[slot]);
+          }
+          if (unexpected) std::fprintf(stderr, "prewarm whole check: ssm %zu %d unexpected rows\n", j, unexpected);
+        }
         static const int pw_check = [] {
           const char* e = std::getenv("SPIN_PREWARM_CHECK");  // debugging: 1 non-finite scan, 2 + redo and diff
           return e ? std::atoi(e) : 0;
@@ -823,8 +860,25 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
                     }
           };
           std::vector<uint16_t> a, b;
+          auto tok_hash = [&]() {
+            uint64_t hsh = 1469598103934665603ull;
+            for (const auto& [slot, from, to] : jobs[j])
+              for (int p = from; p < to; ++p)
+                hsh = (hsh ^ static_cast<uint32_t>(h_tokens_[static_cast<size_t>(slot) * opts_.max_ctx + p])) *
+                      1099511628211ull;
+            return hsh;
+          };
+          const uint64_t th0 = tok_hash();
+          {
+            std::string js;
+            for (const auto& [slot, from, to] : jobs[j])
+              js += " " + std::to_string(slot) + ":[" + std::to_string(from) + "," + std::to_string(to) + ")";
+            std::fprintf(stderr, "prewarm job ssm %zu:%s\n", j, js.c_str());
+          }
           snap(a);
           check_cuda(cudaEventSynchronize(ev_end_), "prewarm check: round end");
+          const uint64_t th1 = tok_hash();
+          if (th0 != th1) std::fprintf(stderr, "prewarm check: host tokens of ssm %zu's job changed during the round\n", j);
           extend(static_cast<int>(j), jobs[j], ps, &pwlane_[j], pw_pin_[j], pw_pin_cap_);
           check_cuda(cudaStreamSynchronize(ps), "prewarm check redo");
           snap(b);
@@ -1367,6 +1421,21 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, const int
     last_verify_rows_ = 0;  // the in-situ kernel replays expect a serial round's layout
   } else {
     RoundPlan& p = plan_round(n, slots, ssm_of);
+    static const bool whole_check = [] {
+      const char* e = std::getenv("SPIN_PREWARM_CHECK");
+      return e && std::atoi(e) == 3;
+    }();
+    if (whole_check && prewarm) {  // debugging: every SSM cache before the round (see enqueue_prewarm)
+      check_cuda(cudaDeviceSynchronize(), "whole check");
+      dbg_kv_before_.resize(ssm_.size());
+      for (size_t jj = 0; jj < ssm_.size(); ++jj) {
+        ModelDev& md = ssm_[jj];
+        const size_t e = static_cast<size_t>(md.L) * opts_.max_requests * md.H * opts_.max_ctx * md.hd;
+        dbg_kv_before_[jj].resize(2 * e);
+        check_cuda(cudaMemcpy(dbg_kv_before_[jj].data(), md.kc, e * 2, cudaMemcpyDeviceToHost), "snap k");
+        check_cuda(cudaMemcpy(dbg_kv_before_[jj].data() + e, md.vc, e * 2, cudaMemcpyDeviceToHost), "snap v");
+      }
+    }
     static const bool pw_first = std::getenv("SPIN_PREWARM_FIRST") != nullptr;  // debugging
     if (prewarm && pw_first) enqueue_prewarm(n, slots, prewarm, ssm_of);
     // stage the lists

@@ -185,6 +185,7 @@ class Engine {
   bool prof_ = false;
   std::atomic<int64_t> launches_{0};
   std::mutex plan_mu_;  // plans_ is shared with the prewarm thread
+  std::vector<std::vector<uint16_t>> dbg_kv_before_;  // SPIN_PREWARM_CHECK=3 snapshots
   struct ProfRec {
     int cat;
     cudaEvent_t a, b;

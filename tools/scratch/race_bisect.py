@@ -22,8 +22,11 @@ else:  # "split": drafting only on SSMs 0/1 in even rounds and SSM 2 in odd roun
     plans = [(rng.integers(0, 2, B) if r % 2 == 0 else np.full(B, 2)).astype(np.int32) for r in range(R + 1)]
 slots = np.arange(B, dtype=np.int32)
 err = None
+verbose = os.environ.get("VERBOSE") == "1"
 for r in range(R):
     pw = np.where(plans[r + 1] != plans[r], plans[r + 1], -1).astype(np.int32)
+    if verbose:
+        print(f"round {r} assign {plans[r].tolist()} prewarm {pw.tolist()}", file=sys.stderr, flush=True)
     try:
         eng.round(slots, plans[r], prewarm=pw)
     except Exception as e:
