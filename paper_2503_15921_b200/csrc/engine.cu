@@ -790,7 +790,8 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
   check_cuda(cudaGetDevice(&dev), "device");
   std::vector<int> drafting_on(R, -1);  // debugging (SPIN_PREWARM_CHECK=3): this round's SSM per slot
   for (int i = 0; i < n; ++i) drafting_on[slots[i]] = ssm_of ? ssm_of[i] : -1;
-  pw_thread_ = std::thread([this, dev, jobs = std::move(jobs), drafting_on]() {
+  const bool pipe_drafts = pipelined();  // the slot just launched ran micro-batched units
+  pw_thread_ = std::thread([this, dev, pipe_drafts, jobs = std::move(jobs), drafting_on]() {
     try {
       check_cuda(cudaSetDevice(dev), "cudaSetDevice");
       for (size_t j = 0; j < jobs.size(); ++j) {
@@ -803,7 +804,13 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
         // an interaction not yet root-caused. The verify is the long phase (7 ms of 8.5 at 13B),
         // so little hiding is lost. SPIN_PREWARM_WITH_DRAFTS=1 restores full overlap (debugging).
         static const bool with_drafts = std::getenv("SPIN_PREWARM_WITH_DRAFTS") != nullptr;
-        if (!with_drafts) check_cuda(cudaStreamWaitEvent(ps, ev_draft_, 0), "prewarm after drafts");
+        if (!with_drafts) {
+          if (pipe_drafts)  // micro-batched slot: every SSM stream's last unit draft (launch_pipe_slot)
+            for (size_t jj = 0; jj < ev_join_.size(); ++jj)
+              check_cuda(cudaStreamWaitEvent(ps, ev_join_[jj], 0), "prewarm after drafts");
+          else
+            check_cuda(cudaStreamWaitEvent(ps, ev_draft_, 0), "prewarm after drafts");
+        }
         static const bool whole_check = [] {
           const char* e = std::getenv("SPIN_PREWARM_CHECK");
           return e && std::atoi(e) == 3;
@@ -1287,6 +1294,8 @@ void Engine::launch_pipe_slot(PipePlan& pp, bool first, bool host_round) {
     check_cuda(cudaEventRecord(u.t_d, sj), "event");
     check_cuda(cudaEventRecord(u.ev_d, sj), "event");
   }
+  // the slot's draft phase on every SSM stream (a prewarm catch-up waits for it, enqueue_prewarm)
+  for (size_t j = 0; j < ssm_.size(); ++j) check_cuda(cudaEventRecord(ev_join_[j], ss_[j]), "drafts done");
   for (int k : pp.vorder) {
     PipeUnit& u = pp.units[k];
     check_cuda(cudaStreamWaitEvent(sv_, u.ev_d, 0), "unit drafted");

@@ -17,9 +17,11 @@ pytestmark = pytest.mark.gpu
 B, W, R = 32, 4, 24
 
 
-def _run(prewarm: bool):
+def _run(prewarm: bool, micro_batches=None):
     tgt = replace(LLAMA_7B, planted_domains=4, planted_gain=20.0)
     eng = Engine(tgt, (LLAMA_68M_DOM, LLAMA_160M_DOM, LLAMA_160M_B_DOM), max_requests=B, max_ctx=1024, window=W)
+    if micro_batches is not None:
+        eng.set_micro_batches(micro_batches)
     eng.prefill(range(B), domain_prompts(B, 128, 512, tgt.vocab, 4, 7))
     rng = np.random.default_rng(11)
     plans = [rng.integers(0, 3, B).astype(np.int32) for _ in range(R + 1)]
@@ -34,5 +36,13 @@ def _run(prewarm: bool):
 
 def test_prewarm_keeps_outcomes_under_concurrency():
     a, b = _run(True), _run(False)
+    for i in range(B):
+        assert np.array_equal(a[i], b[i]), i
+
+
+def test_prewarm_keeps_outcomes_with_micro_batched_slots():
+    """The same under f1 pipelining: micro-batched units per SSM (the catch-up waits for every
+    SSM stream's last unit draft of the slot)."""
+    a, b = _run(True, [2, 2, 2]), _run(False, [2, 2, 2])
     for i in range(B):
         assert np.array_equal(a[i], b[i]), i
