@@ -231,15 +231,16 @@ void Engine::init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool l
   ln.act = dalloc<bf16>(A, static_cast<size_t>(T_cap) * m.F);
   ln.ssp = dalloc<float>(A, static_cast<size_t>(m.D / 16 + 1) * std::min(T_cap, kDraftMaxT));
   ln.hb = dalloc<bf16>(A, static_cast<size_t>(std::min(T_cap, kDraftMaxT)) * m.D);
+  // split-K partials of the largest plan over EVERY row count this lane can run (pieces per tile
+  // vary irregularly with T, and the GEMM writes them with TMA stores bounded only by the plan's
+  // tensor map, not by this allocation); gemm_plan directly, so no plan is cached for each T
   size_t part = 0;
   const int shapes[4][2] = {{3 * m.D, m.D}, {m.D, m.D}, {2 * m.F, m.D}, {m.D, m.F}};
-  for (auto& sh : shapes) {
-    for (int t = std::min(256, T_cap);; t = std::min(t + 256, T_cap)) {
-      const GemmPlan& p = plan(sh[0], sh[1], t, kGemmPartial);
+  for (auto& sh : shapes)
+    for (int t = 1; t <= T_cap; ++t) {
+      const GemmPlan p = gemm_plan(sh[0], sh[1], t, kGemmPartial, num_sms_);
       part = std::max(part, static_cast<size_t>(p.max_pieces) * t * sh[0]);
-      if (t == T_cap) break;
     }
-  }
   ln.part = dalloc<float>(A, part);
   // attention work list + split-KV partials: pieces <= segments + rows x (chunks - 1), and
   // rows x chunks x heads ~ 8 x SMs bounds the chunk splits (attn_chunks); partial slots
