@@ -1085,7 +1085,7 @@ void launch_decode_st(const FwdMeta& m, int n_rows, const AttnGeom& g, const flo
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_allowed();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cfg.stream = s;
@@ -1133,7 +1133,7 @@ void launch_t(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_allowed();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cfg.stream = s;
@@ -1158,7 +1158,7 @@ void launch_ws(const FwdMeta& m, int n_rows, const AttnGeom& g, const float* q, 
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_allowed();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cfg.stream = s;

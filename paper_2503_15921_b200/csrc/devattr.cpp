@@ -1,6 +1,8 @@
 // Per-device kernel attribute bookkeeping (gemm.cuh ensure_smem_optin).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <map>
 #include <mutex>
 #include <utility>
@@ -21,6 +23,11 @@ cudaError_t ensure_smem_optin(const void* kernel, size_t bytes) {
   const cudaError_t r = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
   if (r == cudaSuccess) have = bytes;
   return r;
+}
+
+int pdl_allowed() {
+  static const int v = std::getenv("SPIN_NO_PDL") != nullptr ? 0 : 1;
+  return v;
 }
 
 }  // namespace spin

@@ -594,7 +594,7 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
   int na = 0;
   if (pdl) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    attr[na++].val.programmaticStreamSerializationAllowed = pdl_allowed();
   }
   if (plan.map.pair > 1) {
     attr[na].id = cudaLaunchAttributeClusterDimension;

@@ -109,4 +109,8 @@ bool encode_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_
 // attribute is per device context, so a second spin_ctx on another GPU needs its own).
 cudaError_t ensure_smem_optin(const void* kernel, size_t bytes);
 
+// Programmatic dependent launch on every kernel launch (1), or off everywhere (SPIN_NO_PDL=1,
+// debugging: every kernel then waits for its predecessor's completion before it starts).
+int pdl_allowed();
+
 }  // namespace spin
