@@ -63,7 +63,7 @@ FwdMeta alloc_meta(DevAllocs& A, int n_req, int rows, int chunks) {
   m.req_plist = static_cast<int32_t*>(A.get(4 * static_cast<size_t>(piece_cap)));
   m.n_pieces = static_cast<int32_t*>(A.get(4));
   m.err = static_cast<int32_t*>(A.get(4));
-  check_cuda(cudaMemset(m.err, 0, 4), "memset");
+  check_cuda(zero_sync(m.err, 4), "memset");
   m.piece_cap = piece_cap;
   return m;
 }
@@ -344,10 +344,10 @@ spin_status spin_decomposed_attention(int32_t n_req, int32_t dim, const int32_t*
     const int32_t* d_rowseg = put(row_seg);
     const int32_t* d_s0 = put(req_seg0);
     const int32_t* d_ns = put(req_nseg);
-    check_cuda(cudaMemcpy(ib, host_ints.data(), host_ints.size() * 4, cudaMemcpyHostToDevice), "h2d");
-    check_cuda(cudaMemcpy(dq, q, bytes_d(nq), cudaMemcpyHostToDevice), "h2d");
-    check_cuda(cudaMemcpy(dk, k, bytes_d(nk), cudaMemcpyHostToDevice), "h2d");
-    check_cuda(cudaMemcpy(dv, v, bytes_d(nk), cudaMemcpyHostToDevice), "h2d");
+    check_cuda(upload_sync(ib, host_ints.data(), host_ints.size() * 4), "h2d");
+    check_cuda(upload_sync(dq, q, bytes_d(nq)), "h2d");
+    check_cuda(upload_sync(dk, k, bytes_d(nk)), "h2d");
+    check_cuda(upload_sync(dv, v, bytes_d(nk)), "h2d");
     launch_toy_attention(dq, dk, dv, d_qoff, d_kvoff, d_qrows, d_seg, n_segs, d_rowptr, d_rowseg, width, d_s0, d_ns,
                          n_req, dim, qmax, pm, pl, po, dout, nullptr);
     check_cuda(cudaGetLastError(), "toy attention");
@@ -594,7 +594,7 @@ spin_status spin_device_alloc(int32_t device, size_t bytes, void** ptr) {
     if (!ptr) fail(SPIN_INPUT_ERROR, "spin_device_alloc: null argument");
     check_cuda(cudaSetDevice(device), "cudaSetDevice");
     check_cuda(cudaMalloc(ptr, std::max<size_t>(bytes, 16)), "cudaMalloc");
-    check_cuda(cudaMemset(*ptr, 0, std::max<size_t>(bytes, 16)), "cudaMemset");
+    check_cuda(zero_sync(*ptr, std::max<size_t>(bytes, 16)), "cudaMemset");
   });
 }
 
@@ -607,7 +607,13 @@ spin_status spin_memcpy(void* dst, const void* src, size_t bytes, int32_t kind) 
     if (kind < 1 || kind > 3) fail(SPIN_INPUT_ERROR, "spin_memcpy: kind must be 1 (H2D), 2 (D2H) or 3 (D2D)");
     const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice : kind == 2 ? cudaMemcpyDeviceToHost
                                                                            : cudaMemcpyDeviceToDevice;
-    if (bytes > 0) check_cuda(cudaMemcpy(dst, src, bytes, k), "cudaMemcpy");
+    if (bytes == 0) return;
+    if (k == cudaMemcpyHostToDevice) {  // complete before return, whatever stream reads it next
+      check_cuda(upload_sync(dst, src, bytes), "cudaMemcpy");
+    } else {
+      check_cuda(cudaMemcpy(dst, src, bytes, k), "cudaMemcpy");
+      if (k == cudaMemcpyDeviceToDevice) check_cuda(cudaDeviceSynchronize(), "cudaMemcpy");  // D2D is asynchronous
+    }
   });
 }
 
@@ -634,10 +640,10 @@ spin_status spin_pack_device(const int32_t* kv_lens, int32_t n, int32_t width, i
     FwdMeta m = alloc_meta(allocs, n, nrows, 1);
     std::vector<int32_t> ones(n, 1), qs(n), zeros(n, 0);
     for (int i = 0; i < n; ++i) qs[i] = i;
-    check_cuda(cudaMemcpy(m.req_slot, zeros.data(), 4 * n, cudaMemcpyHostToDevice), "h2d");
-    check_cuda(cudaMemcpy(m.req_qstart, qs.data(), 4 * n, cudaMemcpyHostToDevice), "h2d");
-    check_cuda(cudaMemcpy(m.req_qlen, ones.data(), 4 * n, cudaMemcpyHostToDevice), "h2d");
-    check_cuda(cudaMemcpy(m.req_kvlen, kv_lens, 4 * n, cudaMemcpyHostToDevice), "h2d");
+    check_cuda(upload_sync(m.req_slot, zeros.data(), 4 * n), "h2d");
+    check_cuda(upload_sync(m.req_qstart, qs.data(), 4 * n), "h2d");
+    check_cuda(upload_sync(m.req_qlen, ones.data(), 4 * n), "h2d");
+    check_cuda(upload_sync(m.req_kvlen, kv_lens, 4 * n), "h2d");
     MetaArgs a{};
     a.mode = kMetaExtend;
     a.n_req = n;

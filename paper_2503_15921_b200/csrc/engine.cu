@@ -181,8 +181,8 @@ void Engine::init_model(ModelDev& m, const spin_model_desc& d, bool draft) {
     }
   check_cuda(cudaMalloc(&m.rcos, c.size() * 4), "rope");
   check_cuda(cudaMalloc(&m.rsin, s.size() * 4), "rope");
-  check_cuda(cudaMemcpy(m.rcos, c.data(), c.size() * 4, cudaMemcpyHostToDevice), "rope");
-  check_cuda(cudaMemcpy(m.rsin, s.data(), s.size() * 4, cudaMemcpyHostToDevice), "rope");
+  check_cuda(upload_sync(m.rcos, c.data(), c.size() * 4), "rope");
+  check_cuda(upload_sync(m.rsin, s.data(), s.size() * 4), "rope");
 }
 
 const GemmPlan& Engine::plan(int n_out, int k, int t, int mode, int sms) {
@@ -195,7 +195,7 @@ const GemmPlan& Engine::plan(int n_out, int k, int t, int mode, int sms) {
     if (!p.tile_pieces.empty()) {  // device copy of the stream-K piece table (consumer kernels)
       void* d = nullptr;
       check_cuda(cudaMalloc(&d, p.tile_pieces.size()), "piece table");
-      check_cuda(cudaMemcpy(d, p.tile_pieces.data(), p.tile_pieces.size(), cudaMemcpyHostToDevice), "piece table");
+      check_cuda(upload_sync(d, p.tile_pieces.data(), p.tile_pieces.size()), "piece table");
       p.map.tbl = static_cast<const uint8_t*>(d);
       plan_tables_.push_back(d);
     }
@@ -258,7 +258,7 @@ void Engine::init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool l
   ln.aw.part_l = dalloc<float>(A, np);
   ln.aw.part_o = dalloc<float>(A, np * m.hd);
   ln.aw.counter = dalloc<int32_t>(A, static_cast<size_t>(R_cap) * m.H);
-  check_cuda(cudaMemset(ln.aw.counter, 0, static_cast<size_t>(R_cap) * m.H * 4), "memset");
+  check_cuda(zero_sync(ln.aw.counter, static_cast<size_t>(R_cap) * m.H * 4), "memset");
   const int tiles = (m.V + 127) / 128;
   ln.amax_val = dalloc<float>(A, static_cast<size_t>(tiles) * T_cap);
   ln.amax_idx = dalloc<int32_t>(A, static_cast<size_t>(tiles) * T_cap);
@@ -292,19 +292,15 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
   auto gemm_bytes = [&](int n_out, int k) { return 2.0 * n_out * k + 2.0 * T * k + 2.0 * T * n_out; };
   AttnGeom g{m.H, m.hd, opts_.max_requests, opts_.max_ctx, 0, static_cast<float>(1.0 / std::sqrt(double(m.hd))),
              m.kc, m.vc};
-  // The fused draft kernels serve draft steps only (sh.early: every request's new KV rows are its
-  // query rows). Extends of <= 32 rows (switch catch-ups, prewarm chunks) take the generic
-  // kernels: fused extends running on a prewarm stream beside graph-launched draft steps
-  // produced NaN logits in the 13B config-4 LBSS loop (tools/scratch/repro_c4dom.py; a draft
-  // token of INT_MAX then faulted in embed_ss_kernel); the switch re-enables them for debugging.
-  static const bool fused_extends = std::getenv("SPIN_DRAFT_FUSED_EXTEND") != nullptr;
+  // Draft steps and extends of <= 32 rows (switch catch-ups, prewarm chunks) take the fused
+  // draft kernels; SPIN_DRAFT_NO_FUSED_EXTEND sends the extends to the generic ones (timing).
+  static const bool fused_extends = std::getenv("SPIN_DRAFT_NO_FUSED_EXTEND") == nullptr;
   if (m.sbuf != nullptr && head_mode != 2 && (sh.early || fused_extends) && draft_fused_supported(D, m.H, m.hd, F, T)) {
     forward_draft(m, ln, sh, g, s, head_mode);
     return;
   }
   prof_begin(base + 3, s);
   launch_embed_norm(m.emb, ln.meta, T, D, eps, ln.h, ln.xn, s);
-  if (ln.serial) check_cuda(cudaStreamSynchronize(s), "serial: embed");
   prof_end(s, 0);
   GemmEpilogue ep;
   ep.mode = kGemmPartial;
@@ -326,13 +322,11 @@ void Engine::forward(ModelDev& m, Lane& ln, const FwdShape& sh, cudaStream_t s, 
     const bool stamp_layer = &m == &target_ && l == 1;
     ep.st = stamp_layer ? stamp_slot(10, 2 * pq.grid) : nullptr;
     check_cuda(gemm_launch(pq, w.qkv, ln.xn, ep, s, pdl), "gemm qkv");
-    if (ln.serial) check_cuda(cudaStreamSynchronize(s), "serial: gemm qkv");
     prof_end(s, gemm_bytes(3 * D, D));
     if (!(skip & 1)) {
       prof_begin(base + 3, s);
       launch_qkv_epilogue(ln.part, pq.map, ln.meta, T, g, m.rcos, m.rsin, ln.q, s,
                           stamp_layer ? stamp_slot(16, qkv_epilogue_blocks(T, m.H * m.hd)) : nullptr);
-      if (ln.serial) check_cuda(cudaStreamSynchronize(s), "serial: qkv epilogue");
       prof_end(s, 0);
     }
     prof_begin(base + 2, s);
@@ -519,7 +513,7 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
     stamp_path_ = e;
     stamp_cap_ = size_t(8) << 20;
     check_cuda(cudaMalloc(&stamps_, stamp_cap_ * 8), "stamps");
-    check_cuda(cudaMemset(stamps_, 0, stamp_cap_ * 8), "stamps");
+    check_cuda(zero_sync(stamps_, stamp_cap_ * 8), "stamps");
   }
   check_cuda(cudaStreamCreateWithFlags(&sv_, cudaStreamNonBlocking), "stream");
   ss_.resize(n_ssm);
@@ -548,10 +542,10 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
   check_cuda(cudaMalloc(&st_.committed, R * 4), "committed");
   check_cuda(cudaMalloc(&st_.ssm_len, static_cast<size_t>(n_ssm) * R * 4), "ssm_len");
   check_cuda(cudaMalloc(&st_.drafts, static_cast<size_t>(R) * W * 4), "drafts");
-  check_cuda(cudaMemset(st_.tokens, 0, static_cast<size_t>(R) * opts.max_ctx * 4), "memset");
-  check_cuda(cudaMemset(st_.committed, 0, R * 4), "memset");
-  check_cuda(cudaMemset(st_.ssm_len, 0, static_cast<size_t>(n_ssm) * R * 4), "memset");
-  check_cuda(cudaMemset(st_.drafts, 0, static_cast<size_t>(R) * W * 4), "memset");
+  check_cuda(zero_sync(st_.tokens, static_cast<size_t>(R) * opts.max_ctx * 4), "memset");
+  check_cuda(zero_sync(st_.committed, R * 4), "memset");
+  check_cuda(zero_sync(st_.ssm_len, static_cast<size_t>(n_ssm) * R * 4), "memset");
+  check_cuda(zero_sync(st_.drafts, static_cast<size_t>(R) * W * 4), "memset");
   h_tokens_.assign(static_cast<size_t>(R) * opts.max_ctx, 0);
   h_committed_.assign(R, 0);
   h_ssm_len_.assign(static_cast<size_t>(n_ssm) * R, 0);
@@ -562,7 +556,7 @@ Engine::Engine(const spin_model_desc& target, const spin_model_desc* ssms, int n
   check_cuda(cudaMalloc(&d_in_, in_cap_ * 4), "in");
   check_cuda(cudaMalloc(&d_out_, out_cap_ * 4), "out");
   check_cuda(cudaMalloc(&d_emitted_, 8), "emitted");
-  check_cuda(cudaMemset(d_emitted_, 0, 8), "memset");
+  check_cuda(zero_sync(d_emitted_, 8), "memset");
   check_cuda(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   check_cuda(cudaEventCreate(&ev_start_), "event");
   check_cuda(cudaEventCreate(&ev_draft_), "event");
@@ -711,8 +705,6 @@ void Engine::extend(int model, const std::vector<std::tuple<int, int, int>>& ran
       }
       check_cuda(cudaMemcpyAsync(dst[k], from, cnt[k] * 4, cudaMemcpyHostToDevice, s), "h2d");
     }
-    static const bool sync_copy = std::getenv("SPIN_EXTEND_SYNC_COPY") != nullptr;  // debugging
-    if (sync_copy) check_cuda(cudaStreamSynchronize(s), "extend: row metadata copied");
     MetaArgs a{};
     a.mode = kMetaExtend;
     a.n_req = R;
@@ -789,152 +781,23 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
   // never touches; join_prewarm() joins it before anything else is enqueued.
   int dev = 0;
   check_cuda(cudaGetDevice(&dev), "device");
-  std::vector<int> drafting_on(R, -1);  // debugging (SPIN_PREWARM_CHECK=3): this round's SSM per slot
-  for (int i = 0; i < n; ++i) drafting_on[slots[i]] = ssm_of ? ssm_of[i] : -1;
   const bool pipe_drafts = pipelined();  // the slot just launched ran micro-batched units
-  pw_thread_ = std::thread([this, dev, pipe_drafts, jobs = std::move(jobs), drafting_on]() {
+  pw_thread_ = std::thread([this, dev, pipe_drafts, jobs = std::move(jobs)]() {
     try {
       check_cuda(cudaSetDevice(dev), "cudaSetDevice");
       for (size_t j = 0; j < jobs.size(); ++j) {
         if (jobs[j].empty()) continue;
         cudaStream_t ps = ps_[j];
         check_cuda(cudaEventSynchronize(ev_pw_[j]), "prewarm staging");  // staging reuse
-        // The catch-up overlaps the round's target verification, not its draft phase: run
-        // beside the fused draft kernels (graph replays) it left NaN logits in a later draft of
-        // the 13B config-4 LBSS loop (deterministic at one slot; tools/scratch/repro_c4dom.py),
-        // an interaction not yet root-caused. The verify is the long phase (7 ms of 8.5 at 13B),
-        // so little hiding is lost. SPIN_PREWARM_WITH_DRAFTS=1 restores full overlap (debugging).
-        static const bool with_drafts = std::getenv("SPIN_PREWARM_WITH_DRAFTS") != nullptr;
-        if (!with_drafts) {
+        static const bool after_drafts = std::getenv("SPIN_PREWARM_AFTER_DRAFTS") != nullptr;
+        if (after_drafts) {  // overlap the verification only (timing experiments)
           if (pipe_drafts)  // micro-batched slot: every SSM stream's last unit draft (launch_pipe_slot)
             for (size_t jj = 0; jj < ev_join_.size(); ++jj)
               check_cuda(cudaStreamWaitEvent(ps, ev_join_[jj], 0), "prewarm after drafts");
           else
             check_cuda(cudaStreamWaitEvent(ps, ev_draft_, 0), "prewarm after drafts");
         }
-        static const bool whole_check = [] {
-          const char* e = std::getenv("SPIN_PREWARM_CHECK");
-          return e && std::atoi(e) == 3;
-        }();
-        ModelDev& mdw = ssm_[j];
-        const size_t kv_elems = static_cast<size_t>(mdw.L) * opts_.max_requests * mdw.H * opts_.max_ctx * mdw.hd;
-        const std::vector<uint16_t>& before = dbg_kv_before_[j];  // taken by round() before its launch
         extend(static_cast<int>(j), jobs[j], ps, &pwlane_[j], pw_pin_[j], pw_pin_cap_);
-        if (whole_check && before.size() == 2 * kv_elems) {
-          check_cuda(cudaDeviceSynchronize(), "whole check");  // catch-up and round both done
-          std::vector<uint16_t> after(2 * kv_elems);
-          check_cuda(cudaMemcpy(after.data(), mdw.kc, kv_elems * 2, cudaMemcpyDeviceToHost), "snap k");
-          check_cuda(cudaMemcpy(after.data() + kv_elems, mdw.vc, kv_elems * 2, cudaMemcpyDeviceToHost), "snap v");
-          std::vector<int> job_from(opts_.max_requests, -1), job_to(opts_.max_requests, -1);
-          for (const auto& [slot, from, to] : jobs[j]) job_from[slot] = from, job_to[slot] = to;
-          int unexpected = 0;
-          for (size_t e = 0; e < 2 * kv_elems; e += mdw.hd) {
-            if (std::memcmp(before.data() + e, after.data() + e, mdw.hd * 2) == 0) continue;
-            size_t r = (e % kv_elems) / mdw.hd;
-            const int pos = static_cast<int>(r % opts_.max_ctx);
-            r /= opts_.max_ctx;
-            const int head = static_cast<int>(r % mdw.H);
-            r /= mdw.H;
-            const int slot = static_cast<int>(r % opts_.max_requests), layer = static_cast<int>(r / opts_.max_requests);
-            const bool in_job = pos >= job_from[slot] && pos < job_to[slot];
-            const bool draft = drafting_on[slot] == static_cast<int>(j) && pos >= h_committed_[slot] - 2 - 8;
-            if (!in_job && !draft && unexpected++ < 6)
-              std::fprintf(stderr, "prewarm whole check: ssm %zu unexpected change %s layer %d slot %d head %d pos %d "
-                                   "(slot drafts on %d, committed %d)\n",
-                           j, e < kv_elems ? "K" : "V", layer, slot, head, pos, drafting_on[slot],
-                           h_committed_[slot]);
-          }
-          if (unexpected) std::fprintf(stderr, "prewarm whole check: ssm %zu %d unexpected rows\n", j, unexpected);
-        }
-        static const int pw_check = [] {
-          const char* e = std::getenv("SPIN_PREWARM_CHECK");  // debugging: 1 non-finite scan, 2 + redo and diff
-          return e ? std::atoi(e) : 0;
-        }();
-        if (pw_check == 2) {  // snapshot the rows, recompute them once the round is over, diff
-          check_cuda(cudaStreamSynchronize(ps), "prewarm check");
-          ModelDev& md = ssm_[j];
-          auto snap = [&](std::vector<uint16_t>& out) {
-            out.clear();
-            std::vector<uint16_t> row(md.hd);
-            for (const auto& [slot, from, to] : jobs[j])
-              for (int l = 0; l < md.L; ++l)
-                for (int kv = 0; kv < 2; ++kv)
-                  for (int h = 0; h < md.H; ++h)
-                    for (int p = from; p < to; ++p) {
-                      const size_t off = ((((static_cast<size_t>(l) * opts_.max_requests + slot) * md.H + h) *
-                                           opts_.max_ctx) + p) * md.hd;
-                      cudaMemcpy(row.data(), (kv ? md.vc : md.kc) + off, md.hd * 2, cudaMemcpyDeviceToHost);
-                      out.insert(out.end(), row.begin(), row.end());
-                    }
-          };
-          std::vector<uint16_t> a, b;
-          auto tok_hash = [&]() {
-            uint64_t hsh = 1469598103934665603ull;
-            for (const auto& [slot, from, to] : jobs[j])
-              for (int p = from; p < to; ++p)
-                hsh = (hsh ^ static_cast<uint32_t>(h_tokens_[static_cast<size_t>(slot) * opts_.max_ctx + p])) *
-                      1099511628211ull;
-            return hsh;
-          };
-          const uint64_t th0 = tok_hash();
-          {
-            std::string js;
-            for (const auto& [slot, from, to] : jobs[j])
-              js += " " + std::to_string(slot) + ":[" + std::to_string(from) + "," + std::to_string(to) + ")";
-            std::fprintf(stderr, "prewarm job ssm %zu:%s\n", j, js.c_str());
-          }
-          snap(a);
-          check_cuda(cudaEventSynchronize(ev_end_), "prewarm check: round end");
-          const uint64_t th1 = tok_hash();
-          if (th0 != th1) std::fprintf(stderr, "prewarm check: host tokens of ssm %zu's job changed during the round\n", j);
-          extend(static_cast<int>(j), jobs[j], ps, &pwlane_[j], pw_pin_[j], pw_pin_cap_);
-          check_cuda(cudaStreamSynchronize(ps), "prewarm check redo");
-          snap(b);
-          size_t idx = 0;
-          for (const auto& [slot, from, to] : jobs[j])
-            for (int l = 0; l < md.L; ++l)
-              for (int kv = 0; kv < 2; ++kv) {
-                int diff_rows = 0, first_h = -1, first_p = -1;
-                for (int h = 0; h < md.H; ++h)
-                  for (int p = from; p < to; ++p, idx += md.hd)
-                    if (std::memcmp(a.data() + idx, b.data() + idx, md.hd * 2) != 0) {
-                      if (diff_rows++ == 0) first_h = h, first_p = p;
-                    }
-                if (diff_rows)
-                  std::fprintf(stderr, "prewarm diff: ssm %zu slot %d [%d,%d) layer %d %s rows %d of %d, first head %d pos %d\n",
-                               j, slot, from, to, l, kv ? "V" : "K", diff_rows, md.H * (to - from), first_h, first_p);
-              }
-        }
-        if (pw_check == 1) {  // the recomputed rows, right after the catch-up completes
-          check_cuda(cudaStreamSynchronize(ps), "prewarm check");
-          ModelDev& md = ssm_[j];
-          std::vector<uint16_t> row(md.hd);
-          for (const auto& [slot, from, to] : jobs[j])
-            for (int l = 0; l < md.L; ++l)
-              for (int kv = 0; kv < 2; ++kv) {
-                int bad = 0, first = -1;
-                for (int h = 0; h < md.H; ++h)
-                  for (int p = from; p < to; ++p) {
-                    const size_t off = ((((static_cast<size_t>(l) * opts_.max_requests + slot) * md.H + h) *
-                                         opts_.max_ctx) + p) * md.hd;
-                    cudaMemcpy(row.data(), (kv ? md.vc : md.kc) + off, md.hd * 2, cudaMemcpyDeviceToHost);
-                    for (int i = 0; i < md.hd; ++i)
-                      if ((row[i] & 0x7f80) == 0x7f80) {
-                        if (bad == 0) {
-                          std::fprintf(stderr, "prewarm check: first bad row ssm %zu slot %d layer %d %s head %d pos %d:",
-                                       j, slot, l, kv ? "V" : "K", h, p);
-                          for (int q = 0; q < md.hd; ++q) std::fprintf(stderr, " %04x", row[q]);
-                          std::fprintf(stderr, "\n");
-                        }
-                        ++bad;
-                        if (first < 0 || p < first) first = p;
-                      }
-                  }
-                if (bad)
-                  std::fprintf(stderr, "prewarm check: ssm %zu slot %d [%d,%d) layer %d %s non-finite %d first %d\n", j,
-                               slot, from, to, l, kv ? "V" : "K", bad, first);
-              }
-        }
         for (const auto& r : jobs[j]) {
           const size_t idx = j * opts_.max_requests + std::get<0>(r);
           pw_len_pin_[j][std::get<0>(r)] = std::get<2>(r);
@@ -959,7 +822,6 @@ void Engine::init_prewarm() {
   pw_len_pin_.assign(M, nullptr);
   for (int j = 0; j < M; ++j) {
     init_lane(pwlane_[j], ssm_[j], kExtendRows, kExtendRows, false);
-    pwlane_[j].serial = std::getenv("SPIN_PREWARM_SERIAL") != nullptr;  // debugging
     check_cuda(cudaMallocHost(&pw_pin_[j], pw_pin_cap_ * 4), "prewarm staging");
     check_cuda(cudaMallocHost(&pw_len_pin_[j], static_cast<size_t>(R) * 4), "prewarm staging");
   }
@@ -1431,23 +1293,6 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, const int
     last_verify_rows_ = 0;  // the in-situ kernel replays expect a serial round's layout
   } else {
     RoundPlan& p = plan_round(n, slots, ssm_of);
-    static const bool whole_check = [] {
-      const char* e = std::getenv("SPIN_PREWARM_CHECK");
-      return e && std::atoi(e) == 3;
-    }();
-    if (whole_check && prewarm) {  // debugging: every SSM cache before the round (see enqueue_prewarm)
-      check_cuda(cudaDeviceSynchronize(), "whole check");
-      dbg_kv_before_.resize(ssm_.size());
-      for (size_t jj = 0; jj < ssm_.size(); ++jj) {
-        ModelDev& md = ssm_[jj];
-        const size_t e = static_cast<size_t>(md.L) * opts_.max_requests * md.H * opts_.max_ctx * md.hd;
-        dbg_kv_before_[jj].resize(2 * e);
-        check_cuda(cudaMemcpy(dbg_kv_before_[jj].data(), md.kc, e * 2, cudaMemcpyDeviceToHost), "snap k");
-        check_cuda(cudaMemcpy(dbg_kv_before_[jj].data() + e, md.vc, e * 2, cudaMemcpyDeviceToHost), "snap v");
-      }
-    }
-    static const bool pw_first = std::getenv("SPIN_PREWARM_FIRST") != nullptr;  // debugging
-    if (prewarm && pw_first) enqueue_prewarm(n, slots, prewarm, ssm_of);
     // stage the lists
     std::vector<int> act;
     for (int i = 0; i < n; ++i)
@@ -1472,13 +1317,7 @@ void Engine::round(int n, const int32_t* slots, const int32_t* ssm_of, const int
       capture_round(p);
     }
     // destinations of future switches recomputed on idle streams while this round runs
-    if (prewarm && !pw_first) enqueue_prewarm(n, slots, prewarm, ssm_of);
-    static const bool pw_sync = std::getenv("SPIN_PREWARM_SYNC") != nullptr;  // debugging: no overlap
-    if (prewarm && pw_sync) {
-      sync_sv("round (before prewarm)");
-      if (pw_thread_.joinable()) pw_thread_.join();
-      check_cuda(cudaDeviceSynchronize(), "prewarm (synchronous)");
-    }
+    if (prewarm) enqueue_prewarm(n, slots, prewarm, ssm_of);
     sync_sv("round");
     dump_stamps();
     check_cuda(cudaEventElapsedTime(&draft_ms, ev_start_, ev_draft_), "event timing");
@@ -1738,13 +1577,13 @@ void Engine::verify_bench(int n, const int32_t* slots, const int32_t* draft_lens
   const int T = static_cast<int>(rt.size());
   Lane& ln = tlane_;
   if (T > ln.T_cap) fail(SPIN_CAPACITY_ERROR, "verify_bench: too many query rows for this engine (raise window)");
-  check_cuda(cudaMemcpy(ln.meta.row_tok, rt.data(), T * 4, cudaMemcpyHostToDevice), "h2d");
-  check_cuda(cudaMemcpy(ln.meta.row_slot, rs.data(), T * 4, cudaMemcpyHostToDevice), "h2d");
-  check_cuda(cudaMemcpy(ln.meta.row_pos, rp.data(), T * 4, cudaMemcpyHostToDevice), "h2d");
-  check_cuda(cudaMemcpy(ln.meta.req_slot, sl.data(), n * 4, cudaMemcpyHostToDevice), "h2d");
-  check_cuda(cudaMemcpy(ln.meta.req_qstart, qs.data(), n * 4, cudaMemcpyHostToDevice), "h2d");
-  check_cuda(cudaMemcpy(ln.meta.req_qlen, ql.data(), n * 4, cudaMemcpyHostToDevice), "h2d");
-  check_cuda(cudaMemcpy(ln.meta.req_kvlen, kv.data(), n * 4, cudaMemcpyHostToDevice), "h2d");
+  check_cuda(upload_sync(ln.meta.row_tok, rt.data(), T * 4), "h2d");
+  check_cuda(upload_sync(ln.meta.row_slot, rs.data(), T * 4), "h2d");
+  check_cuda(upload_sync(ln.meta.row_pos, rp.data(), T * 4), "h2d");
+  check_cuda(upload_sync(ln.meta.req_slot, sl.data(), n * 4), "h2d");
+  check_cuda(upload_sync(ln.meta.req_qstart, qs.data(), n * 4), "h2d");
+  check_cuda(upload_sync(ln.meta.req_qlen, ql.data(), n * 4), "h2d");
+  check_cuda(upload_sync(ln.meta.req_kvlen, kv.data(), n * 4), "h2d");
   const int width = opts_.pack_width > 0 ? std::min(opts_.pack_width, n) : n;
   MetaArgs a{};
   a.mode = kMetaExtend;

@@ -51,7 +51,6 @@ struct Lane {
   int32_t* amax_idx = nullptr;
   float* logits = nullptr;
   int head_sms = 0;  // SMs the lm_head GEMM may use (0 = all): off the critical chain, fewer
-  bool serial = false;  // debugging: synchronise the stream after every launch of this lane
   std::vector<void*> allocs;
 };
 
@@ -185,7 +184,6 @@ class Engine {
   bool prof_ = false;
   std::atomic<int64_t> launches_{0};
   std::mutex plan_mu_;  // plans_ is shared with the prewarm thread
-  std::vector<std::vector<uint16_t>> dbg_kv_before_;  // SPIN_PREWARM_CHECK=3 snapshots
   struct ProfRec {
     int cat;
     cudaEvent_t a, b;

@@ -112,5 +112,7 @@ cudaError_t ensure_smem_optin(const void* kernel, size_t bytes);
 // Programmatic dependent launch on every kernel launch (1), or off everywhere (SPIN_NO_PDL=1,
 // debugging: every kernel then waits for its predecessor's completion before it starts).
 int pdl_allowed();
+cudaError_t upload_sync(void* dst, const void* src, size_t bytes);  // devattr.cpp
+cudaError_t zero_sync(void* dst, size_t bytes);
 
 }  // namespace spin
