@@ -1157,7 +1157,7 @@ void Engine::launch_pipe_slot(PipePlan& pp, bool first, bool host_round) {
     check_cuda(cudaEventRecord(u.t_d, sj), "event");
     check_cuda(cudaEventRecord(u.ev_d, sj), "event");
   }
-  // the slot's draft phase on every SSM stream (a prewarm catch-up waits for it, enqueue_prewarm)
+  // the slot's draft phase on every SSM stream (SPIN_PREWARM_AFTER_DRAFTS: a catch-up waits for it)
   for (size_t j = 0; j < ssm_.size(); ++j) check_cuda(cudaEventRecord(ev_join_[j], ss_[j]), "drafts done");
   for (int k : pp.vorder) {
     PipeUnit& u = pp.units[k];

@@ -1,9 +1,10 @@
 """Prewarm must not change outcomes (bandit.cpp:122-139 prewarm_destination only moves the
 switch cost): a fixed pseudo-random assignment per round over three domain SSMs of a
 7B-shaped target, prewarm = the next round's SSM, run with and without prewarm -- committed
-histories identical token for token. This configuration exposed catch-ups corrupted while
-running beside the same SSM's draft kernels; the catch-up now overlaps
-the verify phase only."""
+histories identical token for token. This configuration exposed catch-ups that reduced their
+split-K pieces with a GEMM piece table still in flight on the legacy stream while the drafts
+ran beside them (fixed by devattr.cpp upload_sync); it fails at round 10
+without that fix."""
 from dataclasses import replace
 
 import numpy as np
