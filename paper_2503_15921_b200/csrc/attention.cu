@@ -785,6 +785,237 @@ __global__ void __launch_bounds__(64) attn_ws_kernel(FwdMeta m, AttnGeom g, cons
   ptx::grid_dep_launch();
 }
 
+// Multi-query verify attention (9..8*NQW queries per request: ragged / long windows): one CTA
+// per (pack row, chunk, head) item, NQW consumer warps + one producer warp sharing ONE K/V
+// ring. Consumer warp w owns queries 8w..8w+7 of every piece (attn_kernel<HD, 1>'s per-warp
+// arithmetic: hi / lo Q and P planes, separate lo accumulator chain, scores of tile t + 1
+// issued before tile t's softmax), so every 16-key tile is read from DRAM once for all of a
+// request's queries, a warp whose query tile is empty for the piece (qlen <= 8w) only passes
+// the tile on, and each warp's register budget is the one-tile kernel's (attn_kernel<128, 3>
+// carried 3 tiles per warp and spilled). The producer's lane 0 streams the item's tiles
+// (1-D bulk copies of the pre-swizzled cache rows) and recycles a slot once every consumer
+// warp released it (empty barrier, NQW arrivals). Split-KV pieces: the consumer warps meet at
+// a named barrier, warp 0 takes the arrival ticket and, last, merges (merge_pieces).
+template <int HD, int NQW, int ST>
+struct MqCfg {
+  static constexpr int kStages = ST;
+  static constexpr uint32_t kHalf = 16 * HD * 2;
+  static constexpr uint32_t kStage = 2 * kHalf;
+  static constexpr int kDT = HD / 16;
+  static constexpr int kNR = kDT * 4;
+  static constexpr int kQP = 8 * NQW;
+  static constexpr size_t kTotal = 1024 + kStages * kStage + 2 * kStages * 8;
+};
+
+template <int HD, int NQW, int ST>
+__global__ void __launch_bounds__(32 * (NQW + 1)) attn_mq_kernel(FwdMeta m, AttnGeom g, const float* __restrict__ q,
+                                                                 AttnWork w, bf16* __restrict__ out) {
+  using C = MqCfg<HD, NQW, ST>;
+  constexpr int S = C::kStages, DT = C::kDT, NR = C::kNR, QP = C::kQP;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::kStage);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int gq = lane >> 2, cq = lane & 3;
+  const int H = g.n_heads, D = H * HD;
+  const float sl2 = g.scale * kLog2e;
+  const int head = blockIdx.x % H, rc = blockIdx.x / H;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) ptx::mbar_init(&full[s], 1), ptx::mbar_init(&empty[s], NQW);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  const bool stamp = w.st != nullptr && threadIdx.x == 0;
+  if (stamp) w.st[8 * blockIdx.x] = ptx::globaltimer();
+  // w.early: the work list and the KV rows older than the queries are complete before this
+  // grid starts (attn_kernel), so the producer issues those tiles before the dependency wait
+  const int p_lo = m.item_ptr[rc], p_hi = m.item_ptr[rc + 1];
+  const Piece* pieces = reinterpret_cast<const Piece*>(m.pieces);
+  if (warp == NQW) {  // ---- producer
+    if (lane == 0) {
+      bool dep = !w.early;
+      if (dep) ptx::grid_dep_wait();
+      const uint64_t pol = ptx::policy_evict_first();
+      const size_t kv_base = static_cast<size_t>(g.layer * g.slots) * H;
+      int issued = 0;
+      for (int p = p_lo; p < p_hi; ++p) {
+        const int slot = pieces[p].slot, tok0 = pieces[p].tok0, len = pieces[p].len;
+        const int fresh = pieces[p].kvlen - pieces[p].qlen;  // first key written by this forward
+        const size_t row0 = ((kv_base + static_cast<size_t>(slot) * H + head) * g.ctx) + tok0;
+        for (int t = 0; t * 16 < len; ++t, ++issued) {
+          if (!dep && tok0 + t * 16 + 16 > fresh) ptx::grid_dep_wait(), dep = true;
+          const int st = issued % S;
+          if (issued >= S) ptx::mbar_wait(&empty[st], static_cast<uint32_t>(((issued / S) - 1) & 1));
+          uint8_t* dst = ring + st * C::kStage;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          ptx::mbar_arrive_expect_tx(&full[st], C::kStage);
+          ptx::bulk_load(dst, g.k_cache + (row0 + t * 16) * HD, C::kHalf, &full[st], pol);
+          ptx::bulk_load(dst + C::kHalf, g.v_cache + (row0 + t * 16) * HD, C::kHalf, &full[st], pol);
+        }
+      }
+    }
+    ptx::grid_dep_launch();
+    return;
+  }
+  // ---- consumers: queries 8 * warp .. 8 * warp + 7 of every piece
+  ptx::grid_dep_wait();  // q (and this forward's new keys) come from the QKV epilogue
+  ptx::grid_dep_launch();
+  int consumed = 0;
+  for (int p = p_lo; p < p_hi; ++p) {
+    const Piece ph = pieces[p];
+    const int ntile = (ph.len + 15) / 16;
+    if (8 * warp >= ph.qlen) {  // no query of this warp in the piece: pass its tiles on
+      for (int t = 0; t < ntile; ++t, ++consumed) {
+        ptx::mbar_wait(&full[consumed % S], static_cast<uint32_t>((consumed / S) & 1));
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[consumed % S]);
+      }
+    } else {
+      uint32_t qh[DT][2], ql[DT][2];
+      {
+        const int qi = 8 * warp + gq;
+        const bool ok = qi < ph.qlen;
+        const float* qr = q + static_cast<size_t>(ph.qs + (ok ? qi : 0)) * D + head * HD + 2 * cq;
+#pragma unroll
+        for (int kt = 0; kt < DT; ++kt)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const float2 v = ok ? __ldg(reinterpret_cast<const float2*>(qr + 16 * kt + 8 * hh)) : make_float2(0.f, 0.f);
+            const float x = v.x * sl2, y = v.y * sl2;
+            const float hx = bf_round(x), hy = bf_round(y);
+            qh[kt][hh] = pack_bf2(hx, hy);
+            ql[kt][hh] = pack_bf2(x - hx, y - hy);
+          }
+      }
+      float o[NR], olo[NR];
+#pragma unroll
+      for (int i = 0; i < NR; ++i) o[i] = 0.f, olo[i] = 0.f;
+      float mrun[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f};
+      const int qbase = ph.kvlen - ph.qlen;
+      auto scores = [&](int stg, float (&sv)[4]) {
+        const uint32_t kb = ptx::smem_u32(ring + stg * C::kStage);
+        float sc[4][4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sc[c][0] = sc[c][1] = sc[c][2] = sc[c][3] = 0.f;
+#pragma unroll
+        for (int kt = 0; kt < DT; ++kt) {
+          uint32_t a[4];
+          ldsm_x4(kb + kvoff<HD>((lane & 7) + ((lane >> 3) & 1) * 8, 2 * kt + (lane >> 4), ph.tok0), a);
+          mma16816(sc[kt & 1], a, qh[kt][0], qh[kt][1]);
+          mma16816(sc[2 + (kt & 1)], a, ql[kt][0], ql[kt][1]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sv[e] = (sc[0][e] + sc[1][e]) + (sc[2][e] + sc[3][e]);
+      };
+      float s[4];
+      ptx::mbar_wait(&full[consumed % S], static_cast<uint32_t>((consumed / S) & 1));
+      scores(consumed % S, s);
+      for (int t = 0; t < ntile; ++t, ++consumed) {
+        const int st = consumed % S;
+        const bool more = t + 1 < ntile;
+        float s_next[4];
+        if (more) {
+          const int st1 = (consumed + 1) % S;
+          ptx::mbar_wait(&full[st1], static_cast<uint32_t>(((consumed + 1) / S) & 1));
+          scores(st1, s_next);
+        }
+        const uint32_t vb = ptx::smem_u32(ring + st * C::kStage) + C::kHalf;
+        const int key0 = ph.tok0 + t * 16 + gq;
+        const int kend = ph.tok0 + ph.len;
+        float corr[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int qpos = qbase + 8 * warp + 2 * cq + e;
+          const bool v0 = key0 < kend && (key0 <= qpos || !g.causal);
+          const bool v1 = key0 + 8 < kend && (key0 + 8 <= qpos || !g.causal);
+          s[e] = v0 ? s[e] : -INFINITY;
+          s[2 + e] = v1 ? s[2 + e] : -INFINITY;
+          float mx = fmaxf(s[e], s[2 + e]);
+          mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 4));
+          mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 8));
+          mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 16));
+          const float mnew = fmaxf(mrun[e], mx);
+          corr[e] = mnew == -INFINITY ? 1.f : exp2f(mrun[e] - mnew);
+          const float p0 = mnew == -INFINITY ? 0.f : exp2f(s[e] - mnew);
+          const float p1 = mnew == -INFINITY ? 0.f : exp2f(s[2 + e] - mnew);
+          s[e] = p0;
+          s[2 + e] = p1;
+          lsum[e] = lsum[e] * corr[e] + (p0 + p1);
+          mrun[e] = mnew;
+        }
+#pragma unroll
+        for (int dt = 0; dt < DT; ++dt) {
+          float* oo = o + dt * 4;
+          float* ol = olo + dt * 4;
+          oo[0] *= corr[0], oo[1] *= corr[1], oo[2] *= corr[0], oo[3] *= corr[1];
+          ol[0] *= corr[0], ol[1] *= corr[1], ol[2] *= corr[0], ol[3] *= corr[1];
+        }
+        const float h0 = bf_round(s[0]), h1 = bf_round(s[1]), h2 = bf_round(s[2]), h3 = bf_round(s[3]);
+        const uint32_t ph0 = movm_t(pack_bf2(h0, h1)), ph1 = movm_t(pack_bf2(h2, h3));
+        const uint32_t pl0 = movm_t(pack_bf2(s[0] - h0, s[1] - h1)), pl1 = movm_t(pack_bf2(s[2] - h2, s[3] - h3));
+#pragma unroll
+        for (int dt = 0; dt < DT; ++dt) {
+          uint32_t a[4];
+          ldsm_x4_t(vb + kvoff<HD>((lane & 7) + ((lane >> 4) & 1) * 8, 2 * dt + ((lane >> 3) & 1), ph.tok0), a);
+          mma16816(o + dt * 4, a, ph0, ph1);
+          mma16816(olo + dt * 4, a, pl0, pl1);
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[st]);
+        if (more) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) s[e] = s_next[e];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NR; ++i) o[i] += olo[i];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        float l = lsum[e];
+        l += __shfl_xor_sync(kFull, l, 4);
+        l += __shfl_xor_sync(kFull, l, 8);
+        l += __shfl_xor_sync(kFull, l, 16);
+        lsum[e] = l;
+      }
+      const bool single = ph.npieces == 1;
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int e = i & 3, dt = i >> 2;
+        const int qi = 8 * warp + 2 * cq + (e & 1);
+        const int dim = 16 * dt + gq + (e >> 1) * 8;
+        if (qi >= ph.qlen) continue;
+        if (single) {
+          out[static_cast<size_t>(ph.qs + qi) * D + head * HD + dim] = __float2bfloat16_rn(o[i] / lsum[e & 1]);
+        } else {
+          const size_t pi = (static_cast<size_t>(p) * H + head) * QP + qi;
+          w.part_o[pi * HD + dim] = o[i];
+          if (dt == 0 && gq == 0 && e < 2) w.part_m[pi] = mrun[e], w.part_l[pi] = lsum[e];
+        }
+      }
+    }
+    if (ph.npieces == 1) continue;
+    // ---- every consumer warp's partial of this piece is written: arrival, last merges
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * NQW) : "memory");
+    if (warp != 0) continue;
+    int last = 0;
+    if (lane == 0) {
+      int* cnt = w.counter + static_cast<size_t>(ph.req) * H + head;
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      last = atomicAdd(cnt, 1) == ph.npieces - 1;
+      if (last) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        *cnt = 0;
+      }
+    }
+    last = __shfl_sync(kFull, last, 0);
+    if (last) merge_pieces<HD, QP, false>(m, w, ph, head, H, D, out, lane);
+  }
+  if (stamp) w.st[8 * blockIdx.x + 7] = ptx::globaltimer();
+}
+
 // Few-query (draft step) variant: one CTA per (pack row, chunk, head) item whose four
 // warps take the item's 16-key tiles round robin, so the longest chain is a quarter of
 // a chunk (one ring's worth: a single DRAM round trip) instead of a whole chunk; the
@@ -1168,6 +1399,52 @@ void launch_ws(const FwdMeta& m, int n_rows, const AttnGeom& g, const float* q, 
   cudaLaunchKernelEx(&cfg, attn_ws_kernel<HD>, m, g, q, wk, out, n_items);
 }
 
+template <int HD, int NQW, int ST>
+void launch_mq_st(const FwdMeta& m, int n_rows, const AttnGeom& g, const float* q, const AttnWork& w, bf16* out,
+                  cudaStream_t s) {
+  using MC = MqCfg<HD, NQW, ST>;
+  ensure_smem_optin(reinterpret_cast<const void*>(attn_mq_kernel<HD, NQW, ST>), MC::kTotal);
+  static const int early = [] {
+    const char* e = std::getenv("SPIN_ATTN_EARLY");  // experiments only: 0 disables
+    return e ? std::atoi(e) : 1;
+  }();
+  AttnWork wk = w;
+  wk.early = w.early && early;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_allowed();
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.stream = s;
+  cfg.gridDim = dim3(n_rows * std::max(1, w.chunks) * g.n_heads);  // one CTA per (row, chunk, head)
+  cfg.blockDim = dim3(32 * (NQW + 1));
+  cfg.dynamicSmemBytes = MC::kTotal;
+  cudaLaunchKernelEx(&cfg, attn_mq_kernel<HD, NQW, ST>, m, g, q, wk, out);
+}
+
+template <int HD, int NQW>
+void launch_mq(const FwdMeta& m, int n_rows, const AttnGeom& g, const float* q, const AttnWork& w, bf16* out,
+               cudaStream_t s) {
+  static const int st = [] {
+    const char* e = std::getenv("SPIN_ATTN_MQ_STAGES");  // tuning
+    return e ? std::atoi(e) : 4;
+  }();
+  if (st <= 4) return launch_mq_st<HD, NQW, 4>(m, n_rows, g, q, w, out, s);
+  if (st <= 8) return launch_mq_st<HD, NQW, 8>(m, n_rows, g, q, w, out, s);
+  return launch_mq_st<HD, NQW, 12>(m, n_rows, g, q, w, out, s);
+}
+
+// attn_mq_kernel serves windows of 9..24 queries; SPIN_ATTN_MQ=0 sends them to
+// attn_kernel<HD, 2 / 3> (one warp carrying every query tile; A/B)
+bool mq_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("SPIN_ATTN_MQ");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 template <int HD>
 void launch_hd(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& m, int n_rows, const AttnGeom& g,
                const float* q, const AttnWork& w, bf16* out, cudaStream_t s) {
@@ -1179,6 +1456,10 @@ void launch_hd(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& 
   }();
   if (w.qmax <= 8 && ws && w.st == nullptr) return launch_ws<HD>(m, n_rows, g, q, w, out, s);
   if (w.qmax <= 8) return launch_t<HD, 1>(tm_k, tm_v, m, n_rows, g, q, w, out, s);
+  if (mq_enabled()) {
+    if (w.qmax <= 16) return launch_mq<HD, 2>(m, n_rows, g, q, w, out, s);
+    return launch_mq<HD, 3>(m, n_rows, g, q, w, out, s);
+  }
   if (w.qmax <= 16) return launch_t<HD, 2>(tm_k, tm_v, m, n_rows, g, q, w, out, s);
   return launch_t<HD, 3>(tm_k, tm_v, m, n_rows, g, q, w, out, s);
 }
@@ -1187,6 +1468,7 @@ void launch_hd(const CUtensorMap& tm_k, const CUtensorMap& tm_v, const FwdMeta& 
 
 int attn_ctas(int n_rows, int chunks, int heads, int qmax) {
   if (qmax <= kDecodeQ) return n_rows * std::max(1, chunks) * heads * 2;  // DecCfg::kCluster
+  if (qmax > 8 && mq_enabled()) return n_rows * std::max(1, chunks) * heads;
   return (n_rows * std::max(1, chunks) * heads + kVW - 1) / kVW;
 }
 

@@ -244,7 +244,7 @@ void Engine::init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool l
   ln.part = dalloc<float>(A, part);
   // attention work list + split-KV partials: pieces <= segments + rows x (chunks - 1), and
   // rows x chunks x heads ~ 8 x SMs bounds the chunk splits (attn_chunks); partial slots
-  // are 8 queries wide (extends) or up to 24 (verify with a window up to 16, few pieces)
+  // are 8 queries wide (extends) or 8 * ceil((window + 1) / 8) (verify)
   ln.piece_cap = ln.seg_cap + 8 * num_sms_ / m.H + 64;
   ln.meta.piece_cap = ln.piece_cap;
   ln.meta.item_ptr = dalloc<int32_t>(A, static_cast<size_t>(ln.rows_cap) * 16 + 1);
@@ -253,7 +253,7 @@ void Engine::init_lane(Lane& ln, const ModelDev& m, int T_cap, int R_cap, bool l
   ln.meta.req_plist = dalloc<int32_t>(A, ln.piece_cap);
   ln.meta.n_pieces = dalloc<int32_t>(A, 1);
   ln.meta.row_len = dalloc<int32_t>(A, ln.rows_cap);
-  const size_t np = static_cast<size_t>(ln.piece_cap) * m.H * 8;
+  const size_t np = static_cast<size_t>(ln.piece_cap) * m.H * (8 * ((opts_.window + 8) / 8));
   ln.aw.part_m = dalloc<float>(A, np);
   ln.aw.part_l = dalloc<float>(A, np);
   ln.aw.part_o = dalloc<float>(A, np * m.hd);
