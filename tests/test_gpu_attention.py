@@ -72,3 +72,20 @@ def test_attention_many_segments_per_row(hd, qlen, width):
     qls = np.full(S, qlen, np.int32)
     out, ref = run(hd, H, L, S, ctx, 0, slots, qls, kvl, width, 7 * hd + qlen)
     assert float(np.abs(out - ref).max()) <= 1e-2
+
+
+@pytest.mark.parametrize("hd,width,qmax", [(128, 3, 17), (64, 2, 17), (128, 0, 17), (128, 4, 16), (64, 0, 12)])
+def test_attention_ragged_windows(hd, width, qmax):
+    """Mixed query counts in one launch (ragged drafts, config 3: attn_mq_kernel): warps whose
+    8-query tile is empty for a piece pass its tiles on, split-KV pieces of 9..24-query requests
+    meet at the named barrier and are merged by the last warp."""
+    H, L, S, ctx = 3, 1, 10, 900
+    rng = np.random.default_rng(hd + width + qmax)
+    slots = rng.permutation(S).astype(np.int32)
+    qls = np.minimum(np.array([1, 17, 9, 3, 16, 8, 12, 2, 17, 5], np.int32), qmax).astype(np.int32)
+    kvl = np.maximum(rng.integers(20, 880, S), qls).astype(np.int32)
+    kvl[3] = qls[3]  # a request that sees only its own queries
+    out, ref = run(hd, H, L, S, ctx, 0, slots, qls, kvl, width, 11 * hd + width + qmax)
+    assert float(np.abs(out - ref).max()) <= 1e-2
+    mism = float((out != bf16_bits_to_f32(f32_to_bf16_bits(ref))).mean())
+    assert mism < 0.02, mism
