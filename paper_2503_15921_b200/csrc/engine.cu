@@ -608,6 +608,7 @@ Engine::~Engine() {
   cudaEventDestroy(ev_fork_), cudaEventDestroy(ev_start_), cudaEventDestroy(ev_draft_), cudaEventDestroy(ev_end_);
   cudaEventDestroy(ev_r0_), cudaEventDestroy(ev_r1_);
   for (auto& e : ev_pw_) cudaEventDestroy(e);
+  for (auto& e : ev_pw_stage_) cudaEventDestroy(e);
   for (auto& st : ps_) cudaStreamDestroy(st);
   for (auto& l : pwlane_)
     for (void* p : l.allocs) cudaFree(p);
@@ -788,7 +789,9 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
       for (size_t j = 0; j < jobs.size(); ++j) {
         if (jobs[j].empty()) continue;
         cudaStream_t ps = ps_[j];
-        check_cuda(cudaEventSynchronize(ev_pw_[j]), "prewarm staging");  // staging reuse
+        const size_t hb = 2 * j + static_cast<size_t>(pw_half_[j]);  // this job's staging half
+        pw_half_[j] ^= 1;
+        check_cuda(cudaEventSynchronize(ev_pw_stage_[hb]), "prewarm staging");  // the job before last
         static const bool after_drafts = std::getenv("SPIN_PREWARM_AFTER_DRAFTS") != nullptr;
         if (after_drafts) {  // overlap the verification only (timing experiments)
           if (pipe_drafts)  // micro-batched slot: every SSM stream's last unit draft (launch_pipe_slot)
@@ -797,15 +800,16 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
           else
             check_cuda(cudaStreamWaitEvent(ps, ev_draft_, 0), "prewarm after drafts");
         }
-        extend(static_cast<int>(j), jobs[j], ps, &pwlane_[j], pw_pin_[j], pw_pin_cap_);
+        extend(static_cast<int>(j), jobs[j], ps, &pwlane_[j], pw_pin_[hb], pw_pin_cap_);
         for (const auto& r : jobs[j]) {
           const size_t idx = j * opts_.max_requests + std::get<0>(r);
-          pw_len_pin_[j][std::get<0>(r)] = std::get<2>(r);
-          check_cuda(cudaMemcpyAsync(st_.ssm_len + idx, pw_len_pin_[j] + std::get<0>(r), 4, cudaMemcpyHostToDevice,
+          pw_len_pin_[hb][std::get<0>(r)] = std::get<2>(r);
+          check_cuda(cudaMemcpyAsync(st_.ssm_len + idx, pw_len_pin_[hb] + std::get<0>(r), 4, cudaMemcpyHostToDevice,
                                      ps),
                      "h2d");
         }
         check_cuda(cudaEventRecord(ev_pw_[j], ps), "prewarm event");
+        check_cuda(cudaEventRecord(ev_pw_stage_[hb], ps), "prewarm event");
       }
     } catch (const std::exception& e) {
       pw_error_msg_ = e.what();
@@ -817,13 +821,16 @@ void Engine::enqueue_prewarm(int n, const int32_t* slots, const int32_t* prewarm
 void Engine::init_prewarm() {
   const int M = static_cast<int>(ssm_.size()), R = opts_.max_requests;
   pwlane_.resize(M);
-  pw_pin_.assign(M, nullptr);
+  pw_pin_.assign(2 * M, nullptr);
   pw_pin_cap_ = static_cast<size_t>(8) * (static_cast<size_t>(R) * opts_.max_ctx + kExtendRows);
-  pw_len_pin_.assign(M, nullptr);
-  for (int j = 0; j < M; ++j) {
-    init_lane(pwlane_[j], ssm_[j], kExtendRows, kExtendRows, false);
-    check_cuda(cudaMallocHost(&pw_pin_[j], pw_pin_cap_ * 4), "prewarm staging");
-    check_cuda(cudaMallocHost(&pw_len_pin_[j], static_cast<size_t>(R) * 4), "prewarm staging");
+  pw_len_pin_.assign(2 * M, nullptr);
+  ev_pw_stage_.assign(2 * M, nullptr);
+  pw_half_.assign(M, 0);
+  for (int j = 0; j < M; ++j) init_lane(pwlane_[j], ssm_[j], kExtendRows, kExtendRows, false);
+  for (int h = 0; h < 2 * M; ++h) {
+    check_cuda(cudaMallocHost(&pw_pin_[h], pw_pin_cap_ * 4), "prewarm staging");
+    check_cuda(cudaMallocHost(&pw_len_pin_[h], static_cast<size_t>(R) * 4), "prewarm staging");
+    check_cuda(cudaEventCreateWithFlags(&ev_pw_stage_[h], cudaEventDisableTiming), "event");
   }
 }
 

@@ -163,11 +163,15 @@ class Engine {
   std::vector<Lane> pwlane_;
   std::vector<cudaStream_t> ps_;
   std::vector<cudaEvent_t> ev_pw_;
-  std::vector<int32_t*> pw_pin_;
+  // staging (row metadata, ssm_len values) in two halves per SSM, alternating per job, so a
+  // job never waits for the previous one's catch-up to finish before it can stage
+  std::vector<int32_t*> pw_pin_;  // [2 * M]
+  std::vector<cudaEvent_t> ev_pw_stage_;  // [2 * M]: the job that staged in half b is done
+  std::vector<int> pw_half_;
   size_t pw_pin_cap_ = 0;
   std::vector<char> pw_pending_;
   std::thread pw_thread_;  // enqueues the prewarm extends while the round runs
-  std::vector<int32_t*> pw_len_pin_;  // pinned ssm_len values the prewarm stream uploads
+  std::vector<int32_t*> pw_len_pin_;  // [2 * M] pinned ssm_len values the prewarm stream uploads
   bool pw_error_ = false;
   std::string pw_error_msg_;
   int64_t pw_tokens_ = 0;
