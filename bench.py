@@ -477,10 +477,11 @@ def run_c5(args, ranks):
                                            max_micro_batches=args.max_micro_batches, probe_rounds=3)
     sel = Lbss(N, [N] * len(ssms), alpha=8, beta=2, seed=SEED)
     # warm-up slots (graph capture per assignment shape), then the timed slots
-    serve(eng, sel, N, len(ssms), slots, args.warmup, ranks.comm)
+    pw = not args.c5_no_prewarm
+    serve(eng, sel, N, len(ssms), slots, args.warmup, ranks.comm, prewarm=pw)
     ranks.barrier()
     with ClockSampler(ranks.device) as clk:
-        rep, final = serve(eng, sel, N, len(ssms), slots, args.steps, ranks.comm)
+        rep, final = serve(eng, sel, N, len(ssms), slots, args.steps, ranks.comm, prewarm=pw)
         ranks.barrier()
     dev_ms = ranks.max(rep["device_ms"])
     wall_ms = ranks.max(rep["wall_ms"])
@@ -497,7 +498,7 @@ def run_c5(args, ranks):
                        "comm": ranks.backend, "shared_device": ranks.shared},
             "e2e": {"value": tokens / (wall_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * 3 * n_local,
                     "d2h_bytes_per_step": 4 * n_local * (3 + 2 * WINDOW + 1)},
-            "lbss": {"explore_slots": rep["explore_slots"], "epochs": rep["epochs"], "switch_ms": rep["switch_ms"],
+            "lbss": {"prewarm": pw, "explore_slots": rep["explore_slots"], "epochs": rep["epochs"], "switch_ms": rep["switch_ms"],
                      "final_plan_histogram": np.bincount(final[final >= 0], minlength=len(ssms)).tolist()},
             "pipelining": {"chosen_per_ssm": chosen.tolist(), "curve_tokens_per_s": curve, "probe_rounds": 3,
                            "candidates": "uniform b = 1 (serial) .. 4 micro-batches per SSM"},
@@ -557,6 +558,7 @@ def main():
     ap.add_argument("--max-micro-batches", type=int, default=4, help="f1 tuner candidates (1 = serial only)")
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--c4-uniform", action="store_true", help="c4 with every SSM planted on the whole vocabulary")
+    ap.add_argument("--c5-no-prewarm", action="store_true", help="c5 with synchronous switch catch-ups only")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if os.environ.get("SPIN_BENCH_SHARE_DEVICE") == "1":
