@@ -331,23 +331,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool n_ok = n < n_out;
       const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * bn);
       if (epi.mode == kGemmPartial) {
-        // 16-token chunks through the staging slots; a slot is rewritten only after the
-        // store issued kStgSlots chunks earlier has finished reading it
+        // 32-token groups (two 16-token staging slots, both TMEM loads in flight together)
+        // through two halves of the staging area; a half is rewritten only after the
+        // group stored from it two groups earlier has finished reading it
+        static_assert(kStgSlots == 4, "two groups of two 16-token slots");
         float* stg_base = reinterpret_cast<float*>(smem_red);
-        for (int c0 = 0; c0 < bn; c0 += 16, ++chunk) {
-          float* stg = stg_base + (chunk % kStgSlots) * (16 * kBlockM);
-          if (chunk >= kStgSlots) {
-            if (ew == 0 && lane == 0) ptx::bulk_wait_read<kStgSlots - 1>();
+        for (int c0 = 0; c0 < bn; c0 += 32, ++chunk) {
+          const bool two = c0 + 16 < bn;
+          float* stg = stg_base + (chunk & 1) * (32 * kBlockM);
+          if (chunk >= 2) {
+            if (ew == 0 && lane == 0) ptx::bulk_wait_read<1>();
             asm volatile("bar.sync 1, 128;" ::: "memory");
           }
-          float v[16];
-          ptx::tmem_ld16(t_addr + c0, v);
+          uint32_t r[32];
+          ptx::tmem_ld16_nowait(t_addr + c0, r);
+          if (two) ptx::tmem_ld16_nowait(t_addr + c0 + 16, r + 16);
+          ptx::tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) stg[j * kBlockM + row] = v[j];
+          for (int j = 0; j < 16; ++j) stg[j * kBlockM + row] = __uint_as_float(r[j]);
+          if (two) {
+#pragma unroll
+            for (int j = 16; j < 32; ++j) stg[j * kBlockM + row] = __uint_as_float(r[j]);
+          }
           ptx::fence_proxy_async_smem();
           asm volatile("bar.sync 1, 128;" ::: "memory");
           if (ew == 0 && lane == 0) {
             ptx::tma_store_3d(&tm_part, stg, mt * kBlockM, nt * bn + c0, p.slot);
+            if (two) ptx::tma_store_3d(&tm_part, stg + 16 * kBlockM, mt * kBlockM, nt * bn + c0 + 16, p.slot);
             ptx::bulk_commit();
           }
         }
