@@ -331,33 +331,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool n_ok = n < n_out;
       const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * bn);
       if (epi.mode == kGemmPartial) {
-        // 32-token groups (two 16-token staging slots, both TMEM loads in flight together)
-        // through two halves of the staging area; a half is rewritten only after the
-        // group stored from it two groups earlier has finished reading it
-        static_assert(kStgSlots == 4, "two groups of two 16-token slots");
-        float* stg_base = reinterpret_cast<float*>(smem_red);
+        // Each epilogue warp drains its own 32 TMEM lanes (32 output features) and stores
+        // them itself: 32-token groups (both 16-token TMEM loads in flight together) staged
+        // in the warp's two halves of its staging quarter, one TMA store per 16 tokens x 32
+        // features; a half is rewritten only after the warp's group stored from it two
+        // groups earlier has been read. No barrier across the epilogue warps.
+        static_assert(kStgSlots == 4, "two groups of two 16-token slots per warp");
+        float* stg_base = reinterpret_cast<float*>(smem_red) + ew * (kStgSlots * 16 * 32);
         for (int c0 = 0; c0 < bn; c0 += 32, ++chunk) {
           const bool two = c0 + 16 < bn;
-          float* stg = stg_base + (chunk & 1) * (32 * kBlockM);
+          float* stg = stg_base + (chunk & 1) * (2 * 16 * 32);
           if (chunk >= 2) {
-            if (ew == 0 && lane == 0) ptx::bulk_wait_read<1>();
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (lane == 0) ptx::bulk_wait_read<1>();
+            __syncwarp();
           }
           uint32_t r[32];
           ptx::tmem_ld16_nowait(t_addr + c0, r);
           if (two) ptx::tmem_ld16_nowait(t_addr + c0 + 16, r + 16);
           ptx::tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) stg[j * kBlockM + row] = __uint_as_float(r[j]);
+          for (int j = 0; j < 16; ++j) stg[j * 32 + lane] = __uint_as_float(r[j]);
           if (two) {
 #pragma unroll
-            for (int j = 16; j < 32; ++j) stg[j * kBlockM + row] = __uint_as_float(r[j]);
+            for (int j = 16; j < 32; ++j) stg[j * 32 + lane] = __uint_as_float(r[j]);
           }
           ptx::fence_proxy_async_smem();
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (ew == 0 && lane == 0) {
-            ptx::tma_store_3d(&tm_part, stg, mt * kBlockM, nt * bn + c0, p.slot);
-            if (two) ptx::tma_store_3d(&tm_part, stg + 16 * kBlockM, mt * kBlockM, nt * bn + c0 + 16, p.slot);
+          __syncwarp();
+          if (lane == 0) {
+            const int n0 = mt * kBlockM + ew * 32;
+            ptx::tma_store_3d(&tm_part, stg, n0, nt * bn + c0, p.slot);
+            if (two) ptx::tma_store_3d(&tm_part, stg + 16 * 32, n0, nt * bn + c0 + 16, p.slot);
             ptx::bulk_commit();
           }
         }
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++iter;
     }
     // partials must be in global memory before the grid completes (the consumer reads them)
-    if (epi.mode == kGemmPartial && ew == 0 && lane == 0) ptx::bulk_wait0();
+    if (epi.mode == kGemmPartial && lane == 0) ptx::bulk_wait0();  // every warp's own stores
     if (st && ew == 0 && lane == 0) st[5] = ptx::globaltimer();
   }
 
@@ -583,7 +586,7 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(plan.n_out), static_cast<cuuint64_t>(plan.t),
                           static_cast<cuuint64_t>(plan.max_pieces)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(plan.n_out) * 4, static_cast<cuuint64_t>(plan.n_out) * plan.t * 4};
-    cuuint32_t box[3] = {static_cast<cuuint32_t>(kBlockM), 16, 1};  // one staging slot
+    cuuint32_t box[3] = {32, 16, 1};  // one epilogue warp's staging slot: 32 features x 16 tokens
     cuuint32_t estr[3] = {1, 1, 1};
     if (fn == nullptr || (plan.n_out * 4) % 16 != 0 ||
         fn(&tm_part, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, epi.part, dims, strides, box, estr,
