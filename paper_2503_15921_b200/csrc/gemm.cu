@@ -199,6 +199,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         prefetched = s;
+        // The next k-blocks of the CTA's weight range go to L2 meanwhile (contiguous per
+        // piece in the tiled layout: one bulk prefetch per piece), so the stream after the
+        // wait starts from L2 instead of HBM (SPIN_GEMM_L2_PREFETCH: blocks per CTA).
+        if (!P2 && epi.l2_prefetch_blocks > 0) {
+          int left = epi.l2_prefetch_blocks;
+          PieceIter pf = it;
+          Piece r;
+          int skip = prefetched;
+          while (left > 0 && pf.next(pm, n_tiles, r)) {
+            const int n = r.kb1 - r.kb0;
+            if (skip >= n) {
+              skip -= n;
+              continue;
+            }
+            const int k0 = r.kb0 + skip, cnt = min(n - skip, left);
+            skip = 0;
+            left -= cnt;
+            const int mt = r.tile / pm.n_ntiles;
+            ptx::bulk_prefetch_l2(w_tiled + (static_cast<size_t>(mt) * pm.kb + k0) * (kBlockM * kBlockK),
+                                  static_cast<uint32_t>(cnt) * kTileABytes);
+          }
+        }
       }
       ptx::grid_dep_wait();
       // Early trigger: the dependent (the reduction / epilogue kernel) launches now and its
@@ -623,6 +645,11 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
     return v ? std::atoi(v) : 0;
   }();
   e.early_trigger = early;
+  static const int l2_pf = [] {
+    const char* v = std::getenv("SPIN_GEMM_L2_PREFETCH");  // A/B switch: k-blocks per CTA
+    return v ? std::atoi(v) : 0;
+  }();
+  e.l2_prefetch_blocks = plan.map.mode == kGemmPartial ? l2_pf : 0;
   return cudaLaunchKernelEx(&cfg, p2 ? gemm_tc_kernel<true> : gemm_tc_kernel<false>,
                             static_cast<const __nv_bfloat16*>(W), tm_x, tm_part, tm_w, plan.map, e, plan.n_out, plan.t,
                             plan.stages);
