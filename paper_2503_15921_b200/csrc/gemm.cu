@@ -191,9 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         PieceIter pre = it;
         Piece q;
         int s = 0;
-        while (s < stages && pre.next(pm, n_tiles, q)) {
+        const int pre_n = min(stages, epi.prewait_stages);
+        while (s < pre_n && pre.next(pm, n_tiles, q)) {
           const int mt = q.tile / pm.n_ntiles;
-          for (int kb = q.kb0; kb < q.kb1 && s < stages; ++kb, ++s) {
+          for (int kb = q.kb0; kb < q.kb1 && s < pre_n; ++kb, ++s) {
             if (leader) ptx::mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
             load_a(s, mt, kb);
           }
@@ -650,6 +651,11 @@ cudaError_t gemm_launch(const GemmPlan& plan, const void* W, const void* X, cons
     return v ? std::atoi(v) : 0;
   }();
   e.l2_prefetch_blocks = plan.map.mode == kGemmPartial ? l2_pf : 0;
+  static const int pre_st = [] {
+    const char* v = std::getenv("SPIN_GEMM_PREWAIT_STAGES");  // A/B switch (default: the whole ring)
+    return v ? std::atoi(v) : (1 << 30);
+  }();
+  e.prewait_stages = pre_st;
   return cudaLaunchKernelEx(&cfg, p2 ? gemm_tc_kernel<true> : gemm_tc_kernel<false>,
                             static_cast<const __nv_bfloat16*>(W), tm_x, tm_part, tm_w, plan.map, e, plan.n_out, plan.t,
                             plan.stages);

@@ -81,7 +81,8 @@ struct GemmEpilogue {
   float* logits = nullptr;   // ARGMAX (optional): [t][n_out]
   unsigned long long* st = nullptr;  // optional timeline stamps [CTA][8] (SPIN_STAMPS)
   int early_trigger = 0;             // PDL trigger right after the dependency wait (set by gemm_launch)
-  int l2_prefetch_blocks = 0;        // weight k-blocks beyond the ring prefetched into L2 before the wait
+  int l2_prefetch_blocks = 0;
+  int prewait_stages = 1 << 30;      // ring stages whose weights are issued before the wait        // weight k-blocks beyond the ring prefetched into L2 before the wait
 };
 
 // Weights are stored TILED: [ceil(N/128)][ceil(K/64)] atoms of 128 x 64 bf16, each a
